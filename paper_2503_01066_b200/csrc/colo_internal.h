@@ -1,0 +1,58 @@
+// colo_internal.h -- host-side internals shared by the colo-b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "colo_abi.h"
+#include "colo_common.cuh"
+
+struct colo_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own = nullptr;     // context-owned compute stream
+    cudaStream_t stream = nullptr;  // current stream (own or caller's)
+    cudaStream_t aux = nullptr;     // second stream for the host-buffer pipelines
+    std::string err;
+    int* d_flag = nullptr;          // device error flag (replay validation)
+    // host-pipeline scratch (lazily grown)
+    void* d_pipe = nullptr;
+    size_t pipe_bytes = 0;
+    uint64_t* d_counters = nullptr; // COLO_NCOUNTERS scratch
+};
+
+struct colo_mapset {
+    int device = 0;
+    colo_model m{};
+    colo_gpu g{};
+    colo_grid grid{};
+    colo_mode mode = COLO_CPA;
+    uint64_t hedge_step = 0, hedge_max = 0, assumed = 128, hash = 0;
+    uint32_t C = 0, I = 0, B = 0, Hc = 0, F = 0;
+    uint8_t* d_off = nullptr;   // C*I*B offload codes
+    uint8_t* d_hed = nullptr;   // Hc*F hedge bits
+    uint32_t* d_tab = nullptr;  // (C+1)*(I+1) trace-fused verdict table (hedge_step == cached_step only)
+    uint32_t* d_str = nullptr;  // C+1 stream bits per cached bucket
+    bool fast = false;
+};
+
+namespace colo {
+
+colo_status set_err(colo_ctx* ctx, colo_status st, const std::string& what);
+colo_status cuda_err(colo_ctx* ctx, cudaError_t e, const char* where);
+MapView make_view(const colo_mapset* ms);
+colo_status check_grid_limits(const colo_grid* g);
+colo_status check_model_limits(const colo_model* m);
+// correctly rounded (sum * 2^-96) / n from a 192-bit little-endian fixed-point sum
+double fixed_mean(const uint64_t sum[3], uint64_t n);
+void fixed_add(uint64_t acc[3], const uint64_t v[3]);
+
+}  // namespace colo
+
+#define COLO_CK(ctx, call)                                          \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return colo::cuda_err(ctx, e_, #call); \
+    } while (0)
