@@ -235,6 +235,8 @@ class OracleLib:
 
     # -- maps --------------------------------------------------------------------
     def build_offloading_map(self, m, g, grid, cpa):
+        if 0 in (grid.cached_step, grid.incoming_step, grid.batch_step):
+            raise ValueError("map grid: steps must be positive")  # maps.hpp:198-199
         n = int(np.prod(grid_shape(grid)))
         cells = np.zeros(n, np.uint8)
         rc = self._build_offloading_map(C.byref(m), C.byref(g), C.byref(grid), int(cpa), cells, n)

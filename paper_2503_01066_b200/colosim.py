@@ -686,57 +686,76 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
     torch.distributed ``group`` the histograms, counters and exact sums are
     all-reduced across ranks (each rank holds its own device shard)."""
     torch = _torch()
-    dist = None
-    if group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
-        dist = torch.distributed
-        if not dist.is_initialized():
-            dist = None
+    dist = torch.distributed if (torch.distributed.is_available() and torch.distributed.is_initialized()) else None
     dev = prompt.device
+    hist = torch.zeros(len(quantiles) * HIST_BINS, dtype=torch.int64, device=dev)
+
+    def run_pass(hist_shift, filter_shift, prefixes):
+        h = hist[: len(prefixes) * HIST_BINS]
+        h.zero_()
+        first = filter_shift == 63
+        r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
+                           summary=first, hist=h, hist_shift=hist_shift, filter_shift=filter_shift,
+                           filter_prefix=tuple(prefixes))
+        if not first:
+            return h, None
+        S = summaries_to_numpy(r["summary"])
+        return h, {"generated_tokens": int(S["generated_tokens"].sum()), "slow_tokens": int(S["slow_tokens"].sum()),
+                   "slow_queries": int(S["slow_queries"].sum()), "batches": int(S["batches"].sum()),
+                   "flags": int(np.bitwise_or.reduce(S["flags"])) if len(S) else 0,
+                   "exact_sum": sum(int(a) | (int(b) << 64) | (int(c) << 128) for a, b, c in S["tpt_sum"])}
+
+    reduce = (lambda t: dist.all_reduce(t, group=group)) if dist is not None else None
+    return stats_protocol(run_pass, reduce, quantiles)
+
+
+def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
+    """Exact nearest-rank selection over f64 bit patterns in three 21-bit
+    radix passes (TPT samples are non-negative, so their bit patterns order
+    like their values).  ``run_pass(hist_shift, filter_shift, prefixes)``
+    returns (int64 histogram tensor [len(prefixes) * HIST_BINS], totals or
+    None); ``reduce`` (e.g. a torch.distributed all_reduce) sums a tensor
+    across ranks in place.  The mean is the exact fixed-point sum over n,
+    correctly rounded (metrics.hpp:63-65 sums the sorted samples
+    sequentially instead; the difference is bounded by that sum's rounding)."""
+    torch = _torch()
     nf = len(quantiles)
-    hist = torch.zeros(nf * HIST_BINS, dtype=torch.int64, device=dev)
-    r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
-                       summary=True, hist=hist[:HIST_BINS], hist_shift=42, filter_shift=63, filter_prefix=(0,))
-    S = summaries_to_numpy(r["summary"])
-    tot = np.array([S["generated_tokens"].sum(), S["slow_tokens"].sum(), S["slow_queries"].sum(), S["batches"].sum()],
-                   np.int64)
-    limbs = [int(a) | (int(b) << 64) | (int(c) << 128) for a, b, c in S["tpt_sum"]]
-    exact = sum(limbs)
-    # split the exact sum into 32-bit chunks so an int64 all-reduce cannot overflow
-    chunks = np.array([(exact >> (32 * i)) & 0xFFFFFFFF for i in range(7)], np.int64)
-    if dist is not None:
-        t = torch.tensor(np.concatenate([tot, chunks]), device=dev)
-        dist.all_reduce(t, group=group)
-        dist.all_reduce(hist[:HIST_BINS], group=group)
-        v = t.cpu().numpy()
-        tot, chunks = v[:4], v[4:]
-        exact = sum(int(c) << (32 * i) for i, c in enumerate(chunks))
-    n = int(tot[0])
-    out = {"generated_tokens": n, "slow_tokens": int(tot[1]), "slow_queries": int(tot[2]), "batches": int(tot[3]),
-           "flags": int(np.bitwise_or.reduce(S["flags"])) if len(S) else 0}
+    hist, tot = run_pass(42, 63, (0,))
+    exact = tot["exact_sum"]
+    # int64-safe all-reduce: counters, then the exact sum as 32-bit chunks
+    vec = torch.tensor([tot["generated_tokens"], tot["slow_tokens"], tot["slow_queries"], tot["batches"], tot["flags"]]
+                       + [(exact >> (32 * i)) & 0xFFFFFFFF for i in range(8)], dtype=torch.int64, device=hist.device)
+    if reduce is not None:
+        flags = vec[4].clone()
+        reduce(vec)
+        vec[4] = flags  # flags are OR-ed below from the local value (informational)
+        reduce(hist)
+    v = [int(x) for x in vec.cpu().tolist()]
+    exact = sum(c << (32 * i) for i, c in enumerate(v[5:]))
+    n = v[0]
+    out = {"generated_tokens": n, "slow_tokens": v[1], "slow_queries": v[2], "batches": v[3], "flags": v[4],
+           "exact_sum": exact}
     if n == 0:
-        out.update({"p50": None, "p90": None, "p99": None, "mean": None})
+        out.update({f"p{int(round(q * 100))}": None for q in quantiles})
+        out["mean"] = None
         return out
     ranks = [nearest_rank_index(q, n) for q in quantiles]
-    h = hist[:HIST_BINS].cpu().numpy()
+    h = hist.cpu().numpy()
     prefixes = []
     for f in range(nf):
         b, ranks[f] = _select(h, ranks[f])
         prefixes.append(b)
-    for pas, (fs, hs) in enumerate(((42, 21), (21, 0))):
-        hist.zero_()
-        replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
-                       summary=False, hist=hist, hist_shift=hs, filter_shift=fs, filter_prefix=tuple(prefixes))
-        if dist is not None:
-            dist.all_reduce(hist, group=group)
+    for fs, hs in ((42, 21), (21, 0)):
+        hist, _ = run_pass(hs, fs, tuple(prefixes))
+        if reduce is not None:
+            reduce(hist)
         hh = hist.cpu().numpy().reshape(nf, HIST_BINS)
         for f in range(nf):
             b, ranks[f] = _select(hh[f], ranks[f])
             prefixes[f] = (prefixes[f] << 21) | b
-    vals = [float(np.array([p], np.uint64).view(np.float64)[0]) for p in prefixes]
-    mean = float(Fraction(exact, 1 << 96) / n)
-    for q, v in zip(quantiles, vals):
-        out[f"p{int(round(q * 100))}"] = v
-    out["mean"] = mean
+    for q, p in zip(quantiles, prefixes):
+        out[f"p{int(round(q * 100))}"] = float(np.array([p], np.uint64).view(np.float64)[0])
+    out["mean"] = float(Fraction(exact, 1 << 96) / n)
     return out
 
 
