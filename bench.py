@@ -1,0 +1,331 @@
+"""Benchmark: per-query admission decisions/s on the C2 workload (BASELINE.json
+configs[1]): a 64-device synthetic trace set of 100M queries per GPU, trace-
+fused feature extraction + offload/hedge decision (colo_features_decide).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N>1).  Weak scaling: every rank owns its own
+64 devices x 1,562,500 queries; there is no data-path collective, only the
+final all-reduce of the decision counters (NCCL).  A step is one pass of the
+hot path over the rank's 100M queries (one kernel launch).  Inputs are 1.2 GB
+per step (> 126 MB L2), so no L2 flush is needed between steps.
+
+`value` is device-timed (CUDA events on the launching stream, max over ranks);
+`e2e` is the same metric through the reference-facing host-buffer C-ABI call
+(colo_features_decide_host: pinned host buffers, H2D + kernel + D2H inside the
+timed region, host wall clock, max over ranks).  `--impl reference` times the
+reference's own code (oracle/_ref: the unchanged colosim headers compiled by
+oracle/Makefile) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-I/O admission decisions/sec per GPU (1/2/4/8 B200); % HBM roofline"
+UNIT = "decisions/s"
+DEVICES, PER_DEVICE = 64, 1_562_500
+QPS = [0.05, 0.1, 0.2, 0.3]
+BYTES_PER_DECISION = 12  # prompt u32 + output u32 read, verdict u32 written
+
+
+def dev_set_of(d: int) -> int:
+    """llama8b even / phi14b odd devices; CPA for d%4<2 else CPT.
+    Map-set order: 0 llama CPA, 1 llama CPT, 2 phi CPA, 3 phi CPT."""
+    return (d % 2) * 2 + (0 if d % 4 < 2 else 1)
+
+
+def config(n_gpus: int) -> dict:
+    return {
+        "workload": "C2: 64-device synthetic trace set, 100M queries per GPU, trace-fused features + offload/hedge decision",
+        "devices_per_gpu": DEVICES,
+        "queries_per_gpu": DEVICES * PER_DEVICE,
+        "profiles": "llama8b (even devices) / phi14b (odd); CPA for d%4<2 else CPT; default 500/500/5 grid",
+        "decision_rule": "cached=charged(prev query of device), incoming=p+o, batch=1, pending=0, dev_layers=L (SURVEY §8(d) C2)",
+        "l2": "inputs 1.2 GB/step > 126 MB L2; no flush",
+        "parallelism": f"dp{n_gpus} (devices sharded by GPU, no data-path collective)",
+    }
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def ncu_traffic() -> float | None:
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("k_fused", {}).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
+class ClockSampler:
+    """Polls SM clock and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def report(self) -> dict:
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_trace(seed: int):
+    """Host-side synthetic C2 trace for the reference arm (numpy RNG: prompts from
+    the ShareGPT-like histogram, output 128 -- workload.hpp:214)."""
+    values = np.array([64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096], np.uint32)
+    probs = np.array([0.05, 0.10, 0.15, 0.15, 0.13, 0.12, 0.10, 0.08, 0.06, 0.04, 0.02])
+    rng = np.random.default_rng(seed)
+    n = DEVICES * PER_DEVICE
+    prompt = values[rng.choice(len(values), size=n, p=probs)]
+    output = np.full(n, 128, np.uint32)
+    offs = (np.arange(DEVICES + 1, dtype=np.uint64) * PER_DEVICE).astype(np.uint64)
+    return prompt, output, offs
+
+
+def reference_decide(prompt, output, offs, devices, threads):
+    """The reference's own composition over its own OffloadingMap/HedgingMap
+    (oracle/_ref, ref_features_decide), one device per task, all host threads."""
+    from oracle.oracle import OracleLib, default_gpu, default_grid, default_model, phi14b_model
+
+    ref = OracleLib("ref")
+    g = default_gpu()
+    sets = [(default_model(), g, 1), (default_model(), g, 0), (phi14b_model(), g, 1), (phi14b_model(), g, 0)]
+    grid = default_grid()
+
+    def one(d):
+        lo, hi = int(offs[d]), int(offs[d + 1])
+        m, gg, cpa = sets[dev_set_of(d)]
+        ref.features_decide([(m, gg, cpa)], grid, prompt[lo:hi], output[lo:hi], np.array([0, hi - lo], np.uint64),
+                            np.zeros(1, np.uint16))
+        return hi - lo
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        n = sum(ex.map(one, devices))
+    return n, time.perf_counter() - t0
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    prompt, output, offs = host_trace(1234)
+    sample_devices = list(range(8))  # bounded sample: 8 of the 64 devices (12.5M queries) per step
+    for _ in range(args.warmup):
+        reference_decide(prompt, output, offs, sample_devices, threads)
+    tot_n, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        n, t = reference_decide(prompt, output, offs, sample_devices, threads)
+        tot_n += n
+        tot_t += t
+    value = tot_n / tot_t
+    sample = f"8 of 64 C2 devices (12.5M queries, both profiles and modes) per step, {threads} host threads, oracle/_ref"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config(args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_leg(prompt_h, output_h, offs_h):
+    threads = os.cpu_count() or 1
+    devices = list(range(DEVICES))
+    reference_decide(prompt_h, output_h, offs_h, devices[:1], threads)  # warm
+    n, t = reference_decide(prompt_h, output_h, offs_h, devices, threads)
+    return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"the same GPU-generated C2 arrays, all 64 devices ({n} queries), {threads} host threads, "
+                      f"oracle/_ref (reference headers compiled unchanged), {t:.2f} s"}
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    from paper_2503_01066_b200 import colosim as cs
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = cs.Context(local)
+    stream = torch.cuda.current_stream()
+    g = cs.GpuProfile()
+    sets = [cs.MapSet.build(ctx, m, g, mode=md) for m in (cs.ModelProfile(), cs.ModelProfile.phi14b_like())
+            for md in (cs.TrainingMode.CPA, cs.TrainingMode.CPT)]
+    arrival, prompt, output, offs = cs.synth_trace(ctx, [PER_DEVICE] * DEVICES,
+                                                   [QPS[d % 4] for d in range(DEVICES)], 1234 + 7919 * rank)
+    del arrival
+    dset = torch.tensor([dev_set_of(d) for d in range(DEVICES)], dtype=torch.int16, device="cuda")
+    n = DEVICES * PER_DEVICE
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def step():
+        cs.features_decide(ctx, sets, prompt, output, offs, dset, out=out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * n * args.steps / (ms_max / 1e3)
+    per_launch_s = ms / 1e3 / args.steps
+    achieved = BYTES_PER_DECISION * n / per_launch_s / 1e9
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+
+    # decision counters once, then the one NCCL stats reduction
+    cs.features_decide(ctx, sets, prompt, output, offs, dset, out=out, counters=counters)
+    if dist:
+        dist.all_reduce(counters)
+    cnt = dict(zip(cs.COUNTER_NAMES, [int(x) for x in counters.cpu().tolist()]))
+
+    # e2e: the reference-facing host-buffer call, H2D + kernel + D2H per step
+    hp = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    ho = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hv = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    hp.copy_(prompt)
+    ho.copy_(output)
+    offs_h = offs.cpu().numpy().astype(np.uint64)
+    dset_h = dset.cpu().numpy().astype(np.uint16)
+    e2e_steps = max(1, min(args.steps, 10))
+    cs.features_decide_host(ctx, sets, hp, ho, offs_h, dset_h, out=hv)  # warm (pipeline buffers)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        cs.features_decide_host(ctx, sets, hp, ho, offs_h, dset_h, out=hv)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * n * e2e_steps / float(te.item())
+    assert torch.equal(hv.cuda(), out), "host-buffer path disagrees with the device path"
+
+    line = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config(world),
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": ncu_traffic(),
+                             "kernel": "k_fused<FAST> (colo_features_decide)",
+                             "bytes_per_decision": BYTES_PER_DECISION,
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
+                        "d2h_bytes_per_step": 4 * n * world, "steps": e2e_steps,
+                        "api": "colo_features_decide_host (pinned host buffers, wall clock)"},
+                "gpu_launches": args.steps, "clocks": clk.report(), "counters": cnt}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline_leg(hp.numpy().view(np.uint32), ho.numpy().view(np.uint32), offs_h)
+            except Exception as e:  # oracle/_ref missing on this box
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

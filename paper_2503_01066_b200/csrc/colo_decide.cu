@@ -1,0 +1,624 @@
+// colo_decide.cu -- the admission decision kernels (K1+K2) and their launchers.
+//
+//   k_decide        tuple stream: one 16-B colo_tuple -> one u32 verdict
+//   k_decide_exact  tuple stream, un-quantised (offload_cell_decision + direct hedge)
+//   k_fused_fast    trace SoA -> features -> verdict through the per-set
+//                   (cached bucket x incoming bucket) verdict table in smem
+//   k_fused_gen     same through compose() (hedge grid != offload grid, or
+//                   tables too large for shared memory)
+//
+// All three decision paths evaluate the same function (colo_common.cuh
+// compose(), engine.hpp:513-557 + 437-444); tests/test_gpu_parity.py holds
+// each of them to the CPU oracle and the reference's golden vectors.
+// Reference paths are relative to /root/reference/proj/.
+#include <algorithm>
+#include <cstring>
+
+#include "colo_internal.h"
+
+using namespace colo;
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr unsigned FULL = 0xffffffffu;
+
+int blocks_for(colo_ctx* ctx, const void* fn, int threads, size_t smem) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * ctx->sm_count;
+}
+
+colo_status check_align(colo_ctx* ctx, const void* p) {
+    if (reinterpret_cast<uintptr_t>(p) & 15u) return set_err(ctx, COLO_EINVAL, "device buffers must be 16-byte aligned");
+    return COLO_OK;
+}
+
+// --------------------------------------------------------------- tuple path
+// compose() specialised to 32-bit tuple fields and written branch-free:
+// every lookup index is clamped into range and the out-of-range cases are
+// selected afterwards, so a warp never diverges on the data.
+__device__ __forceinline__ uint32_t compose32(const MapView& mv, const uint8_t* off, const uint8_t* hed, uint32_t c,
+                                              uint32_t inc, uint32_t b, uint32_t pend, uint32_t dev) {
+    // OffloadingMap::lookup nullopt (maps.hpp:105-107)
+    const bool oor = (c > mv.max_c) | (inc > mv.max_i) | (b > mv.max_b) | (inc == 0) | (b == 0);
+    const uint32_t ci = ceil_div(mv.fc, min(c, mv.max_c));
+    const uint32_t ii = ceil_div(mv.fi, max(min(inc, mv.max_i), 1u)) - 1;
+    const uint32_t bi = ceil_div(mv.fb, max(min(b, mv.max_b), 1u)) - 1;
+    uint32_t code = off[(ci * mv.I + ii) * mv.B + bi];
+    code = oor ? 1u : code;                                   // engine.hpp:517-521
+    const bool a2h = code == 1;
+    const uint32_t layers = code >= 2 ? code - 2 : 0u;
+    const uint32_t free_now = a2h ? dev : min(layers, dev);   // engine.hpp:524-527
+    const uint32_t total = min(pend + (a2h ? mv.L : layers), mv.L);  // engine.hpp:528-530
+    // HedgingMap::lookup nullopt (maps.hpp:277-278); forced Recompute on offload fallback
+    const bool hoor = (c == 0) | (c > mv.hmax);
+    const uint32_t hi = mv.hsame ? ci - 1 : ceil_div(mv.fh, min(max(c, 1u), mv.hmax)) - 1;
+    const uint32_t hbit = hed[(oor | hoor) ? 0u : hi * (mv.L + 1) + total];
+    const uint32_t recompute = (oor | hoor) ? 1u : hbit;
+    const uint32_t v = (a2h ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS) | (layers << 2) | (free_now << 10) |
+                       (recompute << 18) | (oor ? COLO_V_OFFLOAD_OOR : 0u) | ((!oor & hoor) ? COLO_V_HEDGE_OOR : 0u) |
+                       ((recompute ? COLO_VD_RECOMPUTE_DROP : COLO_VD_FREE_LOADBACK) << 21);
+    return code == 0 ? 0u : v;                                // NoAction -> ADMIT (engine.hpp:522)
+}
+
+// admit_to_store's streaming pre-commitment, lookup(charged, 1, 1) (engine.hpp:437-444)
+__device__ __forceinline__ uint32_t stream32(const MapView& mv, const uint8_t* off, uint32_t ch) {
+    const bool oor = ch > mv.max_c;
+    const uint32_t code = off[ceil_div(mv.fc, min(ch, mv.max_c)) * mv.I * mv.B];
+    return oor ? (COLO_V_STREAM | COLO_V_STREAM_OOR) : (code == 1 ? COLO_V_STREAM : 0u);
+}
+
+struct DecideParams {
+    MapView mv;
+    const uint4* in;
+    uint32_t* out;
+    uint64_t n;
+    uint64_t* counters;
+};
+
+template <bool SMEM, bool COUNT>
+__global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ DecideParams P) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const MapView mv = P.mv;  // by value: the fields live in registers / uniform registers
+    const uint8_t* off = mv.off;
+    const uint8_t* hed = mv.hed;
+    if (SMEM) {
+        const uint32_t ob = (mv.off_bytes + 15u) & ~15u;
+        for (uint32_t i = threadIdx.x; i < mv.off_bytes; i += blockDim.x) sm[i] = mv.off[i];
+        for (uint32_t i = threadIdx.x; i < mv.hed_bytes; i += blockDim.x) sm[ob + i] = mv.hed[i];
+        __syncthreads();
+        off = sm;
+        hed = sm + ob;
+    }
+    uint64_t cnt[COLO_NCOUNTERS];
+    if (COUNT)
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    constexpr int U = 4;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < P.n; base += stride * U) {
+        uint4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * stride;
+            t[u] = i < P.n ? __ldcs(P.in + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * stride;
+            const uint32_t v = compose32(mv, off, hed, t[u].x, t[u].y, t[u].w & 0xffffu, (t[u].w >> 16) & 0xffu,
+                                         t[u].w >> 24) |
+                               stream32(mv, off, t[u].z);
+            if (i < P.n) {
+                __stcs(P.out + i, v);
+                if (COUNT) count_verdict(v, cnt);
+            }
+        }
+    }
+    if (COUNT) flush_counters(cnt, P.counters);
+}
+
+struct ExactParams {
+    colo_model m;
+    colo_gpu g;
+    uint64_t budget, assumed;
+    uint32_t cpa;
+    const uint4* in;
+    uint32_t* out;
+    uint64_t n;
+    uint64_t* counters;
+};
+
+// Exact per-query verdicts: offload_cell_decision (maps.hpp:215-231) at the
+// raw point + the hedge inequality (maps.hpp:341-356, 380) evaluated directly.
+template <bool COUNT>
+__global__ void __launch_bounds__(kThreads) k_decide_exact(const __grid_constant__ ExactParams P) {
+    uint64_t cnt[COLO_NCOUNTERS];
+    if (COUNT)
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+    const colo_model m = P.m;
+    const colo_gpu g = P.g;
+    const uint32_t L = static_cast<uint32_t>(m.num_layers);
+    const bool cpa = P.cpa != 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 t = __ldcs(P.in + i);
+        const uint32_t cached = t.x, incoming = t.y, charged = t.z;
+        const uint32_t batch = t.w & 0xffffu, pending = (t.w >> 16) & 0xffu, dev = t.w >> 24;
+        const uint32_t fallback = incoming == 0 || batch == 0;
+        const uint32_t code = fallback ? 1u : offload_cell_code(m, P.budget, cpa, cached, incoming, batch);
+        uint32_t v;
+        if (code == 0) {
+            v = 0;
+        } else {
+            const uint32_t layers = code >= 2 ? code - 2 : 0;
+            const uint32_t free_now = code == 1 ? dev : min(layers, dev);
+            const uint32_t total = min(pending + (code == 1 ? L : layers), L);
+            uint32_t recompute = 1, hedge_oor = 0;
+            if (!fallback) {
+                if (cached == 0) {
+                    hedge_oor = 1;
+                } else {
+                    const double rc = hedge_recompute_time(m, cpa, cached, P.assumed);
+                    const double res = hedge_residual_load_time(m, g, cached, total);
+                    recompute = res > rc;
+                }
+            }
+            v = pack_verdict(code == 1 ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS, layers, free_now, recompute, fallback,
+                             hedge_oor, recompute ? COLO_VD_RECOMPUTE_DROP : COLO_VD_FREE_LOADBACK);
+        }
+        if (offload_cell_code(m, P.budget, cpa, charged, 1, 1) == 1) v |= COLO_V_STREAM;
+        __stcs(P.out + i, v);
+        if (COUNT) count_verdict(v, cnt);
+    }
+    if (COUNT) flush_counters(cnt, P.counters);
+}
+
+// --------------------------------------------------------------- fused path
+struct FusedParams {
+    MapView sets[kMaxSets];
+    uint32_t tab_off[kMaxSets];
+    uint32_t str_off[kMaxSets];
+    uint32_t nsets, smem_words;
+    const uint32_t* prompt;
+    const uint32_t* output;
+    uint32_t* out;
+    const uint64_t* dev_off;
+    const uint16_t* dev_set;
+    uint32_t ndev;
+    uint32_t prev_p, prev_o;  // element base-1 (host pipeline chunks)
+    uint64_t base, n;
+    uint64_t* counters;
+};
+
+// largest d with dev_off[d] <= g (dev_off[0] == 0)
+__device__ __forceinline__ uint32_t find_dev(const uint64_t* __restrict__ off, uint32_t ndev, uint64_t g) {
+    uint32_t lo = 0, hi = ndev;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// The map-set parameters the fast path needs, held in registers per warp.
+struct SetRegs {
+    uint32_t max_c, max_i, C, I, W, cpa, tab, str;
+    FastDiv fc, fi;
+};
+
+__device__ __forceinline__ SetRegs load_set(const FusedParams& P, uint32_t s) {
+    const MapView& mv = P.sets[s];
+    SetRegs r;
+    r.max_c = mv.max_c;
+    r.max_i = mv.max_i;
+    r.C = mv.C;
+    r.I = mv.I;
+    r.W = mv.I + 1;
+    r.cpa = mv.cpa;
+    r.tab = P.tab_off[s];
+    r.str = P.str_off[s];
+    r.fc = mv.fc;
+    r.fi = mv.fi;
+    return r;
+}
+
+// cached-axis bucket of x tokens (row C = out of range), maps.hpp:102-108
+__device__ __forceinline__ uint32_t bucket_c(const SetRegs& r, uint64_t x) {
+    return x > r.max_c ? r.C : ceil_div(r.fc, static_cast<uint32_t>(x));
+}
+
+// incoming-axis bucket (column I = out of range or zero), maps.hpp:103-108
+__device__ __forceinline__ uint32_t bucket_i(const SetRegs& r, uint64_t inc) {
+    return (inc > r.max_i || inc == 0) ? r.I : ceil_div(r.fi, static_cast<uint32_t>(inc)) - 1;
+}
+
+constexpr uint32_t kChunk = 256;  // queries per warp step: 8 consecutive per lane
+
+// Per-element path for chunks that straddle a device boundary or the array
+// end: per-element device lookup, previous query read back from memory.
+template <bool FAST, bool COUNT>
+__device__ __forceinline__ void fused_slow(const FusedParams& P, const uint32_t* smw, uint64_t cs, uint64_t ce,
+                                           uint32_t lane, uint64_t (&cnt)[COLO_NCOUNTERS]) {
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint64_t i = cs + lane * 8 + k;
+        if (i >= ce) break;
+        const uint64_t g = P.base + i;
+        const uint32_t dd = find_dev(P.dev_off, P.ndev, g);
+        const uint32_t ss = __ldg(P.dev_set + dd);
+        const MapView& mv = P.sets[ss];
+        uint64_t pc = 0;
+        if (g != __ldg(P.dev_off + dd)) {
+            const uint32_t pp = i ? __ldg(P.prompt + i - 1) : P.prev_p;
+            const uint32_t po = i ? __ldg(P.output + i - 1) : P.prev_o;
+            pc = charged_tokens(pp, po, mv.cpa);
+        }
+        const uint32_t p = __ldg(P.prompt + i), o = __ldg(P.output + i);
+        const uint64_t ch = charged_tokens(p, o, mv.cpa);
+        const uint64_t inc = static_cast<uint64_t>(p) + o;
+        uint32_t v;
+        if (FAST) {
+            const SetRegs r = load_set(P, ss);
+            v = smw[r.tab + bucket_c(r, pc) * r.W + bucket_i(r, inc)] | smw[r.str + bucket_c(r, ch)];
+        } else {
+            v = compose(mv, mv.off, mv.hed, pc, inc, 1, 0, mv.L) | stream_bits(mv, mv.off, ch);
+        }
+        P.out[i] = v;
+        if (COUNT) count_verdict(v, cnt);
+    }
+}
+
+// Trace-fused features -> verdict through the per-set verdict table.
+// Each warp owns a contiguous run of 256-query chunks (lane = 8 consecutive
+// queries = two LDG.128 per column); the next chunk's loads are issued before
+// the current chunk is evaluated, and the device, its map-set parameters and
+// the previous query's cached bucket ride along in registers.
+template <bool COUNT>
+__global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__ FusedParams P) {
+    extern __shared__ __align__(16) uint32_t smw[];
+    for (uint32_t s = 0; s < P.nsets; ++s) {
+        const MapView& mv = P.sets[s];
+        const uint32_t nt = (mv.C + 1) * (mv.I + 1);
+        for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) smw[P.tab_off[s] + i] = mv.tab[i];
+        for (uint32_t i = threadIdx.x; i <= mv.C; i += blockDim.x) smw[P.str_off[s] + i] = mv.str[i];
+    }
+    __syncthreads();
+    uint64_t cnt[COLO_NCOUNTERS];
+    if (COUNT)
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t nchunks = (P.n + kChunk - 1) / kChunk;
+    const uint64_t per = (nchunks + nwarps - 1) / nwarps;
+    const uint64_t c0 = gwarp * per, c1 = min(c0 + per, nchunks);
+    if (c0 < c1) {
+        const uint64_t i_begin = c0 * kChunk, i_end = min(P.n, c1 * kChunk);
+        const uint64_t g0 = P.base + i_begin;
+        uint32_t d = find_dev(P.dev_off, P.ndev, g0);
+        uint64_t hi = __ldg(P.dev_off + d + 1);
+        SetRegs R = load_set(P, __ldg(P.dev_set + d));
+        uint32_t prev_b = 0;  // cached bucket of the previous query (0 = nothing cached)
+        if (g0 != __ldg(P.dev_off + d)) {
+            const uint32_t pp = i_begin ? __ldg(P.prompt + i_begin - 1) : P.prev_p;
+            const uint32_t po = i_begin ? __ldg(P.output + i_begin - 1) : P.prev_o;
+            prev_b = bucket_c(R, charged_tokens(pp, po, R.cpa));
+        }
+        const uint4* p4 = reinterpret_cast<const uint4*>(P.prompt);
+        const uint4* o4 = reinterpret_cast<const uint4*>(P.output);
+        uint4 cp0, cp1, co0, co1;
+        if (i_begin + kChunk <= i_end) {
+            const uint64_t q = (i_begin + lane * 8) >> 2;
+            cp0 = __ldcs(p4 + q);
+            cp1 = __ldcs(p4 + q + 1);
+            co0 = __ldcs(o4 + q);
+            co1 = __ldcs(o4 + q + 1);
+        }
+        for (uint64_t cs = i_begin; cs < i_end; cs += kChunk) {
+            const uint64_t ce = min(cs + kChunk, i_end);
+            uint4 np0, np1, no0, no1;
+            if (cs + 2 * kChunk <= i_end) {  // prefetch the next full chunk
+                const uint64_t q = (cs + kChunk + lane * 8) >> 2;
+                np0 = __ldcs(p4 + q);
+                np1 = __ldcs(p4 + q + 1);
+                no0 = __ldcs(o4 + q);
+                no1 = __ldcs(o4 + q + 1);
+            }
+            if (ce - cs == kChunk && P.base + ce <= hi) {
+                const uint32_t pv[8] = {cp0.x, cp0.y, cp0.z, cp0.w, cp1.x, cp1.y, cp1.z, cp1.w};
+                const uint32_t ov[8] = {co0.x, co0.y, co0.z, co0.w, co1.x, co1.y, co1.z, co1.w};
+                uint32_t cb[8], ib[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    cb[k] = bucket_c(R, charged_tokens(pv[k], ov[k], R.cpa));
+                    ib[k] = bucket_i(R, static_cast<uint64_t>(pv[k]) + ov[k]);
+                }
+                const uint32_t up = __shfl_up_sync(FULL, cb[7], 1);
+                uint32_t pb = lane == 0 ? prev_b : up;
+                uint32_t v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[k] = smw[R.tab + pb * R.W + ib[k]] | smw[R.str + cb[k]];
+                    pb = cb[k];
+                }
+                uint4* dst = reinterpret_cast<uint4*>(P.out + cs + lane * 8);
+                __stcs(dst, make_uint4(v[0], v[1], v[2], v[3]));
+                __stcs(dst + 1, make_uint4(v[4], v[5], v[6], v[7]));
+                if (COUNT)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) count_verdict(v[k], cnt);
+                prev_b = __shfl_sync(FULL, cb[7], 31);
+            } else {
+                fused_slow<true, COUNT>(P, smw, cs, ce, lane, cnt);
+                if (ce < i_end) {  // re-seat the warp state on the device of the next query
+                    d = find_dev(P.dev_off, P.ndev, P.base + ce);
+                    hi = __ldg(P.dev_off + d + 1);
+                    R = load_set(P, __ldg(P.dev_set + d));
+                    prev_b = 0;
+                    if (P.base + ce != __ldg(P.dev_off + d))
+                        prev_b = bucket_c(R, charged_tokens(__ldg(P.prompt + ce - 1), __ldg(P.output + ce - 1), R.cpa));
+                }
+            }
+            cp0 = np0;
+            cp1 = np1;
+            co0 = no0;
+            co1 = no1;
+        }
+    }
+    if (COUNT) flush_counters(cnt, P.counters);
+}
+
+// General trace-fused path: compose() per query from the cell tables.
+template <bool COUNT>
+__global__ void __launch_bounds__(kThreads) k_fused_gen(const __grid_constant__ FusedParams P) {
+    uint64_t cnt[COLO_NCOUNTERS];
+    if (COUNT)
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t nchunks = (P.n + kChunk - 1) / kChunk;
+    for (uint64_t c = gwarp; c < nchunks; c += nwarps)
+        fused_slow<false, COUNT>(P, nullptr, c * kChunk, min((c + 1) * kChunk, P.n), lane, cnt);
+    if (COUNT) flush_counters(cnt, P.counters);
+}
+
+colo_status launch_fused(colo_ctx* ctx, cudaStream_t stream, const colo_mapset* const* sets, size_t nsets,
+                         const uint32_t* d_prompt, const uint32_t* d_output, uint64_t base, size_t n,
+                         const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev, uint32_t* d_out,
+                         uint64_t* d_counters, uint32_t prev_p, uint32_t prev_o) {
+    FusedParams P{};
+    bool fast = true;
+    uint32_t words = 0;
+    for (size_t s = 0; s < nsets; ++s) {
+        P.sets[s] = make_view(sets[s]);
+        fast = fast && sets[s]->fast;
+        P.tab_off[s] = words;
+        words += (sets[s]->C + 1) * (sets[s]->I + 1);
+        P.str_off[s] = words;
+        words += sets[s]->C + 1;
+    }
+    size_t smem = static_cast<size_t>(words) * 4;
+    if (!fast || smem > 160 * 1024) {
+        fast = false;
+        smem = 0;
+    }
+    P.nsets = static_cast<uint32_t>(nsets);
+    P.smem_words = words;
+    P.prompt = d_prompt;
+    P.output = d_output;
+    P.out = d_out;
+    P.dev_off = d_dev_offsets;
+    P.dev_set = d_dev_set;
+    P.ndev = static_cast<uint32_t>(ndev);
+    P.prev_p = prev_p;
+    P.prev_o = prev_o;
+    P.base = base;
+    P.n = n;
+    P.counters = d_counters;
+    const void* fn;
+    if (fast) fn = d_counters ? (const void*)k_fused_fast<true> : (const void*)k_fused_fast<false>;
+    else fn = d_counters ? (const void*)k_fused_gen<true> : (const void*)k_fused_gen<false>;
+    if (smem > 48 * 1024) COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int blocks = blocks_for(ctx, fn, kThreads, smem);
+    const uint64_t need_blocks = (n + kChunk * (kThreads / 32) - 1) / (kChunk * (kThreads / 32));
+    if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(std::max<uint64_t>(need_blocks, 1));
+    void* args[] = {&P};
+    COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, smem, stream));
+    return COLO_OK;
+}
+
+colo_status check_sets(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets) {
+    if (!sets || nsets == 0 || nsets > kMaxSets) return set_err(ctx, COLO_EINVAL, "need 1..16 map sets");
+    for (size_t s = 0; s < nsets; ++s)
+        if (!sets[s]) return set_err(ctx, COLO_EINVAL, "null map set");
+    return COLO_OK;
+}
+
+colo_status grow_pipe(colo_ctx* ctx, size_t bytes) {
+    if (ctx->pipe_bytes >= bytes) return COLO_OK;
+    if (ctx->d_pipe) cudaFree(ctx->d_pipe);
+    ctx->d_pipe = nullptr;
+    ctx->pipe_bytes = 0;
+    COLO_CK(ctx, cudaMalloc(&ctx->d_pipe, bytes));
+    ctx->pipe_bytes = bytes;
+    return COLO_OK;
+}
+
+colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset* ms, const colo_tuple* d_in, size_t n,
+                          uint32_t* d_out, uint64_t* d_counters) {
+    DecideParams P{};
+    P.mv = make_view(ms);
+    P.in = reinterpret_cast<const uint4*>(d_in);
+    P.out = d_out;
+    P.n = n;
+    P.counters = d_counters;
+    const size_t smem = ((P.mv.off_bytes + 15u) & ~15u) + P.mv.hed_bytes;
+    const bool use_smem = smem <= 96 * 1024;
+    const void* fn;
+    if (use_smem) fn = d_counters ? (const void*)k_decide<true, true> : (const void*)k_decide<true, false>;
+    else fn = d_counters ? (const void*)k_decide<false, true> : (const void*)k_decide<false, false>;
+    const size_t dyn = use_smem ? smem : 0;
+    if (dyn > 48 * 1024) COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int blocks = blocks_for(ctx, fn, kThreads, dyn);
+    const uint64_t need_blocks = (n + kThreads - 1) / kThreads;
+    if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+    void* args[] = {&P};
+    COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, stream));
+    return COLO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+colo_status colo_decide(colo_ctx* ctx, const colo_mapset* ms, const colo_tuple* d_in, size_t n, uint32_t* d_out,
+                        uint64_t* d_counters) {
+    if (!ctx || !ms || (n && (!d_in || !d_out))) return COLO_EINVAL;
+    if (n == 0) return COLO_OK;
+    const colo_status st = check_align(ctx, d_in);
+    if (st != COLO_OK) return st;
+    return launch_decide(ctx, ctx->stream, ms, d_in, n, d_out, d_counters);
+}
+
+colo_status colo_decide_exact(colo_ctx* ctx, const colo_model* m, const colo_gpu* g, colo_mode mode, uint64_t assumed,
+                              const colo_tuple* d_in, size_t n, uint32_t* d_out, uint64_t* d_counters) {
+    if (!ctx || !m || !g || (n && (!d_in || !d_out))) return COLO_EINVAL;
+    colo_status st = colo_validate_profile_pair(m, g);
+    if (st != COLO_OK) return set_err(ctx, st, "profile pair rejected (profiles.hpp:129-134)");
+    if (check_model_limits(m) != COLO_OK) return set_err(ctx, COLO_EINVAL, "num_layers > 253");
+    if (n == 0) return COLO_OK;
+    st = check_align(ctx, d_in);
+    if (st != COLO_OK) return st;
+    ExactParams P{};
+    P.m = *m;
+    P.g = *g;
+    P.budget = g->capacity_bytes - g->runtime_reserve_bytes - m->weights_bytes;
+    P.assumed = assumed;
+    P.cpa = mode == COLO_CPA;
+    P.in = reinterpret_cast<const uint4*>(d_in);
+    P.out = d_out;
+    P.n = n;
+    P.counters = d_counters;
+    const void* fn = d_counters ? (const void*)k_decide_exact<true> : (const void*)k_decide_exact<false>;
+    int blocks = blocks_for(ctx, fn, kThreads, 0);
+    const uint64_t need_blocks = (n + kThreads - 1) / kThreads;
+    if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+    void* args[] = {&P};
+    COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, 0, ctx->stream));
+    return COLO_OK;
+}
+
+colo_status colo_features_decide(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets, const uint32_t* d_prompt,
+                                 const uint32_t* d_output, size_t n, const uint64_t* d_dev_offsets,
+                                 const uint16_t* d_dev_set, size_t ndev, uint32_t* d_out, uint64_t* d_counters) {
+    if (!ctx || ndev == 0 || !d_dev_offsets || !d_dev_set) return COLO_EINVAL;
+    const colo_status st = check_sets(ctx, sets, nsets);
+    if (st != COLO_OK) return st;
+    if (n == 0) return COLO_OK;
+    if (check_align(ctx, d_prompt) || check_align(ctx, d_output) || check_align(ctx, d_out)) return COLO_EINVAL;
+    return launch_fused(ctx, ctx->stream, sets, nsets, d_prompt, d_output, 0, n, d_dev_offsets, d_dev_set, ndev, d_out,
+                        d_counters, 0, 0);
+}
+
+colo_status colo_features_decide_host(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets,
+                                      const uint32_t* h_prompt, const uint32_t* h_output, size_t n,
+                                      const uint64_t* h_dev_offsets, const uint16_t* h_dev_set, size_t ndev,
+                                      uint32_t* h_out, uint64_t* h_counters) {
+    if (!ctx || ndev == 0 || !h_dev_offsets || !h_dev_set || (n && (!h_prompt || !h_output || !h_out)))
+        return COLO_EINVAL;
+    colo_status st = check_sets(ctx, sets, nsets);
+    if (st != COLO_OK) return st;
+    if (h_dev_offsets[0] != 0 || h_dev_offsets[ndev] != n) return set_err(ctx, COLO_EINVAL, "device offsets must span [0, n]");
+    for (size_t d = 0; d < ndev; ++d) {
+        if (h_dev_offsets[d + 1] < h_dev_offsets[d]) return set_err(ctx, COLO_EINVAL, "device offsets not monotone");
+        if (h_dev_set[d] >= nsets) return set_err(ctx, COLO_EINVAL, "device map-set index out of range");
+    }
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    const size_t CH = size_t(1) << 24;  // queries per pipeline chunk
+    const size_t chunk_bytes = CH * 12;
+    const size_t meta = ((ndev + 1) * 8 + ndev * 2 + 255) & ~size_t(255);
+    st = grow_pipe(ctx, 2 * chunk_bytes + meta);
+    if (st != COLO_OK) return st;
+    auto* base = static_cast<uint8_t*>(ctx->d_pipe);
+    auto* d_off = reinterpret_cast<uint64_t*>(base + 2 * chunk_bytes);
+    auto* d_set = reinterpret_cast<uint16_t*>(base + 2 * chunk_bytes + (ndev + 1) * 8);
+    cudaStream_t ss[2] = {ctx->stream, ctx->aux};
+    COLO_CK(ctx, cudaMemcpyAsync(d_off, h_dev_offsets, (ndev + 1) * 8, cudaMemcpyHostToDevice, ss[0]));
+    COLO_CK(ctx, cudaMemcpyAsync(d_set, h_dev_set, ndev * 2, cudaMemcpyHostToDevice, ss[0]));
+    uint64_t* d_cnt = h_counters ? ctx->d_counters : nullptr;
+    if (d_cnt) COLO_CK(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(uint64_t) * COLO_NCOUNTERS, ss[0]));
+    cudaEvent_t ready;
+    COLO_CK(ctx, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    COLO_CK(ctx, cudaEventRecord(ready, ss[0]));
+    COLO_CK(ctx, cudaStreamWaitEvent(ss[1], ready, 0));
+    cudaEventDestroy(ready);
+    for (size_t c0 = 0, k = 0; c0 < n; c0 += CH, ++k) {
+        const size_t len = std::min(CH, n - c0);
+        cudaStream_t s = ss[k & 1];
+        auto* buf = base + (k & 1) * chunk_bytes;
+        auto* dp = reinterpret_cast<uint32_t*>(buf);
+        auto* dq = reinterpret_cast<uint32_t*>(buf + CH * 4);
+        auto* dv = reinterpret_cast<uint32_t*>(buf + CH * 8);
+        COLO_CK(ctx, cudaMemcpyAsync(dp, h_prompt + c0, len * 4, cudaMemcpyHostToDevice, s));
+        COLO_CK(ctx, cudaMemcpyAsync(dq, h_output + c0, len * 4, cudaMemcpyHostToDevice, s));
+        st = launch_fused(ctx, s, sets, nsets, dp, dq, c0, len, d_off, d_set, ndev, dv, d_cnt,
+                          c0 ? h_prompt[c0 - 1] : 0, c0 ? h_output[c0 - 1] : 0);
+        if (st != COLO_OK) return st;
+        COLO_CK(ctx, cudaMemcpyAsync(h_out + c0, dv, len * 4, cudaMemcpyDeviceToHost, s));
+    }
+    COLO_CK(ctx, cudaStreamSynchronize(ss[1]));
+    COLO_CK(ctx, cudaStreamSynchronize(ss[0]));
+    if (h_counters) {
+        uint64_t tmp[COLO_NCOUNTERS];
+        COLO_CK(ctx, cudaMemcpy(tmp, d_cnt, sizeof tmp, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < COLO_NCOUNTERS; ++i) h_counters[i] += tmp[i];
+    }
+    return COLO_OK;
+}
+
+colo_status colo_decide_host(colo_ctx* ctx, const colo_mapset* ms, const colo_tuple* h_in, size_t n, uint32_t* h_out,
+                             uint64_t* h_counters) {
+    if (!ctx || !ms || (n && (!h_in || !h_out))) return COLO_EINVAL;
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    const size_t CH = size_t(1) << 23;
+    const size_t chunk_bytes = CH * 20;
+    colo_status st = grow_pipe(ctx, 2 * chunk_bytes);
+    if (st != COLO_OK) return st;
+    auto* base = static_cast<uint8_t*>(ctx->d_pipe);
+    cudaStream_t ss[2] = {ctx->stream, ctx->aux};
+    uint64_t* d_cnt = h_counters ? ctx->d_counters : nullptr;
+    cudaEvent_t ready;
+    COLO_CK(ctx, cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    if (d_cnt) COLO_CK(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(uint64_t) * COLO_NCOUNTERS, ss[0]));
+    COLO_CK(ctx, cudaEventRecord(ready, ss[0]));
+    COLO_CK(ctx, cudaStreamWaitEvent(ss[1], ready, 0));
+    cudaEventDestroy(ready);
+    for (size_t c0 = 0, k = 0; c0 < n; c0 += CH, ++k) {
+        const size_t len = std::min(CH, n - c0);
+        cudaStream_t s = ss[k & 1];
+        auto* buf = base + (k & 1) * chunk_bytes;
+        auto* din = reinterpret_cast<colo_tuple*>(buf);
+        auto* dout = reinterpret_cast<uint32_t*>(buf + CH * 16);
+        COLO_CK(ctx, cudaMemcpyAsync(din, h_in + c0, len * 16, cudaMemcpyHostToDevice, s));
+        st = launch_decide(ctx, s, ms, din, len, dout, d_cnt);
+        if (st != COLO_OK) return st;
+        COLO_CK(ctx, cudaMemcpyAsync(h_out + c0, dout, len * 4, cudaMemcpyDeviceToHost, s));
+    }
+    COLO_CK(ctx, cudaStreamSynchronize(ss[1]));
+    COLO_CK(ctx, cudaStreamSynchronize(ss[0]));
+    if (h_counters) {
+        uint64_t tmp[COLO_NCOUNTERS];
+        COLO_CK(ctx, cudaMemcpy(tmp, d_cnt, sizeof tmp, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < COLO_NCOUNTERS; ++i) h_counters[i] += tmp[i];
+    }
+    return COLO_OK;
+}
+
+}  // extern "C"
