@@ -8,7 +8,7 @@ HDR := include/colo_abi.h $(PKG)/csrc/colo_common.cuh $(PKG)/csrc/colo_internal.
 # -fmad=false: no FMA contraction anywhere (bit-exact f64 vs the x86 reference)
 NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Iinclude -Xcompiler -fPIC,-O2 -Xptxas -v
 
-all: $(PKG)/libcolo_b200.so oracle
+all: $(PKG)/libcolo_b200.so oracle dropin
 
 $(PKG)/libcolo_b200.so: $(SRC) $(HDR)
 	@mkdir -p build
@@ -21,3 +21,17 @@ clean:
 	rm -f $(PKG)/libcolo_b200.so
 
 .PHONY: all oracle clean
+
+# C++ drop-in parity program: the unchanged reference headers + colosim_gpu.hpp
+# (build-time dependency on /root/reference; the binary travels to the GPU box)
+REF ?= /root/reference/proj
+JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+dropin: build/dropin_parity
+
+build/dropin_parity: tests/cpp/dropin_parity.cpp $(PKG)/cpp/colosim_gpu.hpp include/colo_abi.h $(PKG)/libcolo_b200.so
+	@if [ -d "$(REF)/include/colosim" ]; then mkdir -p build && \
+	  g++ -std=c++20 -O2 -ffp-contract=off -I$(REF)/include -I$(JSON_DIR) -Iinclude -I$(PKG)/cpp \
+	    -o $@ tests/cpp/dropin_parity.cpp -L$(PKG) -lcolo_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
+	else echo "dropin: $(REF) absent, keeping prebuilt build/dropin_parity"; fi
+
+.PHONY: dropin

@@ -198,6 +198,32 @@ __device__ __forceinline__ void count_verdict(uint32_t v, uint64_t (&c)[COLO_NCO
     c[COLO_CNT_TOTAL] += 1;
 }
 
+// Warp-aggregated counting: one ballot + popc per category per warp-wide
+// verdict slot (all lanes hold the same running totals).  `valid` masks lanes
+// without an element.  Totals are per warp, so u32 suffices below 2^32
+// elements per warp.
+__device__ __forceinline__ void count_warp(uint32_t v, bool valid, uint32_t (&c)[COLO_NCOUNTERS]) {
+    const uint32_t vd = COLO_V_VERDICT(v);
+    c[COLO_CNT_ADMIT] += __popc(__ballot_sync(0xffffffffu, valid && vd == COLO_VD_ADMIT));
+    c[COLO_CNT_FREE_LOADBACK] += __popc(__ballot_sync(0xffffffffu, valid && vd == COLO_VD_FREE_LOADBACK));
+    c[COLO_CNT_RECOMPUTE_DROP] += __popc(__ballot_sync(0xffffffffu, valid && vd == COLO_VD_RECOMPUTE_DROP));
+    c[COLO_CNT_OFFLOAD_OOR] += __popc(__ballot_sync(0xffffffffu, valid && (v & COLO_V_OFFLOAD_OOR)));
+    c[COLO_CNT_HEDGE_OOR] += __popc(__ballot_sync(0xffffffffu, valid && (v & COLO_V_HEDGE_OOR)));
+    c[COLO_CNT_STREAM] += __popc(__ballot_sync(0xffffffffu, valid && (v & COLO_V_STREAM)));
+    c[COLO_CNT_STREAM_OOR] += __popc(__ballot_sync(0xffffffffu, valid && (v & COLO_V_STREAM_OOR)));
+    c[COLO_CNT_TOTAL] += __popc(__ballot_sync(0xffffffffu, valid));
+}
+
+__device__ __forceinline__ void flush_warp_counters(const uint32_t (&c)[COLO_NCOUNTERS], uint64_t* d_counters) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (lane < COLO_NCOUNTERS) {
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) mine = lane == static_cast<uint32_t>(k) ? c[k] : mine;
+        if (mine) atomicAdd(reinterpret_cast<unsigned long long*>(&d_counters[lane]), static_cast<unsigned long long>(mine));
+    }
+}
+
 __device__ __forceinline__ void flush_counters(uint64_t (&c)[COLO_NCOUNTERS], uint64_t* d_counters) {
 #pragma unroll
     for (int k = 0; k < COLO_NCOUNTERS; ++k) {

@@ -92,13 +92,13 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
         off = sm;
         hed = sm + ob;
     }
-    uint64_t cnt[COLO_NCOUNTERS];
-    if (COUNT)
-#pragma unroll
-        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+    uint32_t cnt[COLO_NCOUNTERS] = {};
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    constexpr int U = 4;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < P.n; base += stride * U) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    constexpr int U = 8;
+    // the trip count is warp-uniform (it depends on the warp's first lane only)
+    const uint64_t wbase = tid & ~uint64_t(31);
+    for (uint64_t base = tid, wb = wbase; wb < P.n; base += stride * U, wb += stride * U) {
         uint4 t[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -111,13 +111,11 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
             const uint32_t v = compose32(mv, off, hed, t[u].x, t[u].y, t[u].w & 0xffffu, (t[u].w >> 16) & 0xffu,
                                          t[u].w >> 24) |
                                stream32(mv, off, t[u].z);
-            if (i < P.n) {
-                __stcs(P.out + i, v);
-                if (COUNT) count_verdict(v, cnt);
-            }
+            if (i < P.n) __stcs(P.out + i, v);
+            if (COUNT) count_warp(v, i < P.n, cnt);
         }
     }
-    if (COUNT) flush_counters(cnt, P.counters);
+    if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
 struct ExactParams {
@@ -242,32 +240,34 @@ constexpr uint32_t kChunk = 256;  // queries per warp step: 8 consecutive per la
 // end: per-element device lookup, previous query read back from memory.
 template <bool FAST, bool COUNT>
 __device__ __forceinline__ void fused_slow(const FusedParams& P, const uint32_t* smw, uint64_t cs, uint64_t ce,
-                                           uint32_t lane, uint64_t (&cnt)[COLO_NCOUNTERS]) {
-    for (uint32_t k = 0; k < 8; ++k) {
+                                           uint32_t lane, uint32_t (&cnt)[COLO_NCOUNTERS]) {
+    for (uint32_t k = 0; k < 8; ++k) {  // warp-uniform trip count (ballot counting)
         const uint64_t i = cs + lane * 8 + k;
-        if (i >= ce) break;
-        const uint64_t g = P.base + i;
-        const uint32_t dd = find_dev(P.dev_off, P.ndev, g);
-        const uint32_t ss = __ldg(P.dev_set + dd);
-        const MapView& mv = P.sets[ss];
-        uint64_t pc = 0;
-        if (g != __ldg(P.dev_off + dd)) {
-            const uint32_t pp = i ? __ldg(P.prompt + i - 1) : P.prev_p;
-            const uint32_t po = i ? __ldg(P.output + i - 1) : P.prev_o;
-            pc = charged_tokens(pp, po, mv.cpa);
+        const bool valid = i < ce;
+        uint32_t v = 0;
+        if (valid) {
+            const uint64_t g = P.base + i;
+            const uint32_t dd = find_dev(P.dev_off, P.ndev, g);
+            const uint32_t ss = __ldg(P.dev_set + dd);
+            const MapView& mv = P.sets[ss];
+            uint64_t pc = 0;
+            if (g != __ldg(P.dev_off + dd)) {
+                const uint32_t pp = i ? __ldg(P.prompt + i - 1) : P.prev_p;
+                const uint32_t po = i ? __ldg(P.output + i - 1) : P.prev_o;
+                pc = charged_tokens(pp, po, mv.cpa);
+            }
+            const uint32_t p = __ldg(P.prompt + i), o = __ldg(P.output + i);
+            const uint64_t ch = charged_tokens(p, o, mv.cpa);
+            const uint64_t inc = static_cast<uint64_t>(p) + o;
+            if (FAST) {
+                const SetRegs r = load_set(P, ss);
+                v = smw[r.tab + bucket_c(r, pc) * r.W + bucket_i(r, inc)] | smw[r.str + bucket_c(r, ch)];
+            } else {
+                v = compose(mv, mv.off, mv.hed, pc, inc, 1, 0, mv.L) | stream_bits(mv, mv.off, ch);
+            }
+            P.out[i] = v;
         }
-        const uint32_t p = __ldg(P.prompt + i), o = __ldg(P.output + i);
-        const uint64_t ch = charged_tokens(p, o, mv.cpa);
-        const uint64_t inc = static_cast<uint64_t>(p) + o;
-        uint32_t v;
-        if (FAST) {
-            const SetRegs r = load_set(P, ss);
-            v = smw[r.tab + bucket_c(r, pc) * r.W + bucket_i(r, inc)] | smw[r.str + bucket_c(r, ch)];
-        } else {
-            v = compose(mv, mv.off, mv.hed, pc, inc, 1, 0, mv.L) | stream_bits(mv, mv.off, ch);
-        }
-        P.out[i] = v;
-        if (COUNT) count_verdict(v, cnt);
+        if (COUNT) count_warp(v, valid, cnt);
     }
 }
 
@@ -286,11 +286,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
         for (uint32_t i = threadIdx.x; i <= mv.C; i += blockDim.x) smw[P.str_off[s] + i] = mv.str[i];
     }
     __syncthreads();
-    uint64_t cnt[COLO_NCOUNTERS];
-    if (COUNT)
-#pragma unroll
-        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
-
+    uint32_t cnt[COLO_NCOUNTERS] = {};
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -351,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
                 __stcs(dst + 1, make_uint4(v[4], v[5], v[6], v[7]));
                 if (COUNT)
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) count_verdict(v[k], cnt);
+                    for (int k = 0; k < 8; ++k) count_warp(v[k], true, cnt);
                 prev_b = __shfl_sync(FULL, cb[7], 31);
             } else {
                 fused_slow<true, COUNT>(P, smw, cs, ce, lane, cnt);
@@ -370,23 +366,20 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
             co1 = no1;
         }
     }
-    if (COUNT) flush_counters(cnt, P.counters);
+    if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
 // General trace-fused path: compose() per query from the cell tables.
 template <bool COUNT>
 __global__ void __launch_bounds__(kThreads) k_fused_gen(const __grid_constant__ FusedParams P) {
-    uint64_t cnt[COLO_NCOUNTERS];
-    if (COUNT)
-#pragma unroll
-        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
+    uint32_t cnt[COLO_NCOUNTERS] = {};
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
     const uint64_t nchunks = (P.n + kChunk - 1) / kChunk;
     for (uint64_t c = gwarp; c < nchunks; c += nwarps)
         fused_slow<false, COUNT>(P, nullptr, c * kChunk, min((c + 1) * kChunk, P.n), lane, cnt);
-    if (COUNT) flush_counters(cnt, P.counters);
+    if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
 colo_status launch_fused(colo_ctx* ctx, cudaStream_t stream, const colo_mapset* const* sets, size_t nsets,

@@ -1,0 +1,133 @@
+// dropin_parity.cpp -- the drop-in, exercised from C++: code written against
+// the unchanged colosim headers (/root/reference/proj/include) hands its own
+// ModelProfile / GpuProfile / GridSteps / GridBounds objects to colosim_gpu
+// (paper_2503_01066_b200/cpp/colosim_gpu.hpp) and must get the reference's
+// answers back, bit for bit.  Built by `make dropin` (needs /root/reference at
+// build time only); run by tests/test_gpu_dropin.py on the GPU box.
+#include <cstdio>
+#include <cstring>
+#include <random>
+
+#include "colosim/engine.hpp"
+#include "colosim/experiment.hpp"
+#include "colosim_gpu.hpp"
+
+using namespace colosim;
+
+static int failures = 0;
+#define EXPECT(cond, ...)                      \
+    do {                                       \
+        if (!(cond)) {                         \
+            std::printf("FAIL: " __VA_ARGS__); \
+            std::printf("\n");                 \
+            ++failures;                        \
+        }                                      \
+    } while (0)
+
+// engine.hpp:513-557 + 437-444 with the reference's own lookups
+static uint32_t reference_verdict(const BuiltMaps& mp, uint64_t L, const colo_tuple& t) {
+    auto dec = mp.offload.lookup(t.cached, t.incoming, t.batch);
+    bool fallback = !dec;
+    if (fallback) dec = OffloadDecision{OffloadAction::AllToHost, 0};
+    uint32_t v = 0;
+    if (dec->action != OffloadAction::NoAction) {
+        uint64_t free_now = dec->action == OffloadAction::AllToHost ? t.dev_layers
+                                                                    : std::min<uint64_t>(dec->layers, t.dev_layers);
+        uint64_t total = std::min<uint64_t>(t.pending + dec->layers_to_free(L), L);
+        bool recompute = true, hoor = false;
+        if (!fallback) {
+            auto h = mp.hedge.lookup(t.cached, total);
+            if (h) recompute = *h == HedgeDecision::Recompute;
+            else hoor = true;
+        }
+        uint32_t action = dec->action == OffloadAction::AllToHost ? 2 : 1;
+        v = action | uint32_t((dec->action == OffloadAction::FreeLayers ? dec->layers : 0) << 2) |
+            uint32_t(free_now << 10) | (recompute ? 1u << 18 : 0) | (fallback ? 1u << 19 : 0) | (hoor ? 1u << 20 : 0) |
+            ((recompute ? 2u : 1u) << 21);
+    }
+    auto s = mp.offload.lookup(t.charged, 1, 1);
+    if (!s) v |= (1u << 23) | (1u << 24);
+    else if (s->action == OffloadAction::AllToHost) v |= 1u << 23;
+    return v;
+}
+
+int main() {
+    colosim_gpu::Context ctx(0);
+    const GpuProfile gpu;
+    for (ModelProfile model : {ModelProfile{}, ModelProfile::phi14b_like()}) {
+        for (TrainingMode mode : {TrainingMode::CPA, TrainingMode::CPT}) {
+            BuiltMaps ref = build_maps(model, gpu, GridSteps{}, GridBounds{}, mode);
+            std::unique_ptr<colosim_gpu::GpuMaps> g(
+                colosim_gpu::build_maps(ctx, model, gpu, GridSteps{}, GridBounds{}, mode == TrainingMode::CPA));
+            EXPECT(g->profile_hash_value() == profile_hash(model, gpu), "profile hash");
+            // every lookup the reference grid can answer, plus out-of-range probes
+            for (uint64_t c = 0; c <= 8600; c += 97)
+                for (uint64_t i = 0; i <= 8600; i += 131)
+                    for (uint64_t b = 0; b <= 55; b += 3) {
+                        auto r = ref.offload.lookup(c, i, b);
+                        auto q = g->offload_lookup(c, i, b);
+                        EXPECT(r.has_value() == q.has_value(), "offload nullopt (%lu,%lu,%lu)", c, i, b);
+                        if (r && q)
+                            EXPECT(int(r->action) == int(q->action) && r->layers == q->layers,
+                                   "offload cell (%lu,%lu,%lu)", c, i, b);
+                    }
+            for (uint64_t c = 0; c <= 8600; c += 50)
+                for (uint64_t f = 0; f <= model.num_layers + 1; ++f) {
+                    auto r = ref.hedge.lookup(c, f);
+                    auto q = g->hedge_lookup(c, f);
+                    EXPECT(r.has_value() == q.has_value(), "hedge nullopt");
+                    if (r && q) EXPECT((*r == HedgeDecision::Recompute) == *q, "hedge cell (%lu,%lu)", c, f);
+                }
+            std::mt19937_64 rng(42);
+            std::vector<colo_tuple> tuples(2000000);
+            for (auto& t : tuples) {
+                t.cached = uint32_t(rng() % 9000);
+                t.incoming = uint32_t(rng() % 9000);
+                t.charged = uint32_t(rng() % 9500);
+                t.batch = uint16_t(rng() % 60);
+                t.pending = uint8_t(rng() % (model.num_layers + 4));
+                t.dev_layers = uint8_t(rng() % (model.num_layers + 4));
+            }
+            uint64_t cnt[COLO_NCOUNTERS] = {};
+            std::vector<uint32_t> v = g->decide(tuples, cnt);
+            size_t bad = 0;
+            for (size_t k = 0; k < tuples.size(); ++k) bad += v[k] != reference_verdict(ref, model.num_layers, tuples[k]);
+            EXPECT(bad == 0, "%zu of %zu verdicts differ", bad, tuples.size());
+            EXPECT(cnt[COLO_CNT_TOTAL] == tuples.size(), "counter total");
+        }
+        // serving replay: Simulation::run(ServingOnly) vs the GPU replay, sample for sample
+        LengthDistribution lengths = LengthDistribution::uniform(100, 4000);
+        for (double qps : {0.05, 0.4, 1.7}) {
+            Trace trace = generate_trace(qps, 1500.0, lengths, std::nullopt, 17);
+            SimConfig cfg;
+            cfg.mode = SimMode::ServingOnly;
+            cfg.model = model;
+            cfg.gpu = gpu;
+            cfg.trace = trace;
+            MetricsReport rep = run_simulation(cfg);
+            std::vector<double> a;
+            std::vector<uint32_t> p, o;
+            for (const auto& r : trace.records) {
+                a.push_back(r.arrival_time);
+                p.push_back(uint32_t(r.prompt_tokens));
+                o.push_back(uint32_t(r.output_tokens));
+            }
+            auto g = colosim_gpu::replay_serving(ctx, model, gpu, a, p, o, 0.05);
+            EXPECT(g.tpt_samples.size() == rep.tpt_samples.size(), "sample count qps %.2f", qps);
+            EXPECT(std::memcmp(g.tpt_samples.data(), rep.tpt_samples.data(), 8 * rep.tpt_samples.size()) == 0,
+                   "TPT samples differ at qps %.2f", qps);
+            EXPECT(g.summary.peak_device_bytes == rep.peak_device_bytes, "peak bytes");
+            EXPECT(g.summary.generated_tokens == rep.generated_tokens, "generated tokens");
+        }
+    }
+    // the reference's error contract through the shim
+    try {
+        GpuProfile tiny;
+        tiny.capacity_bytes = kGiB;
+        colosim_gpu::build_maps(ctx, ModelProfile{}, tiny, GridSteps{}, GridBounds{}, true);
+        EXPECT(false, "tiny gpu accepted");
+    } catch (const std::runtime_error&) {
+    }
+    std::printf("%s: dropin parity, %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
+    return failures ? 1 : 0;
+}
