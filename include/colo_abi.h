@@ -275,11 +275,19 @@ typedef struct colo_replay_opts {
     uint32_t nfilters;                /* 0..3 */
     uint32_t hist_shift;
     uint32_t filter_shift;            /* 63 with prefix 0 selects every sample */
-    uint32_t pad;
+    uint32_t segment_len;             /* queries per replay segment (0 = automatic), see below */
     uint64_t filter_prefix[3];
 } colo_replay_opts;
 
-/* Serving-only replay of every device's trace segment, one device per warp.
+/* Serving-only replay of every device's trace.  Each device is cut into
+ * segments of segment_len queries; the replay runs in three passes:
+ * speculate (every segment in parallel, from an idle server at its first
+ * query), resolve (per device, in order: a segment whose true entry state is
+ * not "idle at its first query" is replayed until it meets one of the
+ * speculative run's idle batch starts, after which both runs coincide), and
+ * replay (every segment in parallel from its true entry state, writing the
+ * outputs).  Every f64 operation is the reference's, in the reference's
+ * order, so the outputs are identical to a single sequential replay.
  * models/gpus: nprofiles profile pairs; d_dev_profile[ndev] picks one per
  * device.  Rejects (EVALIDATION) traces that are unsorted, have zero
  * prompt/output tokens, or hold a query that cannot fit the device alone

@@ -84,7 +84,7 @@ class ReplayOpts(C.Structure):
         ("nfilters", C.c_uint32),
         ("hist_shift", C.c_uint32),
         ("filter_shift", C.c_uint32),
-        ("pad", C.c_uint32),
+        ("segment_len", C.c_uint32),
         ("filter_prefix", C.c_uint64 * 3),
     ]
 

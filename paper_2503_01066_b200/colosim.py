@@ -607,7 +607,7 @@ def _profiles_arrays(profiles: Sequence[Tuple[ModelProfile, GpuProfile]]):
 def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfile]], arrival, prompt, output,
                    dev_offsets, dev_profile, tau: float = math.inf, sets: Optional[Sequence[MapSet]] = None,
                    samples: bool = False, labels: bool = True, batches: bool = False, summary: bool = True,
-                   hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), sync: bool = True):
+                   hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), segment_len: int = 0):
     """Serving-only replay of every device (engine.hpp:140-387, SimMode::ServingOnly).
     Returns a dict of device tensors: samples (f64, reference order),
     labels (u8 per query), batches (raw bytes, BATCH_DTYPE), summary (DeviceSummary bytes)."""
@@ -623,6 +623,7 @@ def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfi
     res = {}
     opts = _lib.ReplayOpts()
     opts.tau = tau
+    opts.segment_len = segment_len
     keep = []
     if sets is not None:
         arr = _sets_array(sets)

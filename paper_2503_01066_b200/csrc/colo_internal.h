@@ -21,6 +21,8 @@ struct colo_ctx {
     void* d_pipe = nullptr;
     size_t pipe_bytes = 0;
     uint64_t* d_counters = nullptr; // COLO_NCOUNTERS scratch
+    void* d_rscratch = nullptr;     // replay segment state (lazily grown)
+    size_t rscratch_bytes = 0;
 };
 
 struct colo_mapset {

@@ -1,0 +1,814 @@
+// colo_serving.cu -- serving-only replay (K4) and exact tail statistics (K5).
+//
+// The reference's Simulation is strictly sequential per instance
+// (engine.hpp:140-164); instances share no state.  A device
+// trace is therefore cut into segments and replayed in passes so the GPU is
+// not limited to one warp per device:
+//
+//   A  speculate  every segment in parallel, assuming the server is idle when
+//                 the segment's first query arrives; records the exit state
+//                 and the first kRegen idle batch starts ("regeneration
+//                 points": at an idle start the whole replay state is reset to
+//                 (head, T = arrival[head]), so two runs that share one agree
+//                 from there on).
+//   B  resolve    one warp per device walks its segments in order: the true
+//                 entry state of segment k is the exit of k-1; the segment is
+//                 re-run only until the true run reaches an idle start that the
+//                 speculative run also had, then the speculative exit is taken.
+//   C  replay     every segment in parallel from its true entry state, writing
+//                 samples, labels, batch records, histograms and partial sums.
+//   D  finalize   per-device summaries from the segment partials; dense batch
+//                 lists and the replay-derived verdicts.
+//
+// Inside a batch the warp's lanes own decode steps: lane l folds step k0+l's
+// duration over the batch members in batch order (engine.hpp:358-365), then
+// the absolute-time fold now_k = now_{k-1} + d_k runs through the lanes in
+// order via shuffles -- every f64 operation is the reference's, in the
+// reference's order, so all passes reproduce Simulation::run bit for bit.
+// Reference paths are relative to /root/reference/proj/.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "colo_internal.h"
+
+using namespace colo;
+
+namespace {
+
+constexpr int kWarps = 4;    // warps per CTA
+constexpr int kStage = 256;  // batch members staged in shared memory per warp
+constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
+constexpr unsigned FULL = 0xffffffffu;
+
+struct DevProfile {
+    colo_model m;
+    uint64_t budget;  // capacity - reserve - weights, engine.hpp:278-280
+    uint64_t fixed;   // weights + reserve, engine.hpp:141
+};
+
+struct Seg {
+    uint32_t dev, pad;
+    uint64_t start, end;  // device-local query range
+};
+
+struct SpecOut {
+    uint64_t exit_head;
+    double exit_T;
+    uint32_t nregen;
+    uint32_t regen[kRegen + 1];  // device-local offsets from the segment start
+};
+
+struct Entry {
+    uint64_t head;
+    double T;
+};
+
+struct Partial {
+    uint64_t gen, slow_tok, slow_q, nbatch, max_need, maxb;
+    uint64_t acc[3];
+    uint64_t flags;
+    double t_end;
+    uint64_t pad;
+};
+
+struct ReplayParams {
+    DevProfile prof[kMaxSets];
+    MapView sets[kMaxSets];
+    uint32_t nprof, has_sets;
+    const double* arr;
+    const uint32_t* p;
+    const uint32_t* o;
+    const uint64_t* dev_off;
+    const uint16_t* dev_prof;
+    uint32_t ndev, nsegs;
+    const Seg* segs;
+    const uint32_t* dev_seg;  // [ndev+1] first segment of each device
+    SpecOut* spec;
+    Entry* entry;
+    Partial* part;
+    uint64_t* seg_base;       // device-local sample offset at each segment start
+    double tau;
+    double* samples;
+    const uint64_t* sample_off;
+    uint8_t* labels;
+    colo_batch* bstage;       // batch record staged at its first query's global index
+    uint8_t* bflag;
+    colo_batch* batches;
+    colo_device_summary* summary;
+    uint64_t* hist;
+    uint32_t nfilters, hist_shift, filter_shift;
+    uint64_t prefix[3];
+    int* err;
+};
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v = max(v, __shfl_xor_sync(FULL, v, s));
+    return v;
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULL, v, s);
+    return v;
+}
+
+// 192-bit fixed-point accumulation (LSB 2^-96) of s * mult.  flags bit0: a
+// sample below the representable range was truncated; bit1: overflow.
+__device__ __forceinline__ void add3(uint64_t (&a)[3], uint64_t w0, uint64_t w1, uint64_t w2) {
+    const uint64_t t0 = a[0] + w0;
+    const uint64_t c0 = t0 < w0;
+    const uint64_t t1 = a[1] + w1;
+    uint64_t c1 = t1 < w1;
+    const uint64_t t1b = t1 + c0;
+    c1 |= t1b < c0;
+    a[0] = t0;
+    a[1] = t1b;
+    a[2] = a[2] + w2 + c1;
+}
+
+__device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, double s, uint32_t mult) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+    const uint32_t ex = static_cast<uint32_t>(bits >> 52) & 0x7ffu;
+    const uint64_t frac = bits & ((1ull << 52) - 1);
+    if (ex == 0) {
+        if (frac) flags |= 1u;
+        return;
+    }
+    uint64_t m = frac | (1ull << 52);
+    int sh = static_cast<int>(ex) - 1075 + 96;
+    if (sh < 0) {
+        flags |= 1u;
+        if (sh <= -53) return;
+        m >>= -sh;
+        sh = 0;
+    }
+    const uint64_t lo = m * mult, hi = __umul64hi(m, static_cast<uint64_t>(mult));
+    const int q = sh >> 6, r = sh & 63;
+    const uint64_t x0 = lo << r;
+    const uint64_t x1 = r ? ((lo >> (64 - r)) | (hi << r)) : hi;
+    const uint64_t x2 = r ? (hi >> (64 - r)) : 0ull;
+    if (q == 0) {
+        add3(a, x0, x1, x2);
+    } else if (q == 1) {
+        if (x2) flags |= 2u;
+        add3(a, 0, x0, x1);
+    } else if (q == 2) {
+        if (x1 | x2) flags |= 2u;
+        add3(a, 0, 0, x0);
+    } else {
+        flags |= 2u;
+    }
+}
+
+enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
+
+struct Acc {  // per-warp outputs of RUN_FULL (every lane holds its own partials)
+    uint64_t gen = 0, slow_tok = 0, slow_q = 0, nbatch = 0, max_need = 0, maxb = 0;
+    uint64_t acc[3] = {0, 0, 0};
+    uint32_t flags = 0;
+    uint64_t sample_pos = 0;
+};
+
+// Replays whole batches from (head, T) while head < stop (engine.hpp:270-387).
+// SPEC records idle batch starts into *sp; RESOLVE stops (synced = true) at
+// the first idle start that the speculative run *sp also had; FULL writes all
+// outputs.  head/T are updated in place.
+template <int MODE>
+__device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, double& T, uint64_t stop,
+                            uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint32_t* sP, uint32_t* sO) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pi = P.dev_prof[d];
+    const colo_model& m = P.prof[pi].m;
+    const uint64_t budget = P.prof[pi].budget;
+    const uint64_t lo = P.dev_off[d], N = P.dev_off[d + 1] - lo;
+    const double* __restrict__ arr = P.arr + lo;
+    const uint32_t* __restrict__ pp = P.p + lo;
+    const uint32_t* __restrict__ po = P.o + lo;
+    const bool want_hist = MODE == RUN_FULL && P.hist != nullptr;
+    uint64_t tail_ptr = head;
+    uint32_t ridx = 0;
+    const uint32_t nreg = MODE == RUN_RESOLVE ? min(sp->nregen, static_cast<uint32_t>(kRegen)) : 0u;
+    synced = false;
+    while (head < stop && head < N) {
+        // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
+        uint64_t tail;
+        const double ah = arr[head];
+        if (ah > T) {  // idle: the first popped arrival starts a batch alone
+            if (MODE == RUN_SPEC) {
+                if (lane == 0 && ridx < kRegen) sp->regen[ridx] = static_cast<uint32_t>(head - seg_start);
+                ++ridx;
+            }
+            if (MODE == RUN_RESOLVE) {
+                const uint32_t rel = static_cast<uint32_t>(head - seg_start);
+                while (ridx < nreg && sp->regen[ridx] < rel) ++ridx;
+                if (ridx < nreg && sp->regen[ridx] == rel) {
+                    synced = true;  // both runs restart identically from this idle start
+                    return;
+                }
+            }
+            T = ah;
+            tail = head + 1;
+            tail_ptr = head + 1;
+        } else {  // queued: every arrival with time <= T has been popped
+            if (tail_ptr < head) tail_ptr = head;
+            while (tail_ptr < N) {
+                const uint64_t j = tail_ptr + lane;
+                const bool in = j < N && arr[j] <= T;
+                const uint32_t bal = __ballot_sync(FULL, in);
+                if (bal == FULL) {
+                    tail_ptr += 32;
+                    continue;
+                }
+                tail_ptr += __ffs(~bal) - 1;
+                break;
+            }
+            tail = tail_ptr;
+        }
+        // ---- batch formation: FIFO, at least one, sum(need) <= budget (engine.hpp:292-306)
+        uint64_t end = head, need_total = 0, max_inc = 0;
+        uint32_t maxo = 0;
+        while (end < tail) {
+            const uint64_t j = end + lane;
+            const bool valid = j < tail;
+            const uint32_t pj = valid ? pp[j] : 0u, oj = valid ? po[j] : 0u;
+            const uint64_t nd = valid ? serving_memory(m, static_cast<uint64_t>(pj) + oj, 1) : 0ull;
+            uint64_t incl = nd;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint64_t y = __shfl_up_sync(FULL, incl, s);
+                if (lane >= static_cast<uint32_t>(s)) incl += y;
+            }
+            incl += need_total;
+            const bool ok = valid && (j == head || incl <= budget);
+            const uint32_t cnt = __popc(__ballot_sync(FULL, ok));
+            if (ok && j - head < kStage) {
+                sP[j - head] = pj;
+                sO[j - head] = oj;
+            }
+            max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
+            maxo = max(maxo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
+            if (cnt) need_total = __shfl_sync(FULL, incl, cnt - 1);
+            end += cnt;
+            if (cnt < 32) break;
+        }
+        __syncwarp();
+        const uint64_t nb = end - head;
+        auto mem_p = [&](uint64_t j) -> uint32_t { return j < kStage ? sP[j] : pp[head + j]; };
+        auto mem_o = [&](uint64_t j) -> uint32_t { return j < kStage ? sO[j] : po[head + j]; };
+
+        // ---- prefill: left fold in batch order (engine.hpp:321-325) -------------
+        double dur = 0.0;
+        for (uint64_t j = 0; j < nb; ++j) dur += prefill_latency(m, mem_p(j), 1, false);
+        const double start = T + 0.0;  // prefill_start = now_ + stall, stall = 0
+        double now = start + dur;      // PrefillDone time = every member's last_token_time
+
+        // ---- decode steps (engine.hpp:358-387) ---------------------------------
+        uint32_t first_slow = 0xffffffffu;
+        for (uint32_t k0 = 0; k0 < maxo; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            double dk = 0.0;
+            uint32_t alive = 0;
+            if (k < maxo) {
+                for (uint64_t j = 0; j < nb; ++j) {
+                    if (k < mem_o(j)) {
+                        dk += decode_step_latency(m, static_cast<uint64_t>(mem_p(j)) + k, 1, false);
+                        ++alive;
+                    }
+                }
+            }
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                const double dl = __shfl_sync(FULL, dk, l);
+                if (k0 + l < maxo) {
+                    const double nw = now + dl;
+                    if (lane == static_cast<uint32_t>(l)) s = nw - now;  // now - last_token_time
+                    now = nw;
+                }
+            }
+            if (MODE == RUN_FULL) {
+                const bool live = k < maxo;
+                const bool slow = live && s > P.tau;
+                const uint32_t sb = __ballot_sync(FULL, slow);
+                if (sb && first_slow == 0xffffffffu) first_slow = k0 + __ffs(sb) - 1;
+                A.gen += alive;
+                if (slow) A.slow_tok += alive;
+                if (live) {
+                    acc_fixed(A.acc, A.flags, s, alive);
+                    if (want_hist) {
+                        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+                        for (uint32_t f = 0; f < P.nfilters; ++f)
+                            if ((bits >> P.filter_shift) == P.prefix[f])
+                                atomicAdd(reinterpret_cast<unsigned long long*>(
+                                              &P.hist[static_cast<uint64_t>(f) * COLO_HIST_BINS +
+                                                      ((bits >> P.hist_shift) & (COLO_HIST_BINS - 1))]),
+                                          static_cast<unsigned long long>(alive));
+                    }
+                }
+                if (P.samples) {
+                    // samples of step k occupy alive_k consecutive slots, steps in order
+                    uint32_t ex = alive;
+#pragma unroll
+                    for (int sft = 1; sft < 32; sft <<= 1) {
+                        const uint32_t y = __shfl_up_sync(FULL, ex, sft);
+                        if (lane >= static_cast<uint32_t>(sft)) ex += y;
+                    }
+                    const uint32_t total = __shfl_sync(FULL, ex, 31);
+                    const uint64_t pos = A.sample_pos + ex - alive;
+                    for (uint32_t a = 0; a < alive; ++a) P.samples[pos + a] = s;
+                    A.sample_pos += total;
+                }
+            }
+        }
+        if (MODE == RUN_FULL) {
+            // labels: a query is slow iff one of its tokens is (o_j > first slow step)
+            for (uint64_t j = lane; j < nb; j += 32) {
+                const bool slowq = mem_o(j) > first_slow;
+                A.slow_q += slowq;
+                if (P.labels) P.labels[lo + head + j] = slowq ? 1 : 0;
+            }
+            if (lane == 0 && P.bstage) {
+                colo_batch b;
+                b.start = start;
+                b.end = now;
+                b.first = static_cast<uint32_t>(head);
+                b.n = static_cast<uint32_t>(nb);
+                b.need_total = need_total;
+                b.max_incoming = max_inc < 0xffffffffull ? static_cast<uint32_t>(max_inc) : 0xffffffffu;
+                b.verdict = 0;
+                P.bstage[lo + head] = b;
+                P.bflag[lo + head] = 1;
+            }
+            A.max_need = max(A.max_need, need_total);
+            A.maxb = max(A.maxb, nb);
+            ++A.nbatch;
+        }
+        T = now;
+        head = end;
+        __syncwarp();
+    }
+    if (MODE == RUN_SPEC && lane == 0) sp->nregen = ridx;
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_validate(const __grid_constant__ ReplayParams P) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const uint32_t pi = P.dev_prof[sg.dev];
+    const colo_model& m = P.prof[pi].m;
+    const uint64_t lo = P.dev_off[sg.dev];
+    bool bad = false;
+    for (uint64_t j = sg.start + lane; j < sg.end; j += 32) {
+        const uint32_t pj = P.p[lo + j], oj = P.o[lo + j];
+        if (pj == 0 || oj == 0) bad = true;  // workload.hpp:176-181
+        else if (serving_memory(m, static_cast<uint64_t>(pj) + oj, 1) > P.prof[pi].budget) bad = true;  // engine.hpp:70-74
+        if (j > 0 && P.arr[lo + j] < P.arr[lo + j - 1]) bad = true;  // sorted by arrival (workload.hpp:165-169)
+    }
+    if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, 1);
+}
+
+// samples: device-local output-token prefix at each segment start
+__global__ void __launch_bounds__(kWarps * 32) k_seg_sums(const __grid_constant__ ReplayParams P) {
+    const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const uint64_t lo = P.dev_off[sg.dev];
+    uint64_t s = 0;
+    for (uint64_t j = sg.start + lane; j < sg.end; j += 32) s += P.o[lo + j];
+    s = warp_sum_u64(s);
+    if (lane == 0) P.seg_base[w] = s;
+}
+
+__global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= P.ndev) return;
+    uint64_t run = 0;
+    for (uint32_t k = P.dev_seg[d]; k < P.dev_seg[d + 1]; ++k) {
+        const uint64_t s = P.seg_base[k];
+        P.seg_base[k] = run;
+        run += s;
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
+    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    uint64_t head = sg.start;
+    double T = -INFINITY;
+    bool synced;
+    Acc A;
+    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, sp[warp], so[warp]);
+    if ((threadIdx.x & 31) == 0) {
+        P.spec[w].exit_head = head;
+        P.spec[w].exit_T = T;
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__ ReplayParams P) {
+    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t d = blockIdx.x * kWarps + warp;
+    if (d >= P.ndev) return;
+    uint64_t head = 0;
+    double T = -INFINITY;  // server idle before the first arrival (probe B4b)
+    Acc A;
+    for (uint32_t k = P.dev_seg[d]; k < P.dev_seg[d + 1]; ++k) {
+        const Seg sg = P.segs[k];
+        if ((threadIdx.x & 31) == 0) P.entry[k] = Entry{head, T};
+        if (head >= sg.end) continue;  // an earlier batch already covers this segment
+        bool synced;
+        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, sp[warp], so[warp]);
+        if (synced) {
+            head = P.spec[k].exit_head;
+            T = P.spec[k].exit_T;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
+    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const Entry e = P.entry[w];
+    uint64_t head = e.head;
+    double T = e.T;
+    Acc A;
+    if (P.samples) {
+        const uint64_t lo = P.dev_off[sg.dev];
+        uint64_t s = 0;  // output tokens of the queries before the entry head inside this segment
+        for (uint64_t j = sg.start + lane; j < min(head, sg.end); j += 32) s += P.o[lo + j];
+        A.sample_pos = P.sample_off[sg.dev] + P.seg_base[w] + warp_sum_u64(s);
+    }
+    bool synced;
+    if (head < sg.end) run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, sp[warp], so[warp]);
+    const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
+    const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint64_t b0 = __shfl_xor_sync(FULL, A.acc[0], s);
+        const uint64_t b1 = __shfl_xor_sync(FULL, A.acc[1], s);
+        const uint64_t b2 = __shfl_xor_sync(FULL, A.acc[2], s);
+        add3(A.acc, b0, b1, b2);
+    }
+    if (lane == 0) {
+        Partial& q = P.part[w];
+        q.gen = gen;
+        q.slow_tok = slow_tok;
+        q.slow_q = slow_q;
+        q.nbatch = A.nbatch;
+        q.max_need = A.max_need;
+        q.maxb = A.maxb;
+        q.acc[0] = A.acc[0];
+        q.acc[1] = A.acc[1];
+        q.acc[2] = A.acc[2];
+        q.flags = fl;
+        q.t_end = T;
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_finalize(const __grid_constant__ ReplayParams P) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = blockIdx.x * kWarps + warp;
+    if (d >= P.ndev) return;
+    uint64_t gen = 0, slow_tok = 0, slow_q = 0, nbatch = 0, max_need = 0, maxb = 0, fl = 0;
+    uint64_t acc[3] = {0, 0, 0};
+    double t_end = 0.0;
+    const uint64_t N = P.dev_off[d + 1] - P.dev_off[d];
+    for (uint32_t k = P.dev_seg[d] + lane; k < P.dev_seg[d + 1]; k += 32) {
+        const Partial& q = P.part[k];
+        gen += q.gen;
+        slow_tok += q.slow_tok;
+        slow_q += q.slow_q;
+        nbatch += q.nbatch;
+        max_need = max(max_need, q.max_need);
+        maxb = max(maxb, q.maxb);
+        fl |= q.flags;
+        add3(acc, q.acc[0], q.acc[1], q.acc[2]);
+        t_end = fmax(t_end, q.t_end);
+    }
+    gen = warp_sum_u64(gen);
+    slow_tok = warp_sum_u64(slow_tok);
+    slow_q = warp_sum_u64(slow_q);
+    nbatch = warp_sum_u64(nbatch);
+    max_need = warp_max_u64(max_need);
+    maxb = warp_max_u64(maxb);
+    fl = warp_max_u64(fl);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint64_t b0 = __shfl_xor_sync(FULL, acc[0], s);
+        const uint64_t b1 = __shfl_xor_sync(FULL, acc[1], s);
+        const uint64_t b2 = __shfl_xor_sync(FULL, acc[2], s);
+        add3(acc, b0, b1, b2);
+        t_end = fmax(t_end, __shfl_xor_sync(FULL, t_end, s));
+    }
+    if (lane == 0) {
+        colo_device_summary& S = P.summary[d];
+        S.generated_tokens = gen;
+        S.slow_tokens = slow_tok;
+        S.slow_queries = slow_q;
+        S.batches = nbatch;
+        S.peak_device_bytes = P.prof[P.dev_prof[d]].fixed + max_need;  // memory.hpp:28-35 watermark
+        S.max_batch_size = maxb;
+        S.end_time = N ? t_end : 0.0;
+        S.tpt_sum[0] = acc[0];
+        S.tpt_sum[1] = acc[1];
+        S.tpt_sum[2] = acc[2];
+        S.flags = fl;
+    }
+}
+
+// Dense batch list per device + the replay-derived verdicts (SURVEY §8(d) C3
+// rule: cached = charged tokens of the last single-query batch before this
+// one, incoming = max_incoming, batch = n, pending 0, dev_layers L,
+// charged = charged(first query)).
+__global__ void __launch_bounds__(kWarps * 32) k_batches(const __grid_constant__ ReplayParams P) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = blockIdx.x * kWarps + warp;
+    if (d >= P.ndev) return;
+    const uint64_t lo = P.dev_off[d], N = P.dev_off[d + 1] - lo;
+    const uint32_t pi = P.dev_prof[d];
+    uint64_t pos = 0;
+    uint64_t slot = 0;  // carry: charged tokens of the last single-query batch so far
+    for (uint64_t j0 = 0; j0 < N; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        const bool f = j < N && P.bflag[lo + j];
+        const uint32_t bal = __ballot_sync(FULL, f);
+        colo_batch b{};
+        uint64_t ch = 0;
+        bool single = false;
+        if (f) {
+            b = P.bstage[lo + j];
+            if (P.has_sets) ch = charged_tokens(P.p[lo + j], P.o[lo + j], P.sets[pi].cpa);
+            single = b.n == 1;
+        }
+        if (P.has_sets) {
+            const uint32_t sm = __ballot_sync(FULL, single);
+            const uint32_t below = sm & ((1u << lane) - 1u);
+            const uint32_t src = below ? 31 - __clz(below) : 0;
+            const uint64_t from = __shfl_sync(FULL, ch, src);
+            const uint64_t my_slot = below ? from : slot;
+            if (f) {
+                const MapView& mv = P.sets[pi];
+                b.verdict = compose(mv, mv.off, mv.hed, my_slot, b.max_incoming, b.n, 0, mv.L) | stream_bits(mv, mv.off, ch);
+            }
+            if (sm) slot = __shfl_sync(FULL, ch, 31 - __clz(sm));
+        }
+        if (f) P.batches[lo + pos + __popc(bal & ((1u << lane) - 1u))] = b;
+        pos += __popc(bal);
+    }
+}
+
+colo_status grow_rscratch(colo_ctx* ctx, size_t bytes) {
+    if (ctx->rscratch_bytes >= bytes) return COLO_OK;
+    if (ctx->d_rscratch) cudaFree(ctx->d_rscratch);
+    ctx->d_rscratch = nullptr;
+    ctx->rscratch_bytes = 0;
+    COLO_CK(ctx, cudaMalloc(&ctx->d_rscratch, bytes));
+    ctx->rscratch_bytes = bytes;
+    return COLO_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+extern "C" {
+
+colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const colo_gpu* gpus, size_t nprofiles,
+                                const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
+                                const uint64_t* d_dev_offsets, const uint16_t* d_dev_profile, size_t ndev,
+                                const colo_replay_opts* opts) {
+    if (!ctx || !models || !gpus || !opts || nprofiles == 0 || nprofiles > kMaxSets || !d_dev_offsets ||
+        !d_dev_profile)
+        return COLO_EINVAL;
+    if (ndev == 0) return COLO_OK;
+    if (n && (!d_arrival || !d_prompt || !d_output)) return COLO_EINVAL;
+    if (opts->d_samples && !opts->d_sample_offsets) return set_err(ctx, COLO_EINVAL, "samples need d_sample_offsets");
+    if (opts->d_hist && (opts->nfilters == 0 || opts->nfilters > 3)) return set_err(ctx, COLO_EINVAL, "nfilters 1..3");
+    ReplayParams P{};
+    for (size_t i = 0; i < nprofiles; ++i) {
+        const colo_status st = colo_validate_profile_pair(&models[i], &gpus[i]);
+        if (st != COLO_OK) return set_err(ctx, st, "profile pair rejected (profiles.hpp:129-134)");
+        P.prof[i].m = models[i];
+        P.prof[i].budget = gpus[i].capacity_bytes - gpus[i].runtime_reserve_bytes - models[i].weights_bytes;
+        P.prof[i].fixed = models[i].weights_bytes + gpus[i].runtime_reserve_bytes;
+        if (opts->sets) {
+            if (!opts->sets[i]) return set_err(ctx, COLO_EINVAL, "null map set");
+            P.sets[i] = make_view(opts->sets[i]);
+        }
+    }
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    // segments (host): device offsets come back once per call
+    std::vector<uint64_t> off(ndev + 1);
+    std::vector<uint16_t> prof(ndev);
+    COLO_CK(ctx, cudaMemcpyAsync(off.data(), d_dev_offsets, (ndev + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    COLO_CK(ctx, cudaMemcpyAsync(prof.data(), d_dev_profile, ndev * 2, cudaMemcpyDeviceToHost, ctx->stream));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (off[0] != 0 || off[ndev] != n) return set_err(ctx, COLO_EINVAL, "device offsets must span [0, n]");
+    for (size_t d = 0; d < ndev; ++d) {
+        if (off[d + 1] < off[d]) return set_err(ctx, COLO_EINVAL, "device offsets not monotone");
+        if (prof[d] >= nprofiles) return set_err(ctx, COLO_EINVAL, "device profile index out of range");
+    }
+    uint64_t seg = opts->segment_len;
+    if (seg == 0) {  // enough segments to fill the GPU several times over, 256..8192 queries each
+        const uint64_t target = static_cast<uint64_t>(ctx->sm_count) * 64;
+        seg = std::min<uint64_t>(8192, std::max<uint64_t>(256, n / std::max<uint64_t>(target, 1)));
+    }
+    std::vector<Seg> segs;
+    std::vector<uint32_t> dev_seg(ndev + 1);
+    for (size_t d = 0; d < ndev; ++d) {
+        dev_seg[d] = static_cast<uint32_t>(segs.size());
+        const uint64_t N = off[d + 1] - off[d];
+        for (uint64_t s = 0; s < N; s += seg) segs.push_back(Seg{static_cast<uint32_t>(d), 0, s, std::min(N, s + seg)});
+    }
+    dev_seg[ndev] = static_cast<uint32_t>(segs.size());
+    const size_t ns = segs.size();
+    const bool want_batches = opts->d_batches != nullptr;
+    size_t bytes = 0;
+    const size_t o_segs = bytes;
+    bytes += align256(ns * sizeof(Seg) + 8);
+    const size_t o_dseg = bytes;
+    bytes += align256((ndev + 1) * 4);
+    const size_t o_spec = bytes;
+    bytes += align256(ns * sizeof(SpecOut) + 8);
+    const size_t o_entry = bytes;
+    bytes += align256(ns * sizeof(Entry) + 8);
+    const size_t o_part = bytes;
+    bytes += align256(ns * sizeof(Partial) + 8);
+    const size_t o_base = bytes;
+    bytes += align256(ns * 8 + 8);
+    const size_t o_bstage = bytes;
+    bytes += want_batches ? align256(n * sizeof(colo_batch) + 8) : 0;
+    const size_t o_bflag = bytes;
+    bytes += want_batches ? align256(n + 8) : 0;
+    colo_status st = grow_rscratch(ctx, bytes);
+    if (st != COLO_OK) return st;
+    auto* base = static_cast<uint8_t*>(ctx->d_rscratch);
+    P.segs = reinterpret_cast<const Seg*>(base + o_segs);
+    P.dev_seg = reinterpret_cast<const uint32_t*>(base + o_dseg);
+    P.spec = reinterpret_cast<SpecOut*>(base + o_spec);
+    P.entry = reinterpret_cast<Entry*>(base + o_entry);
+    P.part = reinterpret_cast<Partial*>(base + o_part);
+    P.seg_base = reinterpret_cast<uint64_t*>(base + o_base);
+    if (ns)
+        COLO_CK(ctx, cudaMemcpyAsync(base + o_segs, segs.data(), ns * sizeof(Seg), cudaMemcpyHostToDevice, ctx->stream));
+    COLO_CK(ctx, cudaMemcpyAsync(base + o_dseg, dev_seg.data(), (ndev + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (want_batches) {
+        P.bstage = reinterpret_cast<colo_batch*>(base + o_bstage);
+        P.bflag = base + o_bflag;
+        COLO_CK(ctx, cudaMemsetAsync(P.bflag, 0, n + 8, ctx->stream));
+    }
+    P.nprof = static_cast<uint32_t>(nprofiles);
+    P.has_sets = opts->sets ? 1u : 0u;
+    P.arr = d_arrival;
+    P.p = d_prompt;
+    P.o = d_output;
+    P.dev_off = d_dev_offsets;
+    P.dev_prof = d_dev_profile;
+    P.ndev = static_cast<uint32_t>(ndev);
+    P.nsegs = static_cast<uint32_t>(ns);
+    P.tau = opts->tau;
+    P.samples = opts->d_samples;
+    P.sample_off = opts->d_sample_offsets;
+    P.labels = opts->d_labels;
+    P.batches = opts->d_batches;
+    P.summary = opts->d_summary;
+    P.hist = opts->d_hist;
+    P.nfilters = opts->d_hist ? opts->nfilters : 0;
+    P.hist_shift = opts->hist_shift;
+    P.filter_shift = opts->filter_shift;
+    for (int f = 0; f < 3; ++f) P.prefix[f] = opts->filter_prefix[f];
+    P.err = ctx->d_flag;
+    COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
+    const uint32_t seg_blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
+    const uint32_t dev_blocks = static_cast<uint32_t>((ndev + kWarps - 1) / kWarps);
+    if (ns) {
+        k_validate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        int flag = 0;
+        COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        if (flag)
+            return set_err(ctx, COLO_EVALIDATION,
+                           "trace rejected: unsorted arrivals, zero tokens, or a query that cannot fit the device alone");
+        if (P.samples) {
+            k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+            k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
+        }
+        k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        k_resolve<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    }
+    if (P.summary) k_finalize<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    if (want_batches && ns) k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    COLO_CK(ctx, cudaGetLastError());
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return COLO_OK;
+}
+
+colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const colo_gpu* gpus, size_t nprofiles,
+                               const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
+                               const uint64_t* d_dev_offsets, const uint16_t* d_dev_profile, size_t ndev, double tau,
+                               double* pctl, colo_device_summary* totals) {
+    if (!ctx || !pctl || !totals) return COLO_EINVAL;
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    const size_t hbytes = sizeof(uint64_t) * 3 * COLO_HIST_BINS;
+    uint64_t* d_hist = nullptr;
+    colo_device_summary* d_sum = nullptr;
+    COLO_CK(ctx, cudaMalloc(&d_hist, hbytes));
+    cudaError_t e = cudaMalloc(&d_sum, sizeof(colo_device_summary) * std::max<size_t>(ndev, 1));
+    if (e != cudaSuccess) {
+        cudaFree(d_hist);
+        return cuda_err(ctx, e, "cudaMalloc(summary)");
+    }
+    std::vector<uint64_t> h(3 * static_cast<size_t>(COLO_HIST_BINS));
+    std::vector<colo_device_summary> sums(ndev);
+    colo_status st = COLO_OK;
+    const double qs[3] = {0.50, 0.90, 0.99};
+    uint64_t rank[3], b1[3], b2[3];
+    uint64_t ntot = 0;
+    *totals = colo_device_summary{};
+    for (int i = 0; i < 4; ++i) pctl[i] = std::nan("");
+    for (int pass = 0; pass < 3 && st == COLO_OK; ++pass) {
+        colo_replay_opts o{};
+        o.tau = tau;
+        o.d_hist = d_hist;
+        o.d_summary = pass == 0 ? d_sum : nullptr;
+        if (pass == 0) {
+            o.nfilters = 1;
+            o.filter_shift = 63;
+            o.hist_shift = 42;
+        } else {
+            o.nfilters = 3;
+            o.filter_shift = pass == 1 ? 42 : 21;
+            o.hist_shift = pass == 1 ? 21 : 0;
+            for (int f = 0; f < 3; ++f) o.filter_prefix[f] = pass == 1 ? b1[f] : ((b1[f] << 21) | b2[f]);
+        }
+        e = cudaMemsetAsync(d_hist, 0, hbytes, ctx->stream);
+        if (e != cudaSuccess) {
+            st = cuda_err(ctx, e, "cudaMemset(hist)");
+            break;
+        }
+        st = colo_replay_serving(ctx, models, gpus, nprofiles, d_arrival, d_prompt, d_output, n, d_dev_offsets,
+                                 d_dev_profile, ndev, &o);
+        if (st != COLO_OK) break;
+        e = cudaMemcpy(h.data(), d_hist, sizeof(uint64_t) * o.nfilters * COLO_HIST_BINS, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+            st = cuda_err(ctx, e, "hist D2H");
+            break;
+        }
+        if (pass == 0) {
+            e = cudaMemcpy(sums.data(), d_sum, sizeof(colo_device_summary) * ndev, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) {
+                st = cuda_err(ctx, e, "summary D2H");
+                break;
+            }
+            for (const auto& s : sums) {
+                totals->generated_tokens += s.generated_tokens;
+                totals->slow_tokens += s.slow_tokens;
+                totals->slow_queries += s.slow_queries;
+                totals->batches += s.batches;
+                totals->peak_device_bytes = std::max(totals->peak_device_bytes, s.peak_device_bytes);
+                totals->max_batch_size = std::max(totals->max_batch_size, s.max_batch_size);
+                totals->end_time = std::max(totals->end_time, s.end_time);
+                fixed_add(totals->tpt_sum, s.tpt_sum);
+                totals->flags |= s.flags;
+            }
+            ntot = totals->generated_tokens;
+            if (ntot == 0) break;
+            for (int f = 0; f < 3; ++f) rank[f] = colo_nearest_rank_index(qs[f], ntot);
+        }
+        for (int f = 0; f < 3; ++f) {
+            uint32_t bin;
+            uint64_t rin;
+            const uint64_t* hf = h.data() + static_cast<size_t>(pass == 0 ? 0 : f) * COLO_HIST_BINS;
+            st = colo_hist_select(hf, COLO_HIST_BINS, rank[f], &bin, &rin);
+            if (st != COLO_OK) {
+                st = set_err(ctx, COLO_EBREACH, "histogram pass lost samples");
+                break;
+            }
+            rank[f] = rin;
+            if (pass == 0) b1[f] = bin;
+            else if (pass == 1) b2[f] = bin;
+            else {
+                const uint64_t bits = (b1[f] << 42) | (b2[f] << 21) | bin;
+                double v;
+                std::memcpy(&v, &bits, 8);
+                pctl[f] = v;
+            }
+        }
+    }
+    if (st == COLO_OK && ntot) pctl[3] = fixed_mean(totals->tpt_sum, ntot);
+    cudaFree(d_hist);
+    cudaFree(d_sum);
+    return st;
+}
+
+}  // extern "C"

@@ -274,14 +274,36 @@ def test_features_vs_oracle(ctx, orc):
 
 
 # ----------------------------------------------------------------- replay
-def run_replay(ctx, a, p, o, tau, m=None, sets=None, profiles=None, offs=None, dprof=None):
+def run_replay(ctx, a, p, o, tau, m=None, sets=None, profiles=None, offs=None, dprof=None, segment_len=0):
     profiles = profiles or [(m or cs.ModelProfile(), G)]
     offs = offs if offs is not None else np.array([0, len(p)], np.int64)
     dprof = dprof if dprof is not None else np.zeros(len(offs) - 1, np.int16)
     return cs.replay_serving(ctx, profiles, torch.from_numpy(np.ascontiguousarray(a, np.float64)).cuda(), i32(p), i32(o),
                              torch.from_numpy(np.asarray(offs, np.int64)).cuda(),
                              torch.from_numpy(np.asarray(dprof, np.int16)).cuda(), tau=tau, sets=sets, samples=True,
-                             labels=True, batches=True, summary=True)
+                             labels=True, batches=True, summary=True, segment_len=segment_len)
+
+
+@pytest.mark.parametrize("segment_len", [1, 3, 17, 64, 1000000])
+@pytest.mark.parametrize("qps", [0.05, 0.3, 1.0, 2.5])
+def test_replay_segmented_speculation(ctx, orc, segment_len, qps):
+    """The speculate/resolve/replay passes are exact for any segment length,
+    from idle (0.05 qps) to saturated (2.5 qps) servers."""
+    hv, hp = sharegpt_histogram()
+    a, p, o = orc.generate_trace(qps, 400.0 / qps, ("histogram", hv, hp), 7)
+    o = np.random.default_rng(int(qps * 100)).integers(1, 200, len(o)).astype(np.uint32)
+    sets = [cs.MapSet.build(ctx, cs.ModelProfile(), G, mode=cs.TrainingMode.CPA)]
+    r = run_replay(ctx, a, p, o, 0.05, sets=sets, segment_len=segment_len)
+    ref = orc.replay_serving(default_model(), OG, a, p, o, tau=0.05, grid=default_grid(), cpa=1)
+    assert (r["samples"].cpu().numpy().view(np.uint64) == ref["samples"].view(np.uint64)).all()
+    assert (r["labels"].cpu().numpy() == ref["labels"]).all()
+    S = cs.summaries_to_numpy(r["summary"])[0]
+    nb = int(S["batches"])
+    assert r["batches"].cpu().numpy()[:nb].tobytes() == ref["batches"].tobytes()
+    assert S["end_time"] == ref["summary"]["end_time"] and int(S["slow_tokens"]) == ref["summary"]["slow_tokens"]
+    exact = sum(int(x) for x in (ref["samples"] * 2.0**96))  # every sample is a multiple of 2^-96 here
+    limbs = [int(v) for v in S["tpt_sum"]]
+    assert limbs[0] + (limbs[1] << 64) + (limbs[2] << 128) == exact
 
 
 @pytest.mark.parametrize("name", ["q005", "q03", "q17", "ties", "varout"])
