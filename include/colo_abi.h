@@ -330,11 +330,15 @@ int64_t colo_generate_trace(double qps, double duration, const colo_dist* length
 /* Bench-scale synthetic trace on the device (counter-based hash RNG, not
  * mt19937): per device d, queries [off[d], off[d+1]) get histogram-sampled
  * prompts (bin_values/bin_probs, <= 32 bins), output = 128, and arrivals
- * from the running sum of exponential gaps at qps[d].  The arrays are inputs
- * only: parity is always checked by running the oracle on the same arrays. */
+ * from the running sum of exponential gaps at qps[d].  Bursty traces: with
+ * d_dev_qps_hi != NULL and burst_period > 0 the rate alternates between
+ * qps[d] and qps_hi[d] every burst_period seconds (rate chosen per 32
+ * arrivals).  The arrays are inputs only: parity is always checked by running
+ * the oracle on the same arrays. */
 colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const double* h_bin_probs, size_t nbins,
-                             const uint64_t* d_dev_offsets, const double* d_dev_qps, size_t ndev, uint64_t seed,
-                             double* d_arrival, uint32_t* d_prompt, uint32_t* d_output);
+                             const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
+                             double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
+                             uint32_t* d_output);
 
 #ifdef __cplusplus
 }

@@ -163,7 +163,7 @@ def lib() -> C.CDLL:
         "colo_nearest_rank_index": (u64, [dbl, u64]),
         "colo_serving_stats": (i32, [vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp, C.POINTER(DeviceSummary)]),
         "colo_generate_trace": (C.c_int64, [dbl, dbl, C.POINTER(Dist), C.POINTER(Dist), u64, vp, vp, vp, sz]),
-        "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, sz, u64, vp, vp, vp]),
+        "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, u64, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -825,9 +825,12 @@ def sharegpt_histogram():
     return np.array(values, np.float64), np.array(probs, np.float64)
 
 
-def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float], seed: int, bins=None):
+def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float], seed: int, bins=None,
+                dev_qps_hi: Optional[Sequence[float]] = None, burst_period: float = 0.0):
     """Bench-scale synthetic device traces generated on the GPU (counter-based
-    RNG).  Returns (arrival f64, prompt i32, output i32, dev_offsets i64) CUDA tensors."""
+    RNG); bursty when dev_qps_hi/burst_period are given (rate alternates every
+    burst_period seconds).  Returns (arrival f64, prompt i32, output i32,
+    dev_offsets i64) CUDA tensors."""
     torch = _torch()
     v, p = bins if bins is not None else sharegpt_histogram()
     dev = torch.device("cuda", ctx.device)
@@ -840,6 +843,8 @@ def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float]
     output = torch.empty(max(n, 4), dtype=torch.int32, device=dev)[:n]
     v = np.ascontiguousarray(v, np.float64)
     p = np.ascontiguousarray(p, np.float64)
-    check(lib().colo_synth_trace(ctx.h, v.ctypes.data, p.ctypes.data, len(v), _ptr(d_off), _ptr(d_qps), len(dev_qps),
-                                 seed, _ptr(arrival), _ptr(prompt), _ptr(output)), ctx.h, "synth_trace")
+    d_hi = torch.tensor(list(dev_qps_hi), dtype=torch.float64, device=dev) if dev_qps_hi is not None else None
+    check(lib().colo_synth_trace(ctx.h, v.ctypes.data, p.ctypes.data, len(v), _ptr(d_off), _ptr(d_qps), _ptr(d_hi),
+                                 burst_period, len(dev_qps), seed, _ptr(arrival), _ptr(prompt), _ptr(output)),
+          ctx.h, "synth_trace")
     return arrival, prompt, output, d_off

@@ -79,6 +79,8 @@ struct SynthParams {
     uint32_t nbins;
     const uint64_t* dev_off;
     const double* dev_qps;
+    const double* dev_qps_hi;
+    double period;
     uint32_t ndev;
     uint64_t seed;
     double* arrival;
@@ -101,9 +103,11 @@ __global__ void k_synth(const __grid_constant__ SynthParams P) {
     uint32_t d = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (d >= P.ndev) return;
     uint64_t lo = P.dev_off[d], hi = P.dev_off[d + 1];
-    double rate = P.dev_qps[d];
+    const double rate_lo = P.dev_qps[d];
+    const double rate_hi = P.period > 0.0 ? P.dev_qps_hi[d] : rate_lo;
     double t = 0.0;
     for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
+        const double rate = (P.period > 0.0 && (static_cast<uint64_t>(t / P.period) & 1ull)) ? rate_hi : rate_lo;
         uint64_t j = j0 + lane;
         uint64_t h = mix64(P.seed ^ mix64(j * 2 + 1));
         double gap = -log(1.0 - u01(h)) / rate;
@@ -275,8 +279,9 @@ colo_status colo_features(colo_ctx* ctx, const colo_model* m, colo_mode mode, co
 }
 
 colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const double* h_bin_probs, size_t nbins,
-                             const uint64_t* d_dev_offsets, const double* d_dev_qps, size_t ndev, uint64_t seed,
-                             double* d_arrival, uint32_t* d_prompt, uint32_t* d_output) {
+                             const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
+                             double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
+                             uint32_t* d_output) {
     if (!ctx || !h_bin_values || !h_bin_probs || nbins == 0 || nbins > 32 || ndev == 0) return COLO_EINVAL;
     SynthParams P{};
     double acc = 0;
@@ -288,6 +293,8 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
     P.nbins = static_cast<uint32_t>(nbins);
     P.dev_off = d_dev_offsets;
     P.dev_qps = d_dev_qps;
+    P.dev_qps_hi = d_dev_qps_hi;
+    P.period = d_dev_qps_hi ? burst_period : 0.0;
     P.ndev = static_cast<uint32_t>(ndev);
     P.seed = seed;
     P.arrival = d_arrival;

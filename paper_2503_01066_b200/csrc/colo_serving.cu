@@ -163,6 +163,35 @@ __device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, dou
     }
 }
 
+// First index >= from whose arrival is > T (or N): every arrival at or before
+// T has been popped by the time the batch starts (engine.hpp:146-147,184-187).
+// Arrivals are sorted, so the warp gallops with 32 probes per step (stride
+// x32) and then refines (stride /32): O(log32 distance) dependent loads, so a
+// saturated server's backlog of millions of queued arrivals costs a handful
+// of steps instead of a linear scan.
+__device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, uint64_t N, uint64_t from, double T) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint64_t lo = from;  // every index in [from, lo) has arrival <= T
+    uint64_t stride = 1;
+    bool gallop = true;
+    while (lo < N) {
+        const uint64_t p = lo + (lane + 1) * stride - 1;
+        const bool le = p < N && arr[p] <= T;
+        const uint32_t bal = __ballot_sync(FULL, le);
+        if (bal == FULL && gallop) {
+            lo += 32 * stride;
+            stride *= 32;
+            continue;
+        }
+        gallop = false;
+        const uint32_t f = __ffs(~bal) - 1;  // bal != FULL once refining (the answer lies in the window)
+        lo += f * stride;
+        if (stride == 1) break;
+        stride /= 32;
+    }
+    return lo < N ? lo : N;
+}
+
 enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
 
 struct Acc {  // per-warp outputs of RUN_FULL (every lane holds its own partials)
@@ -213,18 +242,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             tail = head + 1;
             tail_ptr = head + 1;
         } else {  // queued: every arrival with time <= T has been popped
-            if (tail_ptr < head) tail_ptr = head;
-            while (tail_ptr < N) {
-                const uint64_t j = tail_ptr + lane;
-                const bool in = j < N && arr[j] <= T;
-                const uint32_t bal = __ballot_sync(FULL, in);
-                if (bal == FULL) {
-                    tail_ptr += 32;
-                    continue;
-                }
-                tail_ptr += __ffs(~bal) - 1;
-                break;
-            }
+            tail_ptr = find_tail(arr, N, tail_ptr < head ? head : tail_ptr, T);
             tail = tail_ptr;
         }
         // ---- batch formation: FIFO, at least one, sum(need) <= budget (engine.hpp:292-306)
