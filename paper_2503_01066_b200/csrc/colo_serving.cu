@@ -207,7 +207,7 @@ struct Acc {  // per-warp outputs of RUN_FULL (every lane holds its own partials
 // outputs.  head/T are updated in place.
 template <int MODE>
 __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, double& T, uint64_t stop,
-                            uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint32_t* sP, uint32_t* sO) {
+                            uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint2* sPO) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t pi = P.dev_prof[d];
     const colo_model& m = P.prof[pi].m;
@@ -262,10 +262,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             incl += need_total;
             const bool ok = valid && (j == head || incl <= budget);
             const uint32_t cnt = __popc(__ballot_sync(FULL, ok));
-            if (ok && j - head < kStage) {
-                sP[j - head] = pj;
-                sO[j - head] = oj;
-            }
+            if (ok && j - head < kStage) sPO[j - head] = make_uint2(pj, oj);
             max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
             maxo = max(maxo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
             if (cnt) need_total = __shfl_sync(FULL, incl, cnt - 1);
@@ -274,48 +271,73 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         }
         __syncwarp();
         const uint64_t nb = end - head;
-        auto mem_p = [&](uint64_t j) -> uint32_t { return j < kStage ? sP[j] : pp[head + j]; };
-        auto mem_o = [&](uint64_t j) -> uint32_t { return j < kStage ? sO[j] : po[head + j]; };
+        const bool staged = nb <= kStage;  // every member in shared memory (else read from L1/L2)
+        auto member = [&](uint64_t j) -> uint2 { return staged ? sPO[j] : make_uint2(pp[head + j], po[head + j]); };
 
         // ---- prefill: left fold in batch order (engine.hpp:321-325) -------------
         double dur = 0.0;
-        for (uint64_t j = 0; j < nb; ++j) dur += prefill_latency(m, mem_p(j), 1, false);
+        for (uint64_t j = 0; j < nb; ++j) dur += prefill_latency(m, member(j).x, 1, false);
         const double start = T + 0.0;  // prefill_start = now_ + stall, stall = 0
         double now = start + dur;      // PrefillDone time = every member's last_token_time
 
         // ---- decode steps (engine.hpp:358-387) ---------------------------------
+        // Lane l owns steps k0+l, k0+32+l, k0+64+l, k0+96+l: four independent
+        // left folds over the members (batch order), then four in-order chains.
         uint32_t first_slow = 0xffffffffu;
-        for (uint32_t k0 = 0; k0 < maxo; k0 += 32) {
-            const uint32_t k = k0 + lane;
-            double dk = 0.0;
-            uint32_t alive = 0;
-            if (k < maxo) {
+        for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {
+            double dk[4] = {0.0, 0.0, 0.0, 0.0};
+            uint32_t alive[4] = {0, 0, 0, 0};
+            const uint32_t kb = k0 + lane;
+            if (staged) {
                 for (uint64_t j = 0; j < nb; ++j) {
-                    if (k < mem_o(j)) {
-                        dk += decode_step_latency(m, static_cast<uint64_t>(mem_p(j)) + k, 1, false);
-                        ++alive;
+                    const uint2 mj = sPO[j];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t k = kb + 32 * r;
+                        if (k < mj.y) {
+                            dk[r] += decode_step_latency(m, static_cast<uint64_t>(mj.x) + k, 1, false);
+                            ++alive[r];
+                        }
+                    }
+                }
+            } else {
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint2 mj = make_uint2(pp[head + j], po[head + j]);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t k = kb + 32 * r;
+                        if (k < mj.y) {
+                            dk[r] += decode_step_latency(m, static_cast<uint64_t>(mj.x) + k, 1, false);
+                            ++alive[r];
+                        }
                     }
                 }
             }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+            const uint32_t kr0 = k0 + 32 * r;
+            if (kr0 >= maxo) break;
+            const uint32_t k = kr0 + lane;
             double s = 0.0;
 #pragma unroll
             for (int l = 0; l < 32; ++l) {
-                const double dl = __shfl_sync(FULL, dk, l);
-                if (k0 + l < maxo) {
+                const double dl = __shfl_sync(FULL, dk[r], l);
+                if (kr0 + l < maxo) {
                     const double nw = now + dl;
                     if (lane == static_cast<uint32_t>(l)) s = nw - now;  // now - last_token_time
                     now = nw;
                 }
             }
             if (MODE == RUN_FULL) {
+                const uint32_t alv = alive[r];
                 const bool live = k < maxo;
                 const bool slow = live && s > P.tau;
                 const uint32_t sb = __ballot_sync(FULL, slow);
-                if (sb && first_slow == 0xffffffffu) first_slow = k0 + __ffs(sb) - 1;
-                A.gen += alive;
-                if (slow) A.slow_tok += alive;
+                if (sb && first_slow == 0xffffffffu) first_slow = kr0 + __ffs(sb) - 1;
+                A.gen += alv;
+                if (slow) A.slow_tok += alv;
                 if (live) {
-                    acc_fixed(A.acc, A.flags, s, alive);
+                    acc_fixed(A.acc, A.flags, s, alv);
                     if (want_hist) {
                         const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
                         for (uint32_t f = 0; f < P.nfilters; ++f)
@@ -323,28 +345,29 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                 atomicAdd(reinterpret_cast<unsigned long long*>(
                                               &P.hist[static_cast<uint64_t>(f) * COLO_HIST_BINS +
                                                       ((bits >> P.hist_shift) & (COLO_HIST_BINS - 1))]),
-                                          static_cast<unsigned long long>(alive));
+                                          static_cast<unsigned long long>(alv));
                     }
                 }
                 if (P.samples) {
                     // samples of step k occupy alive_k consecutive slots, steps in order
-                    uint32_t ex = alive;
+                    uint32_t ex = alv;
 #pragma unroll
                     for (int sft = 1; sft < 32; sft <<= 1) {
                         const uint32_t y = __shfl_up_sync(FULL, ex, sft);
                         if (lane >= static_cast<uint32_t>(sft)) ex += y;
                     }
                     const uint32_t total = __shfl_sync(FULL, ex, 31);
-                    const uint64_t pos = A.sample_pos + ex - alive;
-                    for (uint32_t a = 0; a < alive; ++a) P.samples[pos + a] = s;
+                    const uint64_t pos = A.sample_pos + ex - alv;
+                    for (uint32_t a = 0; a < alv; ++a) P.samples[pos + a] = s;
                     A.sample_pos += total;
                 }
+            }
             }
         }
         if (MODE == RUN_FULL) {
             // labels: a query is slow iff one of its tokens is (o_j > first slow step)
             for (uint64_t j = lane; j < nb; j += 32) {
-                const bool slowq = mem_o(j) > first_slow;
+                const bool slowq = member(j).y > first_slow;
                 A.slow_q += slowq;
                 if (P.labels) P.labels[lo + head + j] = slowq ? 1 : 0;
             }
@@ -412,7 +435,7 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
-    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    __shared__ uint2 spo[kWarps][kStage];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -421,7 +444,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant
     double T = -INFINITY;
     bool synced;
     Acc A;
-    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, sp[warp], so[warp]);
+    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, spo[warp]);
     if ((threadIdx.x & 31) == 0) {
         P.spec[w].exit_head = head;
         P.spec[w].exit_T = T;
@@ -429,7 +452,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__ ReplayParams P) {
-    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    __shared__ uint2 spo[kWarps][kStage];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t d = blockIdx.x * kWarps + warp;
     if (d >= P.ndev) return;
@@ -441,7 +464,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__
         if ((threadIdx.x & 31) == 0) P.entry[k] = Entry{head, T};
         if (head >= sg.end) continue;  // an earlier batch already covers this segment
         bool synced;
-        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, sp[warp], so[warp]);
+        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp]);
         if (synced) {
             head = P.spec[k].exit_head;
             T = P.spec[k].exit_T;
@@ -450,7 +473,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
-    __shared__ uint32_t sp[kWarps][kStage], so[kWarps][kStage];
+    __shared__ uint2 spo[kWarps][kStage];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -466,7 +489,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_consta
         A.sample_pos = P.sample_off[sg.dev] + P.seg_base[w] + warp_sum_u64(s);
     }
     bool synced;
-    if (head < sg.end) run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, sp[warp], so[warp]);
+    if (head < sg.end) run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp]);
     const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
     const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
 #pragma unroll
