@@ -130,10 +130,22 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
+def init_dist(dist, torch, local):
+    """NCCL over NVLink (one rank per GPU).  COLO_DIST_BACKEND=gloo exercises the
+    multi-rank plumbing with several ranks sharing one GPU (test only)."""
+    backend = os.environ.get("COLO_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("COLO_DIST_BACKEND", "nccl") != "nccl":
+        local = 0  # test mode: every rank on GPU 0
     return world, rank, local
 
 
@@ -218,7 +230,7 @@ def run_ours(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(dist, torch, local)
     ctx = cs.Context(local)
     stream = torch.cuda.current_stream()
     g = cs.GpuProfile()
@@ -333,7 +345,7 @@ def run_c3(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(dist, torch, local)
     ctx = cs.Context(local)
     D, per = args.c3_devices, args.c3_per_device
     profiles = [(cs.ModelProfile(), cs.GpuProfile()), (cs.ModelProfile.phi14b_like(), cs.GpuProfile())]

@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "colo_internal.h"
+#include "colo_tma.cuh"
 
 using namespace colo;
 
@@ -113,6 +114,69 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
                                stream32(mv, off, t[u].z);
             if (i < P.n) __stcs(P.out + i, v);
             if (COUNT) count_warp(v, i < P.n, cnt);
+        }
+    }
+    if (COUNT) flush_warp_counters(cnt, P.counters);
+}
+
+// Tuple stream through a TMA pipeline: each CTA streams 16-KB tiles of tuples
+// into shared memory kStages tiles ahead with cp.async.bulk (one elected
+// thread, mbarrier completion), so the compute never waits on DRAM and needs
+// no register prefetch buffers.  Map cells sit in shared memory next to the
+// stages.
+constexpr uint32_t kTile = 1024;  // tuples per bulk copy (16 KB)
+constexpr uint32_t kStages = 4;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kThreads) k_decide_tma(const __grid_constant__ DecideParams P) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const MapView mv = P.mv;
+    uint4* tiles = reinterpret_cast<uint4*>(sm);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kStages * kTile * 16);
+    uint8_t* off = sm + kStages * kTile * 16 + 64;
+    const uint32_t ob = (mv.off_bytes + 15u) & ~15u;
+    uint8_t* hed = off + ob;
+    const uint64_t ntiles = (P.n + kTile - 1) / kTile;
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    for (uint32_t i = threadIdx.x; i < mv.off_bytes; i += blockDim.x) off[i] = mv.off[i];
+    for (uint32_t i = threadIdx.x; i < mv.hed_bytes; i += blockDim.x) hed[i] = mv.hed[i];
+    __syncthreads();
+    auto issue = [&](uint32_t s, uint64_t t) {
+        const uint64_t rest = P.n - t * kTile;
+        const uint32_t bytes = static_cast<uint32_t>(rest < kTile ? rest : kTile) * 16u;
+        mbar_arrive_expect_tx(&bars[s], bytes);
+        bulk_g2s(tiles + s * kTile, P.in + t * kTile, bytes, &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (uint32_t s = 0; s < kStages; ++s) {
+            const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
+            if (t < ntiles) issue(s, t);
+        }
+    uint32_t cnt[COLO_NCOUNTERS] = {};
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t s = it % kStages;
+        mbar_wait(&bars[s], (it / kStages) & 1u);
+        const uint64_t base = t * kTile;
+        const uint64_t rest = P.n - base;
+        const uint32_t len = static_cast<uint32_t>(rest < kTile ? rest : kTile);
+#pragma unroll
+        for (uint32_t q = 0; q < kTile / kThreads; ++q) {
+            const uint32_t i = threadIdx.x + q * kThreads;
+            const bool valid = i < len;
+            const uint4 tu = valid ? tiles[s * kTile + i] : make_uint4(0, 0, 0, 0);
+            const uint32_t v = compose32(mv, off, hed, tu.x, tu.y, tu.w & 0xffffu, (tu.w >> 16) & 0xffu, tu.w >> 24) |
+                               stream32(mv, off, tu.z);
+            if (valid) __stcs(P.out + base + i, v);
+            if (COUNT) count_warp(v, valid, cnt);
+        }
+        __syncthreads();  // stage s consumed by every thread
+        if (threadIdx.x == 0) {
+            const uint64_t nt = t + static_cast<uint64_t>(kStages) * gridDim.x;
+            if (nt < ntiles) issue(s, nt);
         }
     }
     if (COUNT) flush_warp_counters(cnt, P.counters);
@@ -454,6 +518,17 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
     P.counters = d_counters;
     const size_t smem = ((P.mv.off_bytes + 15u) & ~15u) + P.mv.hed_bytes;
     const bool use_smem = smem <= 96 * 1024;
+    if (use_smem && !(reinterpret_cast<uintptr_t>(d_in) & 15u)) {  // TMA pipeline
+        const size_t dyn = kStages * kTile * 16 + 64 + smem;
+        const void* fn = d_counters ? (const void*)k_decide_tma<true> : (const void*)k_decide_tma<false>;
+        COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        int blocks = blocks_for(ctx, fn, kThreads, dyn);
+        const uint64_t ntiles = (n + kTile - 1) / kTile;
+        if (static_cast<uint64_t>(blocks) > ntiles) blocks = static_cast<int>(ntiles);
+        void* args[] = {&P};
+        COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, stream));
+        return COLO_OK;
+    }
     const void* fn;
     if (use_smem) fn = d_counters ? (const void*)k_decide<true, true> : (const void*)k_decide<true, false>;
     else fn = d_counters ? (const void*)k_decide<false, true> : (const void*)k_decide<false, false>;
