@@ -332,6 +332,118 @@ def run_ours(args, world, rank, local):
 C3_DEVICES, C3_PER_DEVICE = 128, 7_812_500
 
 
+def run_c5(args, world, rank, local):
+    """C5 (BASELINE.json configs[4]): grid steps {500,250,100,50} x profiles
+    {llama8b, phi14b} x modes {CPT, CPA}; per point the batched quantised map
+    verdicts (colo_decide) and the exact per-query verdicts (colo_decide_exact)
+    on the same question stream, plus their agreement / over-free rates.
+    Per GPU: args.c5_tuples questions (default 1e9 split in 4 chunks)."""
+    import torch
+
+    from paper_2503_01066_b200 import colosim as cs
+
+    torch.cuda.set_device(local)
+    ctx = cs.Context(local)
+    total = args.c5_tuples
+    chunk = min(total, 250_000_000)
+    g = cs.GpuProfile()
+    points = []
+    for step in (500, 250, 100, 50):
+        for mname, m in (("llama8b", cs.ModelProfile()), ("phi14b", cs.ModelProfile.phi14b_like())):
+            for mode in (cs.TrainingMode.CPT, cs.TrainingMode.CPA):
+                points.append((step, mname, m, mode))
+    va = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    vb = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    rows = []
+    t_map = t_exact = 0.0
+    n_done = 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for step, mname, m, mode in points:
+        ms = cs.MapSet.build(ctx, m, g, cs.GridSteps(step, step, 5), cs.GridBounds(), mode)
+        counts = torch.zeros(5, dtype=torch.int64, device="cuda")
+        tm = te = 0.0
+        for c0 in range(0, total, chunk):
+            k = min(chunk, total - c0)
+            tup_k = cs.synth_tuples(ctx, k, m.num_layers, 1 + 7919 * rank + c0)
+            torch.cuda.synchronize()
+            ev[0].record()
+            cs.decide(ctx, ms, tup_k, out=va[:k])
+            ev[1].record()
+            cs.decide_exact(ctx, m, g, mode, tup_k, out=vb[:k])
+            ev[2].record()
+            cs.compare_verdicts(ctx, va[:k], vb[:k], m.num_layers, counts)
+            torch.cuda.synchronize()
+            tm += ev[0].elapsed_time(ev[1]) / 1e3
+            te += ev[1].elapsed_time(ev[2]) / 1e3
+        c = [int(x) for x in counts.cpu().tolist()]
+        rows.append({"step": step, "profile": mname, "mode": mode.name, "agree": c[0] / c[4], "over_free": c[1] / c[4],
+                     "under_free": c[2] / c[4], "same_outcome": c[3] / c[4], "map_decisions_per_s": total / tm,
+                     "exact_decisions_per_s": total / te})
+        t_map += tm
+        t_exact += te
+        n_done += total
+        ms.close()
+    if rank == 0:
+        line = {"metric": "C5 sweep: map (per-I/O batched) vs exact per-query decisions/s", "value": n_done / t_map,
+                "unit": "decisions/s", "n_gpus": world, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": f"C5: 16 sweep points x {total} questions (steps 500/250/100/50 x llama8b/phi14b x CPT/CPA)",
+                           "parallelism": f"dp{world}"},
+                "exact_value": n_done / t_exact, "points": rows}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def run_c1(args, world, rank, local):
+    """C1 (BASELINE.json configs[0]): one device trace of 1M queries
+    (generate_trace, ShareGPT-like lengths, seed 41) at qps 0.3 and 1.7:
+    serving replay + replay-derived verdicts on the GPU, with the reference's
+    own Simulation::run (oracle/_ref) timed on the host beside it."""
+    import torch
+
+    from paper_2503_01066_b200 import colosim as cs
+
+    torch.cuda.set_device(local)
+    ctx = cs.Context(local)
+    hv, hp = cs.sharegpt_histogram()
+    m, g = cs.ModelProfile(), cs.GpuProfile()
+    sets = [cs.MapSet.build(ctx, m, g, mode=cs.TrainingMode.CPA)]
+    out = []
+    for qps in (0.3, 1.7):
+        a, p, o = cs.generate_trace(qps, 1_000_000 / qps, ("histogram", hv, hp), 41, ("fixed", 0.01))
+        da, dp, do = torch.from_numpy(a).cuda(), torch.from_numpy(p.view(np.int32)).cuda(), torch.from_numpy(o.view(np.int32)).cuda()
+        offs = torch.tensor([0, len(p)], dtype=torch.int64, device="cuda")
+        prof = torch.zeros(1, dtype=torch.int16, device="cuda")
+        for _ in range(max(args.warmup, 1)):
+            r = cs.replay_serving(ctx, [(m, g)], da, dp, do, offs, prof, tau=0.05, sets=sets, batches=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = cs.replay_serving(ctx, [(m, g)], da, dp, do, offs, prof, tau=0.05, sets=sets, batches=True)
+        torch.cuda.synchronize()
+        gpu_s = (time.perf_counter() - t0) / args.steps
+        cpu = None
+        try:
+            from oracle.oracle import OracleLib, default_gpu, default_model
+
+            ref = OracleLib("ref")
+            t0 = time.perf_counter()
+            ref.replay_serving(default_model(), default_gpu(), a, p, o, tau=0.05, want_samples=False)
+            cpu = time.perf_counter() - t0
+        except Exception as e:  # oracle/_ref absent
+            cpu = None
+        out.append({"qps": qps, "queries": len(p), "gpu_s": gpu_s, "gpu_queries_per_s": len(p) / gpu_s,
+                    "reference_cpu_s": cpu, "reference_queries_per_s": (len(p) / cpu) if cpu else None})
+    if rank == 0:
+        print(json.dumps({"metric": "C1: single-trace serving replay + replay-derived verdicts, queries/s",
+                          "value": out[-1]["gpu_queries_per_s"], "unit": "queries/s", "n_gpus": 1,
+                          "higher_is_better": True, "dtype": "f64", "data": "synthetic (generate_trace, bit-exact)",
+                          "config": {"workload": "C1: 1M queries, one device, ShareGPT-like lengths, seed 41"},
+                          "cpu_baseline": {"kind": "reference", "cores": 1, "sample": "Simulation::run ServingOnly, same trace"},
+                          "runs": out}), flush=True)
+    ctx.close()
+
+
 def run_c3(args, world, rank, local):
     """C3 (BASELINE.json configs[2]): 128 bursty devices x 7,812,500 queries =
     1B queries per GPU, serving replay + slow labels + the first exact-stats
@@ -419,17 +531,23 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3"], default="c2",
-                    help="c2 (default, the headline): trace-fused decisions; c3: serving replay + labels")
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c5"], default="c2",
+                    help="c2 (default, the headline): trace-fused decisions; c1: single-trace replay vs the "
+                         "reference Simulation; c3: 1B-query bursty replay + labels; c5: map vs exact sweep")
     ap.add_argument("--c3-devices", type=int, default=C3_DEVICES)
     ap.add_argument("--c3-per-device", type=int, default=C3_PER_DEVICE)
+    ap.add_argument("--c5-tuples", type=int, default=1_000_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.workload == "c1":
+        run_c1(args, world, rank, local)
     elif args.workload == "c3":
         run_c3(args, world, rank, local)
+    elif args.workload == "c5":
+        run_c5(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -340,6 +340,19 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
                              double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
                              uint32_t* d_output);
 
+/* ------------------------------------------------------------ C5 sweep */
+/* Synthetic admission questions on the device: cached
+ * U[0,8000], incoming = p + 128 with p from the length histogram, batch
+ * U[1,50], pending/dev_layers U[0,L], charged U[0,9000]; 1 % pushed out of the
+ * default grid.  Counter-based RNG: input data only. */
+colo_status colo_synth_tuples(colo_ctx* ctx, uint64_t seed, size_t n, uint32_t num_layers, const double* h_bin_values,
+                              const double* h_bin_probs, size_t nbins, colo_tuple* d_out);
+/* Map-vs-exact statistics over two verdict arrays on the same questions:
+ * d_counts[0] += agree on (action, layers), [1] += map frees more layers,
+ * [2] += map frees fewer, [3] += same outcome, [4] += total. */
+colo_status colo_compare_verdicts(colo_ctx* ctx, const uint32_t* d_map, const uint32_t* d_exact, size_t n,
+                                  uint32_t num_layers, uint64_t* d_counts);
+
 #ifdef __cplusplus
 }
 #endif

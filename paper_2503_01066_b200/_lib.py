@@ -114,7 +114,7 @@ EXPORTS = [
     "colo_mapset_cells", "colo_mapset_hash", "colo_mapset_destroy", "colo_decide", "colo_decide_exact",
     "colo_features_decide", "colo_features_decide_host", "colo_decide_host", "colo_features",
     "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
-    "colo_generate_trace", "colo_synth_trace",
+    "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
 ]
 
 _lib = None
@@ -164,6 +164,8 @@ def lib() -> C.CDLL:
         "colo_serving_stats": (i32, [vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp, C.POINTER(DeviceSummary)]),
         "colo_generate_trace": (C.c_int64, [dbl, dbl, C.POINTER(Dist), C.POINTER(Dist), u64, vp, vp, vp, sz]),
         "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, u64, vp, vp, vp]),
+        "colo_synth_tuples": (i32, [vp, u64, sz, C.c_uint32, vp, vp, sz, vp]),
+        "colo_compare_verdicts": (i32, [vp, vp, vp, sz, C.c_uint32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -825,6 +825,29 @@ def sharegpt_histogram():
     return np.array(values, np.float64), np.array(probs, np.float64)
 
 
+def synth_tuples(ctx: Context, n: int, num_layers: int, seed: int, bins=None):
+    """C5 question stream on the GPU (colo_synth_tuples): int32 [n, 4] colo_tuple records."""
+    torch = _torch()
+    v, p = bins if bins is not None else sharegpt_histogram()
+    v = np.ascontiguousarray(v, np.float64)
+    p = np.ascontiguousarray(p, np.float64)
+    out = torch.empty((max(n, 1), 4), dtype=torch.int32, device=torch.device("cuda", ctx.device))[:n]
+    check(lib().colo_synth_tuples(ctx.h, seed, n, num_layers, v.ctypes.data, p.ctypes.data, len(v), _ptr(out)),
+          ctx.h, "synth_tuples")
+    return out
+
+
+def compare_verdicts(ctx: Context, map_verdicts, exact_verdicts, num_layers: int, counts=None):
+    """Map-vs-exact agreement (colo_compare_verdicts): int64[5] = agree, over-free,
+    under-free, same outcome, total (accumulated into ``counts`` if given)."""
+    torch = _torch()
+    if counts is None:
+        counts = torch.zeros(5, dtype=torch.int64, device=map_verdicts.device)
+    check(lib().colo_compare_verdicts(ctx.h, _ptr(map_verdicts), _ptr(exact_verdicts), map_verdicts.shape[0],
+                                      num_layers, _ptr(counts)), ctx.h, "compare_verdicts")
+    return counts
+
+
 def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float], seed: int, bins=None,
                 dev_qps_hi: Optional[Sequence[float]] = None, burst_period: float = 0.0):
     """Bench-scale synthetic device traces generated on the GPU (counter-based
