@@ -340,6 +340,37 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
                              double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
                              uint32_t* d_output);
 
+/* ------------------------------------------------------------ file formats */
+/* Offloading / hedging map text files, byte-identical to OffloadingMap::save /
+ * HedgingMap::save (maps.hpp:118-140, 284-295).  Loading refuses a profile
+ * hash other than expected_hash with EVALIDATION (maps.hpp:155-157, 311-312);
+ * cells == NULL queries the cell count.  err (optional) receives the
+ * reference's message text. */
+typedef struct colo_map_header {
+    int kind;                 /* 0 offload, 1 hedge */
+    colo_mode mode;
+    uint64_t profile_hash;
+    uint64_t num_layers;
+    colo_grid grid;           /* hedge maps use cached_step and max_cached only */
+    uint64_t assumed_output_tokens;
+} colo_map_header;
+colo_status colo_map_save(const char* path, const colo_map_header* h, const uint8_t* cells, size_t ncells);
+colo_status colo_map_load(const char* path, uint64_t expected_hash, colo_map_header* h, uint8_t* cells, size_t cap,
+                          size_t* ncells, char* err, size_t errlen);
+colo_status colo_mapset_save(colo_ctx* ctx, const colo_mapset* ms, const char* offload_path, const char* hedge_path);
+colo_status colo_mapset_load(colo_ctx* ctx, const colo_model* m, const colo_gpu* g, const char* offload_path,
+                             const char* hedge_path, colo_mapset** out);
+/* JSON-lines trace (load_trace, workload.hpp:224-254): one object per line
+ * with query_id, arrival_time, prompt_tokens, output_tokens (default 128),
+ * label_delay (null -> NaN); validated and ordered exactly as validate_trace
+ * (stable sort by (arrival, id); negative arrival, zero tokens, duplicate ids
+ * rejected).  Returns the record count, -1 if cap is too small, -2 on error. */
+int64_t colo_load_trace_jsonl(const char* path, double* arrival, uint32_t* prompt, uint32_t* output,
+                              uint64_t* query_id, double* label_delay, size_t cap, char* err, size_t errlen);
+/* Histogram file of {tokens, probability} lines (load_histogram, workload.hpp:274-293). */
+int64_t colo_load_histogram_jsonl(const char* path, double* values, double* probs, size_t cap, char* err,
+                                  size_t errlen);
+
 /* ------------------------------------------------------------ C5 sweep */
 /* Synthetic admission questions on the device: cached
  * U[0,8000], incoming = p + 128 with p from the length histogram, batch

@@ -450,4 +450,57 @@ int64_t ref_generate_trace(double qps, double duration, const orc_dist* lengths,
     }
 }
 
+/* File formats through the reference's own writers/readers (maps.hpp:118-191,
+ * 284-332; workload.hpp:224-271). */
+int ref_save_maps(const orc_model* m, const orc_gpu* g, const orc_grid* grid, int cpa, uint64_t assumed,
+                  const char* offload_path, const char* hedge_path) {
+    try {
+        Maps mp = make_maps(m, g, grid, cpa, grid->cached_step, grid->max_cached, assumed);
+        mp.off.save(offload_path);
+        mp.hedge.save(hedge_path);
+        return ORC_OK;
+    } catch (const std::exception&) {
+        return ORC_EVALIDATION;
+    }
+}
+
+int ref_save_trace(const double* arrival, const uint32_t* prompt, const uint32_t* output, const double* label_delay,
+                   size_t n, const char* path) {
+    try {
+        Trace t;
+        for (size_t i = 0; i < n; ++i) {
+            QueryRecord r;
+            r.query_id = i;
+            r.arrival_time = arrival[i];
+            r.prompt_tokens = prompt[i];
+            r.output_tokens = output[i];
+            if (label_delay && !std::isnan(label_delay[i])) r.label_delay = label_delay[i];
+            t.records.push_back(r);
+        }
+        save_trace(t, path);
+        return ORC_OK;
+    } catch (const std::exception&) {
+        return ORC_EVALIDATION;
+    }
+}
+
+int64_t ref_load_trace(const char* path, double* arrival, uint32_t* prompt, uint32_t* output, uint64_t* ids,
+                       double* label_delay, size_t cap) {
+    try {
+        Trace t = load_trace(path);
+        if (t.records.size() > cap) return -1;
+        for (size_t i = 0; i < t.records.size(); ++i) {
+            const auto& r = t.records[i];
+            arrival[i] = r.arrival_time;
+            prompt[i] = static_cast<uint32_t>(r.prompt_tokens);
+            output[i] = static_cast<uint32_t>(r.output_tokens);
+            ids[i] = r.query_id;
+            label_delay[i] = r.label_delay ? *r.label_delay : std::nan("");
+        }
+        return static_cast<int64_t>(t.records.size());
+    } catch (const std::exception&) {
+        return -2;
+    }
+}
+
 }  // extern "C"

@@ -115,7 +115,14 @@ EXPORTS = [
     "colo_features_decide", "colo_features_decide_host", "colo_decide_host", "colo_features",
     "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
     "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
+    "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
+    "colo_load_histogram_jsonl",
 ]
+
+
+class MapHeader(C.Structure):
+    _fields_ = [("kind", C.c_int), ("mode", C.c_int), ("profile_hash", C.c_uint64), ("num_layers", C.c_uint64),
+                ("grid", Grid), ("assumed_output_tokens", C.c_uint64)]
 
 _lib = None
 
@@ -166,6 +173,12 @@ def lib() -> C.CDLL:
         "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, u64, vp, vp, vp]),
         "colo_synth_tuples": (i32, [vp, u64, sz, C.c_uint32, vp, vp, sz, vp]),
         "colo_compare_verdicts": (i32, [vp, vp, vp, sz, C.c_uint32, vp]),
+        "colo_map_save": (i32, [C.c_char_p, C.POINTER(MapHeader), vp, sz]),
+        "colo_map_load": (i32, [C.c_char_p, u64, C.POINTER(MapHeader), vp, sz, C.POINTER(sz), C.c_char_p, sz]),
+        "colo_mapset_save": (i32, [vp, vp, C.c_char_p, C.c_char_p]),
+        "colo_mapset_load": (i32, [vp, MP, GP, C.c_char_p, C.c_char_p, C.POINTER(vp)]),
+        "colo_load_trace_jsonl": (C.c_int64, [C.c_char_p, vp, vp, vp, vp, vp, sz, C.c_char_p, sz]),
+        "colo_load_histogram_jsonl": (C.c_int64, [C.c_char_p, vp, vp, sz, C.c_char_p, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -385,22 +385,9 @@ class OffloadingMap:
         return (bi + 1) * self.steps.batch_step
 
     def save(self, path: str) -> None:
-        """maps.hpp:118-140 text format."""
-        lines = [f"version 1", "kind offload", f"mode {self.mode.name.lower()}",
-                 f"profile_hash {self.profile_hash_value}", f"num_layers {self.num_layers}",
-                 f"cached_step {self.steps.cached_token_step}", f"incoming_step {self.steps.incoming_token_step}",
-                 f"batch_step {self.steps.batch_step}", f"max_cached {self.bounds.max_cached_tokens}",
-                 f"max_incoming {self.bounds.max_incoming_tokens}", f"max_batch {self.bounds.max_batch}"]
-        for ci in range(self.cached_count()):
-            for ii in range(self.incoming_count()):
-                for bi in range(self.batch_count()):
-                    d = self.cell(ci, ii, bi)
-                    tok = {OffloadAction.NoAction: "noaction", OffloadAction.AllToHost: "host"}.get(
-                        d.action, f"free:{d.layers}")
-                    lines.append(f"{self.cached_bucket_value(ci)},{self.incoming_bucket_value(ii)},"
-                                 f"{self.batch_bucket_value(bi)},{tok}")
-        with open(path, "w") as f:
-            f.write("\n".join(lines) + "\n")
+        """maps.hpp:118-140 text format (colo_map_save)."""
+        save_map_cells(path, "offload", self.mode, self.profile_hash_value, self.num_layers, self.steps, self.bounds,
+                       self.ms.cells()[0])
 
 
 class HedgingMap:
@@ -433,6 +420,12 @@ class HedgingMap:
 
     def cached_bucket_value(self, ci: int) -> int:
         return (ci + 1) * self.cached_token_step
+
+    def save(self, path: str) -> None:
+        """maps.hpp:284-295 text format (colo_map_save)."""
+        save_map_cells(path, "hedge", self.mode, self.profile_hash_value, self.num_layers,
+                       GridSteps(self.cached_token_step, 1, 1), GridBounds(self.max_cached_tokens, 1, 1),
+                       self.ms.cells()[1], self.assumed_output_tokens)
 
 
 @dataclass
@@ -871,3 +864,83 @@ def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float]
                                  burst_period, len(dev_qps), seed, _ptr(arrival), _ptr(prompt), _ptr(output)),
           ctx.h, "synth_trace")
     return arrival, prompt, output, d_off
+
+
+# ------------------------------------------------------------ file formats
+def save_map_cells(path: str, kind: str, mode: TrainingMode, profile_hash_value: int, num_layers: int,
+                   steps: GridSteps, bounds: GridBounds, cells: np.ndarray, assumed_output_tokens: int = 128) -> None:
+    """OffloadingMap::save / HedgingMap::save text (maps.hpp:118-140, 284-295), byte-identical."""
+    h = _lib.MapHeader()
+    h.kind = 0 if kind == "offload" else 1
+    h.mode = int(mode)
+    h.profile_hash = profile_hash_value
+    h.num_layers = num_layers
+    h.grid = _grid(steps, bounds)
+    h.assumed_output_tokens = assumed_output_tokens
+    c = np.ascontiguousarray(cells, np.uint8)
+    check(lib().colo_map_save(path.encode(), C.byref(h), c.ctypes.data, c.size), None, f"cannot write map file: {path}")
+
+
+def load_map_cells(path: str, expected_hash: int):
+    """OffloadingMap::load / HedgingMap::load (maps.hpp:142-191, 297-332): (header dict, cells).
+    Raises ColoValidationError on a profile-hash mismatch or a malformed file."""
+    h = _lib.MapHeader()
+    n = C.c_size_t()
+    err = C.create_string_buffer(512)
+    st = lib().colo_map_load(path.encode(), expected_hash, C.byref(h), None, 0, C.byref(n), err, 512)
+    if st:
+        raise ColoValidationError(st, err.value.decode())
+    cells = np.zeros(n.value, np.uint8)
+    st = lib().colo_map_load(path.encode(), expected_hash, C.byref(h), cells.ctypes.data, cells.size, C.byref(n), err, 512)
+    if st:
+        raise ColoValidationError(st, err.value.decode())
+    g = h.grid
+    hdr = {"kind": "offload" if h.kind == 0 else "hedge", "mode": TrainingMode(h.mode), "profile_hash": h.profile_hash,
+           "num_layers": h.num_layers, "steps": GridSteps(g.cached_step, g.incoming_step, g.batch_step),
+           "bounds": GridBounds(g.max_cached, g.max_incoming, g.max_batch),
+           "assumed_output_tokens": h.assumed_output_tokens}
+    return hdr, cells
+
+
+def save_mapset(ms: MapSet, offload_path: Optional[str], hedge_path: Optional[str]) -> None:
+    """Both maps of a device MapSet in the reference's text format."""
+    check(lib().colo_mapset_save(ms.ctx.h, ms.h, offload_path.encode() if offload_path else None,
+                                 hedge_path.encode() if hedge_path else None), ms.ctx.h, "map save")
+
+
+def load_mapset(ctx: Context, m: ModelProfile, g: GpuProfile, offload_path: str, hedge_path: str) -> MapSet:
+    """Load saved maps onto the device; refuses maps built from other profiles (maps.hpp:155-157)."""
+    h = C.c_void_p()
+    check(lib().colo_mapset_load(ctx.h, C.byref(m.to_c()), C.byref(g.to_c()), offload_path.encode(),
+                                 hedge_path.encode(), C.byref(h)), ctx.h, "map load")
+    ho, _ = load_map_cells(offload_path, profile_hash(m, g))
+    hh, _ = load_map_cells(hedge_path, profile_hash(m, g))
+    return MapSet(ctx, h, m, g, ho["steps"], ho["bounds"], ho["mode"], hh["steps"].cached_token_step,
+                  hh["bounds"].max_cached_tokens, hh["assumed_output_tokens"])
+
+
+def load_trace(path: str):
+    """load_trace (workload.hpp:224-254): validated, (arrival, id)-ordered SoA arrays
+    (arrival f64, prompt u32, output u32, query_id u64, label_delay f64 with NaN = null)."""
+    err = C.create_string_buffer(512)
+    n = lib().colo_load_trace_jsonl(path.encode(), None, None, None, None, None, 0, err, 512)
+    if n == -2:
+        raise ColoValidationError(_lib.COLO_EVALIDATION, err.value.decode())
+    lines = sum(1 for ln in open(path) if ln.strip())  # records <= non-empty lines
+    a, p, o = np.empty(lines), np.empty(lines, np.uint32), np.empty(lines, np.uint32)
+    q, ld = np.empty(lines, np.uint64), np.empty(lines)
+    n = lib().colo_load_trace_jsonl(path.encode(), a.ctypes.data, p.ctypes.data, o.ctypes.data, q.ctypes.data,
+                                    ld.ctypes.data, lines, err, 512)
+    if n < 0:
+        raise ColoValidationError(_lib.COLO_EVALIDATION, err.value.decode())
+    return a[:n], p[:n], o[:n], q[:n], ld[:n]
+
+
+def load_histogram(path: str):
+    """load_histogram (workload.hpp:274-293): (values, probabilities)."""
+    err = C.create_string_buffer(512)
+    v, p = np.empty(1024), np.empty(1024)
+    n = lib().colo_load_histogram_jsonl(path.encode(), v.ctypes.data, p.ctypes.data, 1024, err, 512)
+    if n < 0:
+        raise ColoValidationError(_lib.COLO_EVALIDATION, err.value.decode() or "histogram too large")
+    return v[:n], p[:n]

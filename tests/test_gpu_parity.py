@@ -383,3 +383,18 @@ def test_serving_stats_exact(ctx, orc):
     pc, tot = cs.serving_stats_c(*args, tau=0.05)
     assert tuple(pc[:3]) == (p50, p90, p99) and abs(pc[3] - mean) <= 1e-12 * mean
     assert tot.generated_tokens == len(ref["samples"])
+
+
+def test_mapset_save_load_roundtrip(ctx, tmp_path):  # maps.hpp:118-191, 284-332 through device map sets
+    for m, mode in ((cs.ModelProfile(), cs.TrainingMode.CPA), (cs.ModelProfile.phi14b_like(), cs.TrainingMode.CPT)):
+        ms = cs.MapSet.build(ctx, m, G, mode=mode)
+        po, ph = str(tmp_path / "o.map"), str(tmp_path / "h.map")
+        cs.save_mapset(ms, po, ph)
+        ld = cs.load_mapset(ctx, m, G, po, ph)
+        assert (ld.cells()[0] == ms.cells()[0]).all() and (ld.cells()[1] == ms.cells()[1]).all()
+        assert ld.offload.lookup(4000, 2000, 10) == ms.offload.lookup(4000, 2000, 10)
+        other = cs.ModelProfile(prefill_coef_quad=3e-8, num_layers=m.num_layers)
+        with pytest.raises(cs.ColoValidationError, match="hash"):
+            cs.load_mapset(ctx, other, G, po, ph)
+        ms.offload.save(str(tmp_path / "o2.map"))
+        assert open(str(tmp_path / "o2.map"), "rb").read() == open(po, "rb").read()
