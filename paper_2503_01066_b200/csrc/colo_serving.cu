@@ -28,6 +28,8 @@
 // Reference paths are relative to /root/reference/proj/.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -207,7 +209,8 @@ struct Acc {  // per-warp outputs of RUN_FULL (every lane holds its own partials
 // outputs.  head/T are updated in place.
 template <int MODE>
 __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, double& T, uint64_t stop,
-                            uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint2* sPO) {
+                            uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint2* sPO, double* sPD,
+                            double* sDK) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t pi = P.dev_prof[d];
     const colo_model& m = P.prof[pi].m;
@@ -262,7 +265,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             incl += need_total;
             const bool ok = valid && (j == head || incl <= budget);
             const uint32_t cnt = __popc(__ballot_sync(FULL, ok));
-            if (ok && j - head < kStage) sPO[j - head] = make_uint2(pj, oj);
+            if (ok && j - head < kStage) {
+                sPO[j - head] = make_uint2(pj, oj);
+                sPD[j - head] = static_cast<double>(pj);
+            }
             max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
             maxo = max(maxo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
             if (cnt) need_total = __shfl_sync(FULL, incl, cnt - 1);
@@ -271,63 +277,96 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         }
         __syncwarp();
         const uint64_t nb = end - head;
+        // The replay walks each array sequentially: keep the next ~1K queries of
+        // prompt/output and the arrivals around the queue tail warm in L2 so the
+        // dependent loads of later batches hit L2 instead of DRAM.
+        {
+            const uint64_t q = end + 512 + lane * 32;
+            if (q < N) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + q));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(po + q));
+            }
+            const uint64_t a0 = (tail_ptr > end ? tail_ptr : end) + lane * 16;
+            if (a0 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(arr + a0));
+        }
         const bool staged = nb <= kStage;  // every member in shared memory (else read from L1/L2)
         auto member = [&](uint64_t j) -> uint2 { return staged ? sPO[j] : make_uint2(pp[head + j], po[head + j]); };
+        // exact (double)p_j: p < 2^32 and k < 2^32, so (double)p + (double)k == (double)(p + k)
+        auto member_pd = [&](uint64_t j) -> double { return staged ? sPD[j] : static_cast<double>(pp[head + j]); };
 
         // ---- prefill: left fold in batch order (engine.hpp:321-325) -------------
+        // cost_model.hpp:18-25 with batch 1: 1.0 * (lin*t + (quad*t)*t) == lin*t + (quad*t)*t
         double dur = 0.0;
-        for (uint64_t j = 0; j < nb; ++j) dur += prefill_latency(m, member(j).x, 1, false);
+#pragma unroll 4
+        for (uint64_t j = 0; j < nb; ++j) {
+            const double t = member_pd(j);
+            dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
+        }
         const double start = T + 0.0;  // prefill_start = now_ + stall, stall = 0
         double now = start + dur;      // PrefillDone time = every member's last_token_time
 
         // ---- decode steps (engine.hpp:358-387) ---------------------------------
         // Lane l owns steps k0+l, k0+32+l, k0+64+l, k0+96+l: four independent
-        // left folds over the members (batch order), then four in-order chains.
+        // left folds over the members in batch order (cost_model.hpp:28-35,
+        // batch 1: 1.0 * (gamma + delta*ctx)), unrolled so member loads and
+        // multiplies overlap the accumulate chains; the step durations go to
+        // shared memory and the absolute-time chain reads them back in order.
         uint32_t first_slow = 0xffffffffu;
+        const double gam = m.decode_coef_const, del = m.decode_coef_context;
         for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {
             double dk[4] = {0.0, 0.0, 0.0, 0.0};
             uint32_t alive[4] = {0, 0, 0, 0};
             const uint32_t kb = k0 + lane;
+            double kd[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
             if (staged) {
+#pragma unroll 4
                 for (uint64_t j = 0; j < nb; ++j) {
-                    const uint2 mj = sPO[j];
+                    const uint32_t oj = sPO[j].y;
+                    const double pj = sPD[j];
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
-                        const uint32_t k = kb + 32 * r;
-                        if (k < mj.y) {
-                            dk[r] += decode_step_latency(m, static_cast<uint64_t>(mj.x) + k, 1, false);
+                        if (kb + 32 * r < oj) {
+                            dk[r] += gam + del * (pj + kd[r]);
                             ++alive[r];
                         }
                     }
                 }
             } else {
                 for (uint64_t j = 0; j < nb; ++j) {
-                    const uint2 mj = make_uint2(pp[head + j], po[head + j]);
+                    const uint32_t oj = po[head + j];
+                    const double pj = static_cast<double>(pp[head + j]);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
-                        const uint32_t k = kb + 32 * r;
-                        if (k < mj.y) {
-                            dk[r] += decode_step_latency(m, static_cast<uint64_t>(mj.x) + k, 1, false);
+                        if (kb + 32 * r < oj) {
+                            dk[r] += gam + del * (pj + kd[r]);
                             ++alive[r];
                         }
                     }
                 }
             }
 #pragma unroll
+            for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = dk[r];
+            __syncwarp();
+            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int l = 0; l < 32; ++l) {
+                    if (k0 + 32 * r + l < maxo) {
+                        const double nw = now + sDK[32 * r + l];
+                        if (lane == static_cast<uint32_t>(l)) sv[r] = nw - now;  // now - last_token_time
+                        now = nw;
+                    }
+                }
+            __syncwarp();
+#pragma unroll
             for (int r = 0; r < 4; ++r) {
             const uint32_t kr0 = k0 + 32 * r;
             if (kr0 >= maxo) break;
             const uint32_t k = kr0 + lane;
-            double s = 0.0;
-#pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                const double dl = __shfl_sync(FULL, dk[r], l);
-                if (kr0 + l < maxo) {
-                    const double nw = now + dl;
-                    if (lane == static_cast<uint32_t>(l)) s = nw - now;  // now - last_token_time
-                    now = nw;
-                }
-            }
+            const double s = sv[r];
             if (MODE == RUN_FULL) {
                 const uint32_t alv = alive[r];
                 const bool live = k < maxo;
@@ -436,6 +475,7 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
 
 __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
+    __shared__ double spd[kWarps][kStage], sdk[kWarps][128];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -444,17 +484,20 @@ __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant
     double T = -INFINITY;
     bool synced;
     Acc A;
-    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, spo[warp]);
+    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, spo[warp], spd[warp], sdk[warp]);
     if ((threadIdx.x & 31) == 0) {
         P.spec[w].exit_head = head;
         P.spec[w].exit_T = T;
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__ ReplayParams P) {
-    __shared__ uint2 spo[kWarps][kStage];
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t d = blockIdx.x * kWarps + warp;
+// One warp per CTA: resolve is a sequential chain per device, so each device
+// gets an SM of its own (no issue-slot or FP64-pipe sharing between devices).
+__global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayParams P) {
+    __shared__ uint2 spo[1][kStage];
+    __shared__ double spd[1][kStage], sdk[1][128];
+    const uint32_t warp = 0;
+    const uint32_t d = blockIdx.x;
     if (d >= P.ndev) return;
     uint64_t head = 0;
     double T = -INFINITY;  // server idle before the first arrival (probe B4b)
@@ -464,7 +507,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__
         if ((threadIdx.x & 31) == 0) P.entry[k] = Entry{head, T};
         if (head >= sg.end) continue;  // an earlier batch already covers this segment
         bool synced;
-        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp]);
+        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp], spd[warp],
+                                 sdk[warp]);
         if (synced) {
             head = P.spec[k].exit_head;
             T = P.spec[k].exit_T;
@@ -474,6 +518,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_resolve(const __grid_constant__
 
 __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
+    __shared__ double spd[kWarps][kStage], sdk[kWarps][128];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -489,7 +534,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_consta
         A.sample_pos = P.sample_off[sg.dev] + P.seg_base[w] + warp_sum_u64(s);
     }
     bool synced;
-    if (head < sg.end) run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp]);
+    if (head < sg.end)
+        run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp], spd[warp], sdk[warp]);
     const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
     const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
 #pragma unroll
@@ -743,9 +789,27 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
+        const bool timing = std::getenv("COLO_REPLAY_TIMING") != nullptr;  // per-pass device times to stderr
+        cudaEvent_t ev[4];
+        if (timing)
+            for (auto& e : ev) cudaEventCreate(&e);
+        if (timing) cudaEventRecord(ev[0], ctx->stream);
         k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
-        k_resolve<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        if (timing) cudaEventRecord(ev[1], ctx->stream);
+        k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
+        if (timing) cudaEventRecord(ev[2], ctx->stream);
         k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        if (timing) {
+            cudaEventRecord(ev[3], ctx->stream);
+            cudaEventSynchronize(ev[3]);
+            float a, b, c;
+            cudaEventElapsedTime(&a, ev[0], ev[1]);
+            cudaEventElapsedTime(&b, ev[1], ev[2]);
+            cudaEventElapsedTime(&c, ev[2], ev[3]);
+            std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms, replay %.3f ms\n",
+                         ns, static_cast<unsigned long long>(seg), a, b, c);
+            for (auto& e : ev) cudaEventDestroy(e);
+        }
     }
     if (P.summary) k_finalize<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
     if (want_batches && ns) k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
