@@ -3,8 +3,8 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 PKG := paper_2503_01066_b200
-SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu
-HDR := include/colo_abi.h $(PKG)/csrc/colo_common.cuh $(PKG)/csrc/colo_internal.h
+SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu $(PKG)/csrc/colo_colocated.cu
+HDR := include/colo_abi.h $(PKG)/csrc/colo_common.cuh $(PKG)/csrc/colo_internal.h $(PKG)/csrc/colo_replay.cuh
 # -fmad=false: no FMA contraction anywhere (bit-exact f64 vs the x86 reference)
 NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Iinclude -Xcompiler -fPIC,-O2 -Xptxas -v
 

@@ -35,6 +35,13 @@
  *                                   (SURVEY.md §8(d) C2 rule)
  *   colo_replay_serving             Simulation::run in SimMode::ServingOnly
  *                                                                    include/colosim/engine.hpp:140-164, 270-387
+ *   colo_replay_colocated           Simulation::run in SimMode::Colocated (the admission loop:
+ *                                   slot, offloader, hedge, prefetch, preemption, cache timeout)
+ *                                                                    include/colosim/engine.hpp:140-822,
+ *                                                                    include/colosim/memory.hpp:19-211
+ *   colo_colocated_stats            run_simulation(Colocated) + finalize over a device set
+ *                                                                    include/colosim/engine.hpp:938-941,
+ *                                                                    include/colosim/metrics.hpp:56-69
  *   colo_hist_select / percentiles  finalize / nearest_rank          include/colosim/metrics.hpp:48-69
  *   colo_generate_trace             generate_trace (host, bit-exact) include/colosim/workload.hpp:193-220
  */
@@ -312,6 +319,89 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
                                const uint64_t* d_dev_offsets, const uint16_t* d_dev_profile, size_t ndev, double tau,
                                double* pctl, colo_device_summary* totals);
 
+/* ------------------------------------------------------- colocated replay */
+/* Per-device MetricsReport (metrics.hpp:17-44; the first 14 fields, same
+ * meaning) plus replay extras.  training_throughput = trained_tokens /
+ * training_busy_time when busy > 0 (metrics.hpp:67-68). */
+typedef struct colo_colocated_summary {
+    uint64_t generated_tokens;
+    uint64_t trained_tokens;
+    double training_busy_time;
+    uint64_t peak_device_bytes;
+    uint64_t peak_training_activation_bytes;
+    uint64_t preemptions;
+    uint64_t layers_freed;
+    uint64_t loads;
+    uint64_t recomputes;
+    double copy_stall_seconds;
+    uint64_t labels_dropped;
+    double prefetch_wait_seconds;
+    uint64_t completed_jobs;
+    uint64_t map_fallbacks;
+    /* extras */
+    uint64_t batches;
+    uint64_t max_batch_size;
+    uint64_t offload_decisions; /* apply_offload_decision calls (engine.hpp:309-310) */
+    uint64_t admissions;        /* admit_to_store calls (engine.hpp:317-318) */
+    uint64_t slow_tokens;       /* tokens with TPT > tau */
+    uint64_t slow_queries;      /* queries with any token TPT > tau */
+    double end_time;            /* time of the last decode step */
+    uint64_t status;            /* COLO_OK, or COLO_EBREACH: the reference run throws (InvariantBreach /
+                                   std::logic_error) and this device's other fields are partial */
+    uint64_t tpt_sum[3];        /* exact sum of TPT samples, fixed point, LSB 2^-96 */
+    uint64_t flags;             /* bit0: a sample fell outside the exact-sum range */
+} colo_colocated_summary;
+
+/* Extra verdict bits in colocated batch records (colo_batch.verdict): the
+ * offload decision apply_offload_decision took for this batch (action,
+ * layers, free_now, hedge, oor bits and the final outcome, including the KV
+ * corner's drop, engine.hpp:549-552), and the slot admission. */
+#define COLO_V_EVALUATED (1u << 25)  /* apply_offload_decision ran (engine.hpp:309-310) */
+#define COLO_V_ADMITTED (1u << 26)   /* admit_to_store ran for this batch (engine.hpp:317-318);
+                                        COLO_V_STREAM / _STREAM_OOR give its streaming flag */
+
+typedef struct colo_colocated_opts {
+    double cache_timeout;            /* SimConfig::cache_timeout (engine.hpp:55); the reference default is 60 */
+    const double* d_label_delay;     /* [n] seconds; < 0 or NaN = the label never arrives; NULL = default_label_delay */
+    double default_label_delay;      /* used when d_label_delay == NULL (< 0 = never) */
+    double tau;                      /* slow-token threshold (TPT > tau) */
+    double* d_samples;               /* TPT samples in reference order; needs d_sample_offsets */
+    const uint64_t* d_sample_offsets;/* [ndev+1] prefix sums of output tokens per device */
+    uint8_t* d_labels;               /* [n] 1 = slow query */
+    colo_batch* d_batches;           /* batch b of device d at d_dev_offsets[d] + b */
+    colo_colocated_summary* d_summary; /* [ndev] */
+    uint64_t* d_hist;                /* TPT histogram pass, as colo_replay_opts */
+    uint32_t nfilters;
+    uint32_t hist_shift;
+    uint32_t filter_shift;
+    uint32_t pad;
+    uint64_t filter_prefix[3];
+} colo_colocated_opts;
+
+/* Colocated replay (SimMode::Colocated) of every device's trace, one warp per
+ * device.  Device d uses map set sets[d_dev_set[d]], whose model, GPU profile
+ * and training mode are the simulation's (SimConfig::validate requires the
+ * maps to match them, engine.hpp:60-68).  Events are handled in the
+ * reference's (time, sequence) order and every f64 operation is the
+ * reference's in its order, so each device's report and samples equal
+ * Simulation::run's.  EVALIDATION as colo_replay_serving; EBREACH when a
+ * device's run breaches an invariant (its summary has status COLO_EBREACH).
+ * Synchronous (returns after the replay finished). */
+colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets, const double* d_arrival,
+                                  const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
+                                  const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev,
+                                  const colo_colocated_opts* opts);
+
+/* Colocated replays of a device set plus exact TPT statistics over the union
+ * of all devices' samples: pctl[0..2] nearest-rank p50/p90/p99, pctl[3] the
+ * mean (correctly rounded from the exact sum); NaN without samples.  *totals:
+ * counters summed, peaks maxed (d_summary may be NULL).  Three replay passes
+ * (radix select over the f64 bit patterns). */
+colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets, const double* d_arrival,
+                                 const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
+                                 const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev,
+                                 const colo_colocated_opts* opts, double* pctl, colo_colocated_summary* totals);
+
 /* --------------------------------------------------------- trace synthesis */
 /* generate_trace (workload.hpp:193-220) on the host, bit-exact (mt19937_64 +
  * libm log).  dist kind: 0 fixed, 1 uniform, 2 histogram.  Returns the query
@@ -325,7 +415,11 @@ typedef struct colo_dist {
     uint64_t min_tokens; /* 0 = none */
 } colo_dist;
 int64_t colo_generate_trace(double qps, double duration, const colo_dist* lengths, const colo_dist* label_delay,
-                            uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, size_t cap);
+                            uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, double* label_out,
+                            size_t cap);
+/* label_out (may be NULL): per-query label delay, sample_seconds of the
+ * label-delay distribution (workload.hpp:118-120), -1.0 when label_delay is
+ * NULL (QueryRecord::label_delay == nullopt). */
 
 /* Bench-scale synthetic trace on the device (counter-based hash RNG, not
  * mt19937): per device d, queries [off[d], off[d+1]) get histogram-sampled

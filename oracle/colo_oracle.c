@@ -605,7 +605,8 @@ static double sample_raw(const orc_dist* d, mt64* s) {
 /* workload.hpp:193-220 (output_tokens fixed at 128, :214); returns the number
  * of queries, or -1 when `cap` is too small. */
 int64_t orc_generate_trace(double qps, double duration, const orc_dist* lengths, const orc_dist* label_delay,
-                           uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, size_t cap) {
+                           uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, double* label_out,
+                           size_t cap) {
     mt64 s;
     mt64_seed(&s, seed);
     double t = 0;
@@ -620,7 +621,12 @@ int64_t orc_generate_trace(double qps, double duration, const orc_dist* lengths,
         arrival[n] = t;
         prompt[n] = (uint32_t)tok;
         output[n] = 128;
-        if (label_delay) (void)sample_raw(label_delay, &s); /* consumes the same draws */
+        double ld = -1.0; /* nullopt (content_hash convention, workload.hpp:156) */
+        if (label_delay) { /* sample_seconds, workload.hpp:118-120 */
+            double raw = sample_raw(label_delay, &s);
+            ld = 0.0 < raw ? raw : 0.0;
+        }
+        if (label_out) label_out[n] = ld;
         ++n;
     }
     return (int64_t)n;

@@ -87,6 +87,39 @@ class Summary(C.Structure):
     ]
 
 
+class ColoReport(C.Structure):
+    """orc_colo_report (colo_oracle.h): MetricsReport fields (metrics.hpp:17-44) + replay extras."""
+
+    _fields_ = [
+        ("generated_tokens", C.c_uint64),
+        ("trained_tokens", C.c_uint64),
+        ("training_busy_time", C.c_double),
+        ("peak_device_bytes", C.c_uint64),
+        ("peak_training_activation_bytes", C.c_uint64),
+        ("preemptions", C.c_uint64),
+        ("layers_freed", C.c_uint64),
+        ("loads", C.c_uint64),
+        ("recomputes", C.c_uint64),
+        ("copy_stall_seconds", C.c_double),
+        ("labels_dropped", C.c_uint64),
+        ("prefetch_wait_seconds", C.c_double),
+        ("completed_jobs", C.c_uint64),
+        ("map_fallbacks", C.c_uint64),
+        ("batches", C.c_uint64),
+        ("max_batch_size", C.c_uint64),
+        ("offload_decisions", C.c_uint64),
+        ("admissions", C.c_uint64),
+        ("slow_tokens", C.c_uint64),
+        ("slow_queries", C.c_uint64),
+        ("end_time", C.c_double),
+        ("status", C.c_uint64),
+    ]
+
+
+# MetricsReport fields the reference itself reports (metrics.hpp:17-44)
+METRICS_FIELDS = [f for f, _ in ColoReport._fields_[:14]]
+
+
 class Dist(C.Structure):
     _fields_ = [
         ("kind", C.c_int),
@@ -175,7 +208,7 @@ class OracleLib:
             "hedge_recompute_time": (C.c_double, [MP, C.c_int, C.c_uint64, C.c_uint64, ip]),
             "hedge_residual_load_time": (C.c_double, [MP, GP, C.c_uint64, C.c_uint64, ip]),
             "finalize": (C.c_int, [f64p, C.c_size_t] + [C.POINTER(C.c_double)] * 4),
-            "generate_trace": (C.c_int64, [C.c_double, C.c_double, C.POINTER(Dist), C.POINTER(Dist), C.c_uint64, f64p, u32p, u32p, C.c_size_t]),
+            "generate_trace": (C.c_int64, [C.c_double, C.c_double, C.POINTER(Dist), C.POINTER(Dist), C.c_uint64, f64p, u32p, u32p, C.c_void_p, C.c_size_t]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, p + name)
@@ -374,6 +407,53 @@ class OracleLib:
         res["pctl"] = pctl
         return res
 
+    def replay_colocated(self, m, g, grid, cpa, arrival, prompt, output, label_delay=None, cache_timeout=60.0,
+                         tau=float("inf"), want_samples=True, want_batches=True):
+        """Colocated replay (Simulation::run, SimMode::Colocated; maps from build_maps).
+        label_delay: per-query seconds, < 0 = nullopt (None = all nullopt).
+        Returns dict(report, samples, labels, batches, pctl, rc)."""
+        arrival = np.ascontiguousarray(arrival, np.float64)
+        prompt = np.ascontiguousarray(prompt, np.uint32)
+        output = np.ascontiguousarray(output, np.uint32)
+        ld = None if label_delay is None else np.ascontiguousarray(label_delay, np.float64)
+        n = len(prompt)
+        ns = int(output.astype(np.uint64).sum())
+        samples = np.zeros(max(ns, 1), np.float64) if want_samples else None
+        labels = np.zeros(max(n, 1), np.uint8)
+        batches = np.zeros(max(n, 1), BATCH_DTYPE) if want_batches else None
+        rep = ColoReport()
+        vp = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None
+        pctl = None
+        if self.which == "ref":
+            pctl = np.full(4, np.nan)
+            rc = self.lib.ref_replay_colocated(C.byref(m), C.byref(g), C.byref(grid), C.c_int(int(cpa)),
+                                               C.c_double(cache_timeout), vp(arrival), vp(prompt), vp(output), vp(ld),
+                                               C.c_uint64(n), vp(samples), vp(batches), C.byref(rep), vp(pctl))
+            labels = None
+        else:
+            off = self.build_offloading_map(m, g, grid, cpa)
+            hed = self.build_hedging_map(m, g, grid.cached_step, grid.max_cached, cpa, 128)
+            mp = Maps(grid, off.ctypes.data, grid.cached_step, grid.max_cached, hed.ctypes.data, m.num_layers)
+            rc = self.lib.orc_replay_colocated(C.byref(m), C.byref(g), C.byref(mp), C.c_int(int(cpa)),
+                                               C.c_double(cache_timeout), vp(arrival), vp(prompt), vp(output), vp(ld),
+                                               C.c_uint64(n), C.c_double(tau), vp(samples), vp(labels), vp(batches),
+                                               C.byref(rep))
+            labels = labels[:n]
+        if rc not in (0, 3):
+            raise ValueError(f"replay_colocated rc={rc}")
+        ng = rep.generated_tokens if rc == 0 else 0
+        res = {
+            "rc": rc,
+            "report": {f: getattr(rep, f) for f, _ in ColoReport._fields_},
+            "samples": samples[:ng] if samples is not None else None,
+            "labels": labels,
+            "batches": batches[: rep.batches] if batches is not None else None,
+        }
+        if pctl is None and samples is not None and ng:
+            pctl = np.array(self.finalize(res["samples"]))
+        res["pctl"] = pctl
+        return res
+
     def finalize(self, samples):
         s = np.ascontiguousarray(samples, np.float64)
         a, b, c, d = C.c_double(), C.c_double(), C.c_double(), C.c_double()
@@ -382,8 +462,9 @@ class OracleLib:
             raise ValueError("finalize on empty samples")
         return a.value, b.value, c.value, d.value
 
-    def generate_trace(self, qps, duration, lengths, seed, label_delay=None, cap=None):
-        """lengths/label_delay: ('fixed', v) | ('uniform', lo, hi) | ('histogram', values, probs); optional min_tokens kw."""
+    def generate_trace(self, qps, duration, lengths, seed, label_delay=None, cap=None, with_labels=False):
+        """lengths/label_delay: ('fixed', v) | ('uniform', lo, hi) | ('histogram', values, probs); optional min_tokens kw.
+        with_labels: also return the per-query label delays (-1.0 = nullopt)."""
         keep = []
 
         def mk(spec):
@@ -408,9 +489,13 @@ class OracleLib:
         if cap is None:
             cap = int(qps * duration * 1.5 + 1000)
         arr, pr, out = np.zeros(cap), np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
-        n = self._generate_trace(qps, duration, C.byref(ld), C.byref(dd) if dd is not None else None, seed, arr, pr, out, cap)
+        lab = np.zeros(cap)
+        n = self._generate_trace(qps, duration, C.byref(ld), C.byref(dd) if dd is not None else None, seed, arr, pr, out,
+                                 lab.ctypes.data, cap)
         if n < 0:
             raise ValueError(f"generate_trace rc={n}")
+        if with_labels:
+            return arr[:n].copy(), pr[:n].copy(), out[:n].copy(), lab[:n].copy()
         return arr[:n].copy(), pr[:n].copy(), out[:n].copy()
 
 

@@ -407,6 +407,98 @@ int ref_replay_serving(const orc_model* m, const orc_gpu* g, const double* arriv
     }
 }
 
+/* Colocated replay through the reference's own Simulation::run in
+ * SimMode::Colocated (engine.hpp:140-822) with maps from build_maps
+ * (experiment.hpp:144-152: hedge grid = the offload grid's cached axis,
+ * assumed output 128).  label_delay[i] < 0 (or NULL) = nullopt.  Fills the
+ * MetricsReport fields of orc_colo_report, pctl[0..3] (p50/p90/p99/mean, NaN
+ * without samples) and the raw samples; returns ORC_EBREACH when the run
+ * throws InvariantBreach / std::logic_error, ORC_EVALIDATION for a refused
+ * configuration.  batches: (start, end, first, n) from the event log. */
+int ref_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_grid* grid, int cpa, double cache_timeout,
+                         const double* arrival, const uint32_t* prompt, const uint32_t* output,
+                         const double* label_delay, uint64_t n, double* samples, orc_batch* batches,
+                         orc_colo_report* out, double* pctl) {
+    std::memset(out, 0, sizeof *out);
+    try {
+        SimConfig cfg;
+        cfg.mode = SimMode::Colocated;
+        cfg.training = to_mode(cpa);
+        cfg.model = to_model(m);
+        cfg.gpu = to_gpu(g);
+        cfg.cache_timeout = cache_timeout;
+        cfg.collect_events = batches != nullptr;
+        Maps mp = make_maps(m, g, grid, cpa, grid->cached_step, grid->max_cached, 128);
+        cfg.offload_map = mp.off;
+        cfg.hedge_map = mp.hedge;
+        for (uint64_t i = 0; i < n; ++i) {
+            QueryRecord r;
+            r.query_id = i;
+            r.arrival_time = arrival[i];
+            r.prompt_tokens = prompt[i];
+            r.output_tokens = output[i];
+            if (label_delay && label_delay[i] >= 0) r.label_delay = label_delay[i];
+            cfg.trace.records.push_back(r);
+        }
+        validate_trace(cfg.trace);
+        Simulation sim(cfg);
+        MetricsReport rep;
+        try {
+            rep = sim.run();
+        } catch (const InvariantBreach&) {
+            out->status = ORC_EBREACH;
+            return ORC_EBREACH;
+        } catch (const std::logic_error&) {
+            out->status = ORC_EBREACH;
+            return ORC_EBREACH;
+        }
+        out->generated_tokens = rep.generated_tokens;
+        out->trained_tokens = rep.trained_tokens;
+        out->training_busy_time = rep.training_busy_time;
+        out->peak_device_bytes = rep.peak_device_bytes;
+        out->peak_training_activation_bytes = rep.peak_training_activation_bytes;
+        out->preemptions = rep.preemptions;
+        out->layers_freed = rep.layers_freed;
+        out->loads = rep.loads;
+        out->recomputes = rep.recomputes;
+        out->copy_stall_seconds = rep.copy_stall_seconds;
+        out->labels_dropped = rep.labels_dropped;
+        out->prefetch_wait_seconds = rep.prefetch_wait_seconds;
+        out->completed_jobs = rep.completed_jobs;
+        out->map_fallbacks = rep.map_fallbacks;
+        const double nan = std::nan("");
+        if (pctl) {
+            pctl[0] = rep.tpt_p50 ? *rep.tpt_p50 : nan;
+            pctl[1] = rep.tpt_p90 ? *rep.tpt_p90 : nan;
+            pctl[2] = rep.tpt_p99 ? *rep.tpt_p99 : nan;
+            pctl[3] = rep.tpt_mean ? *rep.tpt_mean : nan;
+        }
+        if (samples) std::memcpy(samples, rep.tpt_samples.data(), rep.tpt_samples.size() * sizeof(double));
+        if (batches) {
+            uint64_t head = 0, b = 0;
+            double last_step = 0;
+            for (const auto& e : sim.events()) {
+                if (e.kind == EventKind::PrefillDone) {
+                    if (b) batches[b - 1].end = last_step;
+                    orc_batch& rb = batches[b++];
+                    std::memset(&rb, 0, sizeof rb);
+                    rb.start = e.start;
+                    rb.first = static_cast<uint32_t>(head);
+                    rb.n = static_cast<uint32_t>(e.a);
+                    head += static_cast<uint64_t>(e.a);
+                } else if (e.kind == EventKind::DecodeStepDone) {
+                    last_step = e.time;
+                }
+            }
+            if (b) batches[b - 1].end = last_step;
+            out->batches = b;
+        }
+        return ORC_OK;
+    } catch (const std::exception&) {
+        return ORC_EVALIDATION;
+    }
+}
+
 int ref_finalize(const double* samples, size_t n, double* p50, double* p90, double* p99, double* mean) {
     if (n == 0) return ORC_EINVAL;
     MetricsReport r;
@@ -433,7 +525,8 @@ static LengthDistribution to_dist(const orc_dist* d) {
 }
 
 int64_t ref_generate_trace(double qps, double duration, const orc_dist* lengths, const orc_dist* label_delay,
-                           uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, size_t cap) {
+                           uint64_t seed, double* arrival, uint32_t* prompt, uint32_t* output, double* label_out,
+                           size_t cap) {
     try {
         std::optional<LengthDistribution> ld;
         if (label_delay) ld = to_dist(label_delay);
@@ -443,6 +536,7 @@ int64_t ref_generate_trace(double qps, double duration, const orc_dist* lengths,
             arrival[i] = t.records[i].arrival_time;
             prompt[i] = static_cast<uint32_t>(t.records[i].prompt_tokens);
             output[i] = static_cast<uint32_t>(t.records[i].output_tokens);
+            if (label_out) label_out[i] = t.records[i].label_delay ? *t.records[i].label_delay : -1.0;
         }
         return static_cast<int64_t>(t.records.size());
     } catch (const std::exception&) {

@@ -32,6 +32,10 @@ class ColoInvalidArgument(ColoError, ValueError):
     """COLO_EINVAL -- where the reference throws std::invalid_argument."""
 
 
+class ColoBreachError(ColoError):
+    """COLO_EBREACH -- where the reference throws InvariantBreach (engine.hpp:43-46)."""
+
+
 class Model(C.Structure):
     _fields_ = [
         ("num_layers", C.c_uint64),
@@ -89,6 +93,57 @@ class ReplayOpts(C.Structure):
     ]
 
 
+class ColocatedSummary(C.Structure):
+    """colo_colocated_summary: MetricsReport fields (metrics.hpp:17-44) + replay extras."""
+
+    _fields_ = [
+        ("generated_tokens", C.c_uint64),
+        ("trained_tokens", C.c_uint64),
+        ("training_busy_time", C.c_double),
+        ("peak_device_bytes", C.c_uint64),
+        ("peak_training_activation_bytes", C.c_uint64),
+        ("preemptions", C.c_uint64),
+        ("layers_freed", C.c_uint64),
+        ("loads", C.c_uint64),
+        ("recomputes", C.c_uint64),
+        ("copy_stall_seconds", C.c_double),
+        ("labels_dropped", C.c_uint64),
+        ("prefetch_wait_seconds", C.c_double),
+        ("completed_jobs", C.c_uint64),
+        ("map_fallbacks", C.c_uint64),
+        ("batches", C.c_uint64),
+        ("max_batch_size", C.c_uint64),
+        ("offload_decisions", C.c_uint64),
+        ("admissions", C.c_uint64),
+        ("slow_tokens", C.c_uint64),
+        ("slow_queries", C.c_uint64),
+        ("end_time", C.c_double),
+        ("status", C.c_uint64),
+        ("tpt_sum", C.c_uint64 * 3),
+        ("flags", C.c_uint64),
+    ]
+
+
+class ColocatedOpts(C.Structure):
+    _fields_ = [
+        ("cache_timeout", C.c_double),
+        ("d_label_delay", C.c_void_p),
+        ("default_label_delay", C.c_double),
+        ("tau", C.c_double),
+        ("d_samples", C.c_void_p),
+        ("d_sample_offsets", C.c_void_p),
+        ("d_labels", C.c_void_p),
+        ("d_batches", C.c_void_p),
+        ("d_summary", C.c_void_p),
+        ("d_hist", C.c_void_p),
+        ("nfilters", C.c_uint32),
+        ("hist_shift", C.c_uint32),
+        ("filter_shift", C.c_uint32),
+        ("pad", C.c_uint32),
+        ("filter_prefix", C.c_uint64 * 3),
+    ]
+
+
 class Dist(C.Structure):
     _fields_ = [
         ("kind", C.c_int),
@@ -104,6 +159,7 @@ class Dist(C.Structure):
 
 assert C.sizeof(Model) == 96 and C.sizeof(Gpu) == 32 and C.sizeof(Grid) == 48
 assert C.sizeof(DeviceSummary) == 88
+assert C.sizeof(ColocatedSummary) == 208
 
 # Every symbol include/colo_abi.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -116,7 +172,7 @@ EXPORTS = [
     "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
     "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
     "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
-    "colo_load_histogram_jsonl",
+    "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats",
 ]
 
 
@@ -169,7 +225,10 @@ def lib() -> C.CDLL:
         "colo_hist_select": (i32, [vp, sz, u64, C.POINTER(C.c_uint32), C.POINTER(u64)]),
         "colo_nearest_rank_index": (u64, [dbl, u64]),
         "colo_serving_stats": (i32, [vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp, C.POINTER(DeviceSummary)]),
-        "colo_generate_trace": (C.c_int64, [dbl, dbl, C.POINTER(Dist), C.POINTER(Dist), u64, vp, vp, vp, sz]),
+        "colo_generate_trace": (C.c_int64, [dbl, dbl, C.POINTER(Dist), C.POINTER(Dist), u64, vp, vp, vp, vp, sz]),
+        "colo_replay_colocated": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts)]),
+        "colo_colocated_stats": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts), vp,
+                                       C.POINTER(ColocatedSummary)]),
         "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, u64, vp, vp, vp]),
         "colo_synth_tuples": (i32, [vp, u64, sz, C.c_uint32, vp, vp, sz, vp]),
         "colo_compare_verdicts": (i32, [vp, vp, vp, sz, C.c_uint32, vp]),
@@ -200,4 +259,6 @@ def check(status: int, ctx=None, what: str = "") -> None:
         raise ColoValidationError(status, detail)
     if status == COLO_EINVAL:
         raise ColoInvalidArgument(status, detail)
+    if status == COLO_EBREACH:
+        raise ColoBreachError(status, detail)
     raise ColoError(status, detail)

@@ -25,7 +25,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from ._lib import ColoError, ColoInvalidArgument, ColoValidationError, HIST_BINS, NCOUNTERS, check, lib
+from ._lib import ColoBreachError, ColoError, ColoInvalidArgument, ColoValidationError, HIST_BINS, NCOUNTERS, check, lib
 
 KIB, MIB, GIB = 1024, 1024**2, 1024**3
 KB, MB, GB = 1000, 1000**2, 1000**3
@@ -773,6 +773,110 @@ def serving_stats_c(ctx: Context, profiles, arrival, prompt, output, dev_offsets
     return list(pctl), tot
 
 
+# ------------------------------------------------------------- colocated replay
+
+COLOCATED_FIELDS = [f for f, _ in _lib.ColocatedSummary._fields_]
+# MetricsReport fields the reference reports per run (metrics.hpp:17-44)
+METRICS_FIELDS = COLOCATED_FIELDS[:14]
+
+
+def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay, default_label_delay,
+                    cache_timeout, tau, samples, labels, batches, summary, res, keep):
+    torch = _torch()
+    dev = prompt.device
+    _need_cuda(arrival, "arrival", 8)
+    _need_cuda(prompt, "prompt", 4)
+    _need_cuda(output, "output", 4)
+    _need_cuda(dev_offsets, "dev_offsets", 8)
+    _need_cuda(dev_set, "dev_set", 2)
+    n = prompt.shape[0]
+    ndev = dev_set.shape[0]
+    o = _lib.ColocatedOpts()
+    o.cache_timeout = cache_timeout
+    o.default_label_delay = default_label_delay
+    o.tau = tau
+    if label_delay is not None:
+        _need_cuda(label_delay, "label_delay", 8)
+        o.d_label_delay = label_delay.data_ptr()
+    if samples:
+        o64 = output.to(torch.int64)
+        cs = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(o64, 0)])
+        per_dev = cs[dev_offsets].contiguous()
+        total = int(per_dev[-1].item())
+        res["samples"] = torch.empty(max(total, 1), dtype=torch.float64, device=dev)[:total]
+        res["sample_offsets"] = per_dev
+        o.d_samples = res["samples"].data_ptr() if total else torch.empty(1, dtype=torch.float64, device=dev).data_ptr()
+        o.d_sample_offsets = per_dev.data_ptr()
+    if labels:
+        res["labels"] = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)[:n]
+        o.d_labels = res["labels"].data_ptr() if n else 0
+    if batches:
+        res["batches"] = torch.zeros((max(n, 1), BATCH_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        o.d_batches = res["batches"].data_ptr()
+    if summary:
+        res["summary"] = torch.zeros((max(ndev, 1), C.sizeof(_lib.ColocatedSummary)), dtype=torch.uint8, device=dev)
+        o.d_summary = res["summary"].data_ptr()
+    arr = _sets_array(sets)
+    keep.append(arr)
+    return o, arr, n, ndev
+
+
+def replay_colocated(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
+                     label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
+                     tau: float = math.inf, samples: bool = False, labels: bool = True, batches: bool = False,
+                     summary: bool = True):
+    """Colocated replay of every device (Simulation::run, SimMode::Colocated,
+    engine.hpp:140-822).  Device d runs with map set ``sets[dev_set[d]]`` and
+    that set's model, GPU profile and training mode (SimConfig::validate,
+    engine.hpp:60-68).  ``label_delay``: optional f64 device tensor per query
+    (< 0 or NaN = the label never arrives); otherwise every query uses
+    ``default_label_delay`` (the reference's TraceSpec default is fixed 0.01 s,
+    experiment.hpp:45).  Raises ColoBreachError if a device's run breaches an
+    invariant (the reference throws InvariantBreach).
+    Returns a dict of device tensors: samples, labels, batches (BATCH_DTYPE
+    bytes at d_dev_offsets[d] + b), summary (ColocatedSummary bytes)."""
+    res, keep = {}, []
+    o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
+                                      default_label_delay, cache_timeout, tau, samples, labels, batches, summary,
+                                      res, keep)
+    try:
+        check(lib().colo_replay_colocated(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),
+                                          _ptr(output), n, _ptr(dev_offsets), _ptr(dev_set), ndev, C.byref(o)),
+              ctx.h, "replay_colocated")
+    except ColoBreachError as e:
+        e.result = res  # per-device summaries carry status COLO_EBREACH where the run broke
+        raise
+    return res
+
+
+def colocated_summaries(summary_bytes) -> list:
+    """ColocatedSummary bytes -> list of dicts (one per device)."""
+    a = summary_bytes.cpu().numpy() if hasattr(summary_bytes, "cpu") else np.asarray(summary_bytes)
+    a = np.ascontiguousarray(a)
+    out = []
+    for row in a.reshape(-1, C.sizeof(_lib.ColocatedSummary)):
+        s = _lib.ColocatedSummary.from_buffer_copy(row.tobytes())
+        out.append({f: (list(getattr(s, f)) if f == "tpt_sum" else getattr(s, f)) for f in COLOCATED_FIELDS})
+    return out
+
+
+def colocated_stats(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
+                    label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
+                    tau: float = math.inf):
+    """colo_colocated_stats: colocated replays of every device + exact
+    nearest-rank p50/p90/p99 and mean of the union of their TPT samples
+    (finalize, metrics.hpp:56-69).  Returns (pctl[4], totals dict)."""
+    res, keep = {}, []
+    o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
+                                      default_label_delay, cache_timeout, tau, False, False, False, False, res, keep)
+    pctl = (C.c_double * 4)()
+    tot = _lib.ColocatedSummary()
+    check(lib().colo_colocated_stats(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),
+                                     _ptr(output), n, _ptr(dev_offsets), _ptr(dev_set), ndev, C.byref(o), pctl,
+                                     C.byref(tot)), ctx.h, "colocated_stats")
+    return list(pctl), {f: (list(getattr(tot, f)) if f == "tpt_sum" else getattr(tot, f)) for f in COLOCATED_FIELDS}
+
+
 # ------------------------------------------------------------- workload
 def _dist(spec):
     if spec is None:
@@ -794,20 +898,24 @@ def _dist(spec):
     return d, keep
 
 
-def generate_trace(qps: float, duration: float, lengths, seed: int, label_delay=None, min_tokens: int = 0):
-    """workload.hpp:193-220 on the host, bit-exact (returns arrival, prompt, output numpy arrays).
+def generate_trace(qps: float, duration: float, lengths, seed: int, label_delay=None, min_tokens: int = 0,
+                   with_labels: bool = False):
+    """workload.hpp:193-220 on the host, bit-exact (returns arrival, prompt, output numpy arrays, plus the
+    per-query label delays -- -1.0 = nullopt -- when ``with_labels``).
     lengths/label_delay: ('fixed', v) | ('uniform', lo, hi) | ('histogram', values, probs)."""
     ld, k1 = _dist(lengths)
     ld.min_tokens = min_tokens
     dd, k2 = _dist(label_delay)
     cap = int(qps * duration * 1.3 + 64 * math.sqrt(qps * duration + 1) + 1000)
-    arr, pr, out = np.empty(cap), np.empty(cap, np.uint32), np.empty(cap, np.uint32)
+    arr, pr, out, lab = np.empty(cap), np.empty(cap, np.uint32), np.empty(cap, np.uint32), np.empty(cap)
     n = lib().colo_generate_trace(qps, duration, C.byref(ld), C.byref(dd) if dd is not None else None, seed,
-                                  arr.ctypes.data, pr.ctypes.data, out.ctypes.data, cap)
+                                  arr.ctypes.data, pr.ctypes.data, out.ctypes.data, lab.ctypes.data, cap)
     if n == -2:
         raise ColoValidationError(_lib.COLO_EVALIDATION, "generate_trace: invalid qps/duration/distribution")
     if n < 0:
         raise ColoError(_lib.COLO_EINVAL, "generate_trace: capacity exceeded")
+    if with_labels:
+        return arr[:n].copy(), pr[:n].copy(), out[:n].copy(), lab[:n].copy()
     return arr[:n].copy(), pr[:n].copy(), out[:n].copy()
 
 

@@ -300,7 +300,7 @@ double sample_raw(const colo_dist* d, std::mt19937_64& g) {
 
 extern "C" int64_t colo_generate_trace(double qps, double duration, const colo_dist* lengths,
                                        const colo_dist* label_delay, uint64_t seed, double* arrival, uint32_t* prompt,
-                                       uint32_t* output, size_t cap) {
+                                       uint32_t* output, double* label_out, size_t cap) {
     if (!(qps > 0) || !(duration > 0) || !lengths || !dist_valid(lengths) || !dist_valid(label_delay)) return -2;
     std::mt19937_64 gen(seed);
     double t = 0;
@@ -315,7 +315,9 @@ extern "C" int64_t colo_generate_trace(double qps, double duration, const colo_d
         arrival[n] = t;
         prompt[n] = static_cast<uint32_t>(tok);
         output[n] = 128;  // workload.hpp:214
-        if (label_delay) (void)sample_raw(label_delay, gen);
+        double ld = -1.0;  // nullopt
+        if (label_delay) ld = std::max(0.0, sample_raw(label_delay, gen));  // sample_seconds, workload.hpp:118-120
+        if (label_out) label_out[n] = ld;
         ++n;
     }
     return static_cast<int64_t>(n);

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "colo_internal.h"
+#include "colo_replay.cuh"
 
 using namespace colo;
 
@@ -104,95 +105,6 @@ struct ReplayParams {
     uint64_t prefix[3];
     int* err;
 };
-
-__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) v = max(v, __shfl_xor_sync(FULL, v, s));
-    return v;
-}
-
-__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(FULL, v, s);
-    return v;
-}
-
-// 192-bit fixed-point accumulation (LSB 2^-96) of s * mult.  flags bit0: a
-// sample below the representable range was truncated; bit1: overflow.
-__device__ __forceinline__ void add3(uint64_t (&a)[3], uint64_t w0, uint64_t w1, uint64_t w2) {
-    const uint64_t t0 = a[0] + w0;
-    const uint64_t c0 = t0 < w0;
-    const uint64_t t1 = a[1] + w1;
-    uint64_t c1 = t1 < w1;
-    const uint64_t t1b = t1 + c0;
-    c1 |= t1b < c0;
-    a[0] = t0;
-    a[1] = t1b;
-    a[2] = a[2] + w2 + c1;
-}
-
-__device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, double s, uint32_t mult) {
-    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
-    const uint32_t ex = static_cast<uint32_t>(bits >> 52) & 0x7ffu;
-    const uint64_t frac = bits & ((1ull << 52) - 1);
-    if (ex == 0) {
-        if (frac) flags |= 1u;
-        return;
-    }
-    uint64_t m = frac | (1ull << 52);
-    int sh = static_cast<int>(ex) - 1075 + 96;
-    if (sh < 0) {
-        flags |= 1u;
-        if (sh <= -53) return;
-        m >>= -sh;
-        sh = 0;
-    }
-    const uint64_t lo = m * mult, hi = __umul64hi(m, static_cast<uint64_t>(mult));
-    const int q = sh >> 6, r = sh & 63;
-    const uint64_t x0 = lo << r;
-    const uint64_t x1 = r ? ((lo >> (64 - r)) | (hi << r)) : hi;
-    const uint64_t x2 = r ? (hi >> (64 - r)) : 0ull;
-    if (q == 0) {
-        add3(a, x0, x1, x2);
-    } else if (q == 1) {
-        if (x2) flags |= 2u;
-        add3(a, 0, x0, x1);
-    } else if (q == 2) {
-        if (x1 | x2) flags |= 2u;
-        add3(a, 0, 0, x0);
-    } else {
-        flags |= 2u;
-    }
-}
-
-// First index >= from whose arrival is > T (or N): every arrival at or before
-// T has been popped by the time the batch starts (engine.hpp:146-147,184-187).
-// Arrivals are sorted, so the warp gallops with 32 probes per step (stride
-// x32) and then refines (stride /32): O(log32 distance) dependent loads, so a
-// saturated server's backlog of millions of queued arrivals costs a handful
-// of steps instead of a linear scan.
-__device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, uint64_t N, uint64_t from, double T) {
-    const uint32_t lane = threadIdx.x & 31;
-    uint64_t lo = from;  // every index in [from, lo) has arrival <= T
-    uint64_t stride = 1;
-    bool gallop = true;
-    while (lo < N) {
-        const uint64_t p = lo + (lane + 1) * stride - 1;
-        const bool le = p < N && arr[p] <= T;
-        const uint32_t bal = __ballot_sync(FULL, le);
-        if (bal == FULL && gallop) {
-            lo += 32 * stride;
-            stride *= 32;
-            continue;
-        }
-        gallop = false;
-        const uint32_t f = __ffs(~bal) - 1;  // bal != FULL once refining (the answer lies in the window)
-        lo += f * stride;
-        if (stride == 1) break;
-        stride /= 32;
-    }
-    return lo < N ? lo : N;
-}
 
 enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
 

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle.oracle import (Grid, OracleLib, TUPLE_DTYPE, default_gpu, default_grid, default_model, phi14b_model,  # noqa: E402
+from oracle.oracle import (KGB, KGIB, Grid, OracleLib, TUPLE_DTYPE, default_gpu, default_grid, default_model, phi14b_model,  # noqa: E402
                            sharegpt_histogram)
 
 
@@ -167,5 +167,88 @@ def main():
             print(f, os.path.getsize(os.path.join(HERE, f)))
 
 
+def colocated_cases(ref):
+    """Colocated-replay cases (Simulation::run, SimMode::Colocated): name ->
+    (model, gpu, grid, cpa, cache_timeout, arrival, prompt, output, label_delay)."""
+    hv, hp = sharegpt_histogram()
+    m, g, grid = default_model(), default_gpu(), default_grid()
+    cases = {}
+    a, p, o, ld = ref.generate_trace(0.3, 600.0, ("histogram", hv, hp), 41, ("fixed", 0.01), with_labels=True)
+    cases["sharegpt_q03_cpa"] = (m, g, grid, 1, 60.0, a, p, o, ld)
+    cases["sharegpt_q03_cpt"] = (m, g, grid, 0, 60.0, a, p, o, ld)
+    a, p, o, ld = ref.generate_trace(1.7, 150.0, ("histogram", hv, hp), 42, ("fixed", 0.01), with_labels=True)
+    cases["sharegpt_q17_cpa"] = (m, g, grid, 1, 60.0, a, p, o, ld)
+    a, p, o, ld = ref.generate_trace(0.14, 1200.0, ("uniform", 4000, 7000), 5, ("uniform", 0.0, 30.0), with_labels=True)
+    cases["long_q014_cpa_t5"] = (m, g, grid, 1, 5.0, a, p, o, ld)
+    cases["long_q014_cpt"] = (m, g, grid, 0, 60.0, a, p, o, ld)
+    a, p, o, ld = ref.generate_trace(0.2, 900.0, ("uniform", 2000, 7000), 9, ("fixed", 0.01), with_labels=True)
+    cases["phi_q02_cpa"] = (phi14b_model(), g, Grid(250, 250, 5, 8000, 8000, 50), 1, 60.0, a, p, o, ld)
+    cases["phi_q02_cpt"] = (phi14b_model(), g, grid, 0, 60.0, a, p, o, ld)
+    a, p, o, ld = ref.generate_trace(0.1, 1500.0, ("uniform", 100, 9000), 7, ("uniform", 0.0, 100.0), with_labels=True)
+    o = (np.arange(len(a)) * 37 % 199 + 1).astype(np.uint32)  # variable outputs
+    cases["wide_varout_cpa"] = (m, g, grid, 1, 60.0, a, p, o, ld)
+    # engine test cases (tests/test_engine.cpp:186-265)
+    g2 = default_gpu()
+    g2.d2h_bandwidth, g2.h2d_bandwidth = 2 * KGB, 1000 * KGB
+    cases["copy_stall"] = (m, g2, grid, 1, 60.0, np.array([0.0] + [5.0] * 10), np.full(11, 4000, np.uint32),
+                           np.full(11, 128, np.uint32), np.full(11, -1.0))
+    cases["offload_path"] = (m, g, grid, 1, 60.0, np.array([0.0] + [4.6 + 0.001 * i for i in range(1, 11)]),
+                             np.array([4000] + [2000] * 10, np.uint32), np.full(11, 128, np.uint32),
+                             np.array([0.01] + [-1.0] * 10))
+    cases["stream_6000"] = (m, g, grid, 1, 60.0, np.array([0.0, 2000.0]), np.array([6000, 6000], np.uint32),
+                            np.full(2, 128, np.uint32), np.array([0.01, 0.01]))
+    cases["late_label"] = (m, g, grid, 1, 60.0, np.array([0.0, 10.0]), np.array([1000, 1000], np.uint32),
+                           np.full(2, 128, np.uint32), np.array([3600.0, 0.01]))
+    cases["empty"] = (m, g, grid, 1, 60.0, np.zeros(0), np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0))
+    # an InvariantBreach: small device, slow copies (found by fuzzing the reference)
+    g3 = default_gpu()
+    g3.capacity_bytes, g3.d2h_bandwidth, g3.h2d_bandwidth = 80 * KGIB, 2 * KGB, 200 * KGB
+    a, p, o, ld = ref.generate_trace(0.3, 40 / 0.3 + 200, ("uniform", 6735.0, 8213.0), 206955, ("uniform", 0.0, 0.01),
+                                     with_labels=True)
+    cases["breach_slow_d2h"] = (m, g3, grid, 1, 60.0, a, p, o, ld)
+    g4 = default_gpu()
+    g4.capacity_bytes, g4.d2h_bandwidth, g4.h2d_bandwidth = 40 * KGIB, 1 * KGB, 200 * KGB
+    a, p, o, ld = ref.generate_trace(0.1, 40 / 0.1 + 200, ("uniform", 6519.0, 8610.0), 867572, ("uniform", 0.0, 5.0),
+                                     with_labels=True)
+    cases["breach_small_cpt"] = (m, g4, Grid(250, 500, 5, 8000, 8000, 50), 0, 60.0, a, p, o, ld)
+    return cases
+
+
+def colocated(ref):
+    out = {}
+    names = []
+    for name, (m, g, grid, cpa, to, a, p, o, ld) in colocated_cases(ref).items():
+        r = ref.replay_colocated(m, g, grid, cpa, a, p, o, ld, to)
+        names.append(name)
+        out[f"{name}_model"] = np.frombuffer(bytes(m), np.uint8)
+        out[f"{name}_gpu"] = np.frombuffer(bytes(g), np.uint8)
+        out[f"{name}_grid"] = np.frombuffer(bytes(grid), np.uint8)
+        out[f"{name}_cfg"] = np.array([cpa, to], np.float64)
+        out[f"{name}_a"], out[f"{name}_p"], out[f"{name}_o"], out[f"{name}_ld"] = a, p, o, ld
+        out[f"{name}_rc"] = np.array([r["rc"]])
+        out[f"{name}_report"] = np.frombuffer(bytes(_report_struct(r["report"])), np.uint8)
+        if r["rc"] == 0:
+            out[f"{name}_samples"] = r["samples"]
+            out[f"{name}_pctl"] = r["pctl"]
+            b = r["batches"]
+            out[f"{name}_batches"] = np.stack([b["start"], b["end"], b["first"].astype(np.float64),
+                                               b["n"].astype(np.float64)], 1)
+        print(name, len(a), r["rc"], {k: r["report"][k] for k in ("completed_jobs", "recomputes", "loads", "labels_dropped")})
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "colocated.npz"), **out)
+
+
+def _report_struct(rep):
+    from oracle.oracle import ColoReport
+    c = ColoReport()
+    for f, _ in ColoReport._fields_:
+        setattr(c, f, rep[f])
+    return c
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["colocated"]:
+        colocated(OracleLib("ref"))
+    else:
+        main()
+        colocated(OracleLib("ref"))
