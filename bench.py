@@ -444,6 +444,149 @@ def run_c1(args, world, rank, local):
     ctx.close()
 
 
+def reference_colocated(dev_traces, threads):
+    """The reference's own Simulation::run (SimMode::Colocated) through
+    oracle/_ref, one device per task on all host threads.  dev_traces: list of
+    (model, gpu, cpa, arrival, prompt, output)."""
+    from oracle.oracle import OracleLib, default_grid
+
+    ref = OracleLib("ref")
+    grid = default_grid()
+
+    def one(t):
+        m, g, cpa, a, p, o = t
+        ref.replay_colocated(m, g, grid, cpa, a, p, o, np.full(len(a), 0.01), 60.0, want_samples=False,
+                             want_batches=False)
+        return len(a)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        n = sum(ex.map(one, dev_traces))
+    return n, time.perf_counter() - t0
+
+
+def run_colo(args, world, rank, local):
+    """Colocated replay (the full admission loop).
+    (1) C1 (BASELINE.json configs[0]): the 1M-query single-device trace at
+        qps 0.3 and 1.7 (generate_trace, ShareGPT-like lengths, label delay
+        0.01 s, seed 41), CPA: one warp on the GPU vs the reference's own
+        Simulation::run (oracle/_ref, one host core).
+    (2) Fleet: --colo-devices devices x --colo-per-device queries per GPU
+        (synth_trace, qps 0.05/0.1/0.2/0.3, llama8b/phi14b x CPA/CPT as C2),
+        device-timed replay (samples reduced to exact sums / slow counts); the reference on a bounded
+        device sample across all host threads."""
+    import torch
+
+    from oracle.oracle import default_gpu, default_model, phi14b_model
+    from paper_2503_01066_b200 import colosim as cs
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        init_dist(dist, torch, local)
+    ctx = cs.Context(local)
+    hv, hp = cs.sharegpt_histogram()
+    g = cs.GpuProfile()
+    models = (cs.ModelProfile(), cs.ModelProfile.phi14b_like())
+    sets = [cs.MapSet.build(ctx, m, g, mode=md) for m in models for md in (cs.TrainingMode.CPA, cs.TrainingMode.CPT)]
+    threads = os.cpu_count() or 1
+    c1 = []
+    if rank == 0 and not args.colo_skip_c1:
+        for qps in (0.3, 1.7):
+            a, p, o = cs.generate_trace(qps, 1_000_000 / qps, ("histogram", hv, hp), 41, ("fixed", 0.01))
+            da, dp, do = (torch.from_numpy(a).cuda(), torch.from_numpy(p.view(np.int32)).cuda(),
+                          torch.from_numpy(o.view(np.int32)).cuda())
+            offs = torch.tensor([0, len(p)], dtype=torch.int64, device="cuda")
+            dset = torch.zeros(1, dtype=torch.int16, device="cuda")
+            r = cs.replay_colocated(ctx, sets[:1], da, dp, do, offs, dset, tau=0.05)  # warm
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = cs.replay_colocated(ctx, sets[:1], da, dp, do, offs, dset, tau=0.05)
+            torch.cuda.synchronize()
+            gpu_s = time.perf_counter() - t0
+            S = cs.colocated_summaries(r["summary"])[0]
+            cpu_s = None
+            if not args.no_cpu_baseline:
+                try:
+                    _, cpu_s = reference_colocated([(default_model(), default_gpu(), 1, a, p, o)], 1)
+                except Exception:
+                    cpu_s = None
+            c1.append({"qps": qps, "queries": len(p), "gpu_s": gpu_s, "gpu_queries_per_s": len(p) / gpu_s,
+                       "reference_cpu_s": cpu_s, "reference_queries_per_s": len(p) / cpu_s if cpu_s else None,
+                       "completed_jobs": S["completed_jobs"], "recomputes": S["recomputes"],
+                       "preemptions": S["preemptions"], "batches": S["batches"]})
+    D, per = args.colo_devices, args.colo_per_device
+    arrival, prompt, output, offs = cs.synth_trace(ctx, [per] * D, [QPS[d % 4] for d in range(D)],
+                                                   777 + 7919 * rank)
+    dset = torch.tensor([dev_set_of(d) for d in range(D)], dtype=torch.int16, device="cuda")
+    n = D * per
+
+    def step():
+        return cs.replay_colocated(ctx, sets, arrival, prompt, output, offs, dset, tau=0.05, labels=False)
+
+    for _ in range(max(args.warmup, 1)):
+        r = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            r = step()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    S = cs.colocated_summaries(r["summary"])
+    keys = ("generated_tokens", "trained_tokens", "completed_jobs", "recomputes", "preemptions", "loads",
+            "layers_freed", "labels_dropped", "map_fallbacks", "batches", "offload_decisions", "admissions")
+    tot = torch.tensor([sum(s[k] for s in S) for k in keys], dtype=torch.int64, device="cuda")
+    if dist:
+        dist.all_reduce(tot)
+    sec = float(t.item()) / 1e3
+    value = world * n * args.steps / sec
+    if rank == 0:
+        line = {"metric": "colocated replay queries/s (full admission loop, Simulation::run Colocated)",
+                "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"colocated fleet: {D} devices x {per} queries per GPU (qps 0.05/0.1/0.2/0.3, "
+                                       "llama8b/phi14b x CPA/CPT as C2, label delay 0.01 s, timeout 60 s)",
+                           "parallelism": f"dp{world} (one warp per device)"},
+                "totals": dict(zip(keys, [int(x) for x in tot.cpu().tolist()])),
+                "roofline": {"bound": "latency (sequential per-device event loop)", "achieved": None,
+                             "peak": None, "unit": "GB/s", "frac": None, "traffic": None},
+                "gpu_launches": 2 * args.steps, "clocks": clk.report(), "c1": c1}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                k = min(D, max(threads, 8))
+                offs_h = offs.cpu().numpy()
+                a_h, p_h, o_h = arrival.cpu().numpy(), prompt.cpu().numpy().view(np.uint32), output.cpu().numpy().view(np.uint32)
+                mods = [(default_model(), 1), (default_model(), 0), (phi14b_model(), 1), (phi14b_model(), 0)]
+                tr = []
+                for d in range(k):
+                    lo, hi = int(offs_h[d]), int(offs_h[d + 1])
+                    mm, cpa = mods[dev_set_of(d)]
+                    tr.append((mm, default_gpu(), cpa, a_h[lo:hi], p_h[lo:hi], o_h[lo:hi]))
+                nq, ts = reference_colocated(tr, threads)
+                line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "sample": f"{k} of the fleet's devices ({nq} queries), Simulation::run "
+                                                  f"Colocated via oracle/_ref, {threads} host threads, {ts:.1f} s"}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
 def run_c3(args, world, rank, local):
     """C3 (BASELINE.json configs[2]): 128 bursty devices x 7,812,500 queries =
     1B queries per GPU, serving replay + slow labels + the first exact-stats
@@ -531,9 +674,13 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c5"], default="c2",
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c5", "colo"], default="c2",
                     help="c2 (default, the headline): trace-fused decisions; c1: single-trace replay vs the "
-                         "reference Simulation; c3: 1B-query bursty replay + labels; c5: map vs exact sweep")
+                         "reference Simulation; c3: 1B-query bursty replay + labels; c5: map vs exact sweep; "
+                         "colo: colocated replay (C1 trace + device fleet)")
+    ap.add_argument("--colo-devices", type=int, default=1184)  # 8 resident warps x 148 SMs
+    ap.add_argument("--colo-per-device", type=int, default=50_000)
+    ap.add_argument("--colo-skip-c1", action="store_true")
     ap.add_argument("--c3-devices", type=int, default=C3_DEVICES)
     ap.add_argument("--c3-per-device", type=int, default=C3_PER_DEVICE)
     ap.add_argument("--c5-tuples", type=int, default=1_000_000_000)
@@ -548,6 +695,8 @@ def main():
         run_c3(args, world, rank, local)
     elif args.workload == "c5":
         run_c5(args, world, rank, local)
+    elif args.workload == "colo":
+        run_colo(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

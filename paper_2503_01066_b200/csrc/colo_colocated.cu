@@ -166,6 +166,17 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     uint64_t l_seq = 0, l_gen = 0, to_seq = 0, to_gen = 0;
     uint32_t ld_n = 0, ld_cur = 0;
     uint64_t ld_gen = 0, ld_seq0 = 0;
+    // slot aggregates kept incrementally (recomputed after bulk updates):
+    //   ag_dev  device_act_bytes()       (memory.hpp:91-96)
+    //   ag_cnt  device_resident_layers() (memory.hpp:108-113)
+    //   ag_pend host_only_pending()      (memory.hpp:101-106)
+    //   ag_t    sum of recorded bytes of not consumed / dropped layers (engine.hpp:817-819)
+    uint64_t ag_dev = 0, ag_t = 0;
+    uint32_t ag_cnt = 0, ag_pend = 0;
+    // per-pass constants (recomputed bit-identically when the key changes)
+    uint64_t fwd_tok = ~0ull, cp_bytes = ~0ull;
+    double fwd_val = 0.0, cp_val = 0.0;
+    double na = N ? arr[0] : 0.0;  // arrival time of query ai
     // report (uniform) + per-lane sample partials
     uint64_t r_trained = 0, r_ptab = 0, r_pre = 0, r_freed = 0, r_loads = 0, r_recomp = 0, r_dropped = 0, r_jobs = 0,
              r_fb = 0, r_batches = 0, r_maxb = 0, r_offd = 0, r_adm = 0;
@@ -189,6 +200,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         resv += bytes;
     };
     auto pass_tok = [&](uint64_t i) -> uint64_t { return i == 0 ? pass0 : (i == 1 ? pass1 : pass2); };
+    uint64_t cur_tok = 0;  // passes[pass_index] of the running forward pass (set by begin_pass)
     auto fwd_layer = [&](uint64_t t) -> double {  // cost_model.hpp:39-41
         return prefill_latency(m, t, 1, false) / dL;
     };
@@ -196,19 +208,53 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         return m.backward_to_forward_ratio * fwd_layer(t);
     };
 
-    // ---- per-layer slot state, lane-parallel --------------------------------
-    auto dev_act_bytes = [&]() -> uint64_t {  // memory.hpp:91-96
-        uint64_t s = 0;
-        for (uint32_t l = lane; l < L; l += 32)
-            if (S.flg[l] & LF_DEV) s += S.rec[l];
-        return warp_sum_u64(s);
+    // ---- per-layer slot state ------------------------------------------------
+    auto contrib = [&](uint8_t f, uint64_t r, bool add) {  // one layer's share of the aggregates
+        const bool dv = f & LF_DEV, lv = !(f & (LF_CONS | LF_DROP));
+        const uint64_t db = dv ? r : 0, tb = lv ? r : 0;
+        const uint32_t dc = dv ? 1u : 0u, pc = (!dv && lv && r > 0) ? 1u : 0u;
+        if (add) {
+            ag_dev += db;
+            ag_t += tb;
+            ag_cnt += dc;
+            ag_pend += pc;
+        } else {
+            ag_dev -= db;
+            ag_t -= tb;
+            ag_cnt -= dc;
+            ag_pend -= pc;
+        }
+    };
+    auto recount = [&]() {  // lane-parallel recomputation after a bulk update
+        uint64_t db = 0, tb = 0;
+        uint32_t dc = 0, pc = 0;
+        for (uint32_t l = lane; l < L; l += 32) {
+            const uint8_t f = S.flg[l];
+            const uint64_t r = S.rec[l];
+            const bool dv = f & LF_DEV, lv = !(f & (LF_CONS | LF_DROP));
+            db += dv ? r : 0;
+            tb += lv ? r : 0;
+            dc += dv;
+            pc += !dv && lv && r > 0;
+        }
+        ag_dev = warp_sum_u64(db);
+        ag_t = warp_sum_u64(tb);
+        ag_cnt = static_cast<uint32_t>(warp_sum_u64(dc));
+        ag_pend = static_cast<uint32_t>(warp_sum_u64(pc));
+    };
+    auto set_layer = [&](uint32_t l, uint8_t f, uint64_t r) {  // single-layer update (owner lane writes)
+        contrib(S.flg[l], S.rec[l], false);
+        contrib(f, r, true);
+        __syncwarp();
+        if (lane == (l & 31)) {
+            S.flg[l] = f;
+            S.rec[l] = r;
+        }
+        __syncwarp();
     };
     auto training_peak = [&]() {  // engine.hpp:815-822
         if (!has_store) return;
-        uint64_t s = 0;
-        for (uint32_t l = lane; l < L; l += 32)
-            if (!(S.flg[l] & (LF_CONS | LF_DROP))) s += S.rec[l];
-        const uint64_t cur = kv_held + warp_sum_u64(s);
+        const uint64_t cur = kv_held + ag_t;
         if (cur > r_ptab) r_ptab = cur;
     };
     auto teardown = [&]() {  // engine.hpp:468-479
@@ -221,6 +267,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             }
         __syncwarp();
         led_free(warp_sum_u64(s));
+        recount();
         if (kv_held) led_free(kv_held);
         has_store = false;
         has_job = false;
@@ -237,15 +284,14 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             f |= LF_DEV;
         }
         r += bytes;
-        const double start = dmax(t, d2h_busy);
-        d2h_busy = start + static_cast<double>(bytes) / static_cast<double>(pf.d2h);
-        __syncwarp();
-        if (lane == (l & 31)) {
-            S.flg[l] = f;
-            S.rec[l] = r;
-            S.lcd[l] = d2h_busy;
+        if (bytes != cp_bytes) {  // transfer_time (cost_model.hpp:68-71)
+            cp_bytes = bytes;
+            cp_val = static_cast<double>(bytes) / static_cast<double>(pf.d2h);
         }
-        __syncwarp();
+        const double start = dmax(t, d2h_busy);
+        d2h_busy = start + cp_val;
+        if (lane == (l & 31)) S.lcd[l] = d2h_busy;
+        set_layer(l, f, r);
         ++seq;
     };
     // engine.hpp:563-610
@@ -261,6 +307,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         }
         __syncwarp();
         led_free(warp_sum_u64(s));
+        ag_dev = ag_t = 0;
+        ag_cnt = ag_pend = 0;
         const uint64_t response_kv = kv_held - prompt_kv;
         if (response_kv) led_free(response_kv);
         kv_held = prompt_kv;
@@ -296,7 +344,12 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
 
     // ---- training path --------------------------------------------------------
     auto schedule_forward = [&]() {  // engine.hpp:685-691
-        t_dur = fwd_layer(pass_tok(pass_index));
+        const uint64_t tok = cur_tok;
+        if (tok != fwd_tok) {
+            fwd_tok = tok;
+            fwd_val = fwd_layer(tok);
+        }
+        t_dur = fwd_val;
         tinf = true;
         t_fwd = true;
         t_a = static_cast<uint32_t>(cursor);
@@ -304,12 +357,13 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         t_seq = seq++;
     };
     auto begin_pass = [&]() {  // engine.hpp:662-683
+        cur_tok = pass_tok(pass_index);
         if (kv_charged != static_cast<int64_t>(pass_index)) {
             kv_charged = static_cast<int64_t>(pass_index);
             if (cpa) {
                 const bool is_prompt = incl_prompt && pass_index == 0;
                 if (!(is_prompt && prompt_kv > 0)) {
-                    const uint64_t kv = kv_bytes(m, pass_tok(pass_index), 1);
+                    const uint64_t kv = kv_bytes(m, cur_tok, 1);
                     if (!led_alloc(kv)) breach = true;
                     kv_held += kv;
                     if (is_prompt) prompt_kv += kv;
@@ -404,14 +458,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             vbits = COLO_V_EVALUATED | pack_verdict(0, 0, 0, 0, 0, 0, COLO_VD_ADMIT);
             return 0.0;
         }
-        uint32_t dev_layers = 0, pending = 0;
-        for (uint32_t l0 = 0; l0 < L; l0 += 32) {
-            const uint32_t l = l0 + lane;
-            const uint8_t f = l < L ? S.flg[l] : 0;
-            const uint64_t r = l < L ? S.rec[l] : 0;
-            dev_layers += __popc(__ballot_sync(kFullMask, f & LF_DEV));
-            pending += __popc(__ballot_sync(kFullMask, l < L && !(f & (LF_DEV | LF_CONS | LF_DROP)) && r > 0));
-        }
+        const uint32_t dev_layers = ag_cnt, pending = ag_pend;
         const uint32_t action = code == 1 ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS;
         const uint32_t layers = code >= 2 ? code - 2 : 0;
         const uint32_t free_now = code == 1 ? dev_layers : min(layers, dev_layers);
@@ -455,6 +502,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         __syncwarp();
         ready = warp_max_f64(ready);
         led_free(warp_sum_u64(fb));
+        recount();
         r_freed += freed;
         if (live() + need_total > cap) {  // KV corner (engine.hpp:549-552)
             drop_for_recompute(need_total);
@@ -480,6 +528,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             S.flg[l] = 0;
         }
         __syncwarp();
+        ag_dev = ag_t = 0;
+        ag_cnt = ag_pend = 0;
         src = j;
         prompt_kv = 0;
         kv_held = 0;
@@ -573,7 +623,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         qhead = end;
         uint32_t vbits = 0;
         double stall = 0.0;
-        if (has_store && kv_held + dev_act_bytes() > 0) stall = apply_offload(max_inc, nb, need_total, vbits);
+        if (has_store && kv_held + ag_dev > 0) stall = apply_offload(max_inc, nb, need_total, vbits);
         if (!led_alloc(need_total)) breach = true;  // engine.hpp:312-313
         bool rec = false;
         if (nb == 1 && !has_store) {
@@ -626,17 +676,25 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
 #pragma unroll
             for (int r = 0; r < 4; ++r) S.dk[32 * r + lane] = dk[r];
             __syncwarp();
+            // absolute-time chain now_k = now_{k-1} + d_k (sequential, one lane),
+            // the durations are overwritten by the absolute times
+            const uint32_t cnt = min(128u, maxo - k0);
+            if (lane == 0) {
+                double t = tnow;
+#pragma unroll 8
+                for (uint32_t i = 0; i < cnt; ++i) {
+                    t = t + S.dk[i];
+                    S.dk[i] = t;
+                }
+            }
+            __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                    if (k0 + 32 * r + l < maxo) {
-                        const double nw = tnow + S.dk[32 * r + l];
-                        if (lane == static_cast<uint32_t>(l)) sv[r] = nw - tnow;  // now - last_token_time
-                        tnow = nw;
-                    }
-                }
+            for (int r = 0; r < 4; ++r) {  // sample = now - last_token_time
+                const uint32_t i = 32 * r + lane;
+                if (i < cnt) sv[r] = S.dk[i] - (i ? S.dk[i - 1] : tnow);
+            }
+            tnow = S.dk[cnt - 1];
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -701,11 +759,14 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         s_seq = seq - 1;
         __syncwarp();
     };
+    // start_serving_batch is always the tail action of the handler that calls
+    // it, so it runs once at the bottom of the event loop (one inlined copy).
+    bool want_serve = false;
     auto preempt = [&]() -> bool {  // engine.hpp:725-731
         if (qhead == ai) return false;
         ++r_pre;
         ++plan_gen;
-        start_serving();
+        want_serve = true;
         return true;
     };
 
@@ -729,13 +790,15 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         consider(to_on, to_t, to_seq, EK_TIMEOUT);
         if (ld_cur < ld_n && ld_gen != plan_gen) ld_cur = ld_n;  // cancelled plan: every load is a no-op
         if (ld_cur < ld_n) consider(true, S.ldone[ld_cur], ld_seq0 + ld_cur, EK_LOAD);
-        if (ai < N && (bk == EK_NONE || arr[ai] <= bt)) {  // arrivals win time ties
+        if (ai < N && (bk == EK_NONE || na <= bt)) {  // arrivals win time ties
             if (sbusy || tinf) {  // engine.hpp:273: queued only; take every arrival up to the next event
                 ai = bk == EK_NONE ? N : find_tail(arr, N, ai, bt);
+                na = ai < N ? arr[ai] : 0.0;
                 continue;
             }
-            now = arr[ai];
+            now = na;
             ++ai;
+            na = ai < N ? arr[ai] : 0.0;
             if (has_job && waiting) {  // interrupt_training_wait(true), engine.hpp:622-631
                 const double waited = now - wait_since;
                 r_wait += waited;
@@ -744,9 +807,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 ++r_pre;
                 ++plan_gen;
             }
-            start_serving();
-            continue;
-        }
+            want_serve = true;
+        } else {
         if (bk == EK_NONE) break;
         now = bt;
         if (bk == EK_SERVE) {  // the batch's last DecodeStepDone (engine.hpp:367-408)
@@ -773,12 +835,12 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             }
             led_free(release);
             r_end = now;
-            start_serving();
+            want_serve = true;
         } else if (bk == EK_TRAIN) {
             tinf = false;
             tbusy += t_dur;
             if (t_fwd) {  // engine.hpp:693-722
-                const uint64_t bytes = pass_tok(pass_index) * m.act_bytes_per_token_per_layer;
+                const uint64_t bytes = cur_tok * m.act_bytes_per_token_per_layer;
                 if (stream && S.rec[cursor] == 0) ++r_freed;
                 record(static_cast<uint32_t>(cursor), bytes, now);
                 training_peak();
@@ -799,10 +861,9 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             } else {  // engine.hpp:761-779, complete_job :807-813
                 const uint32_t a = t_a;
                 const uint8_t f = S.flg[a];
-                if (f & LF_DEV) led_free(S.rec[a]);
-                __syncwarp();
-                if (lane == (a & 31)) S.flg[a] = static_cast<uint8_t>((f & ~LF_DEV) | LF_CONS);
-                __syncwarp();
+                const uint64_t r = S.rec[a];
+                if (f & LF_DEV) led_free(r);
+                set_layer(a, static_cast<uint8_t>((f & ~LF_DEV) | LF_CONS), r);
                 if (a == 0) {
                     r_trained += jp + (cpa ? 2 * jo : 0);
                     ++r_jobs;
@@ -829,10 +890,9 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         } else {  // EK_LOAD, engine.hpp:781-797
             const uint32_t a = S.llayer[ld_cur];
             ++ld_cur;
-            if (!led_alloc(S.rec[a])) breach = true;
-            __syncwarp();
-            if (lane == (a & 31)) S.flg[a] |= LF_DEV;
-            __syncwarp();
+            const uint64_t r = S.rec[a];
+            if (!led_alloc(r)) breach = true;
+            set_layer(a, static_cast<uint8_t>(S.flg[a] | LF_DEV), r);
             ++r_loads;
             if (has_job && waiting && phase == PH_BWD && cursor == a && !sbusy && qhead == ai) {
                 const double waited = now - wait_since;
@@ -841,6 +901,11 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 waiting = false;
                 schedule_backward();
             }
+        }
+        }
+        if (want_serve) {
+            want_serve = false;
+            start_serving();
         }
     }
 
