@@ -320,9 +320,9 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
                                double* pctl, colo_device_summary* totals);
 
 /* ------------------------------------------------------- colocated replay */
-/* Per-device MetricsReport (metrics.hpp:17-44; the first 14 fields, same
- * meaning) plus replay extras.  training_throughput = trained_tokens /
- * training_busy_time when busy > 0 (metrics.hpp:67-68). */
+/* Per-device MetricsReport (metrics.hpp:17-44; the first 15 fields, same
+ * meaning; oom_flag = oom_jobs > 0) plus replay extras.  training_throughput =
+ * trained_tokens / training_busy_time when busy > 0 (metrics.hpp:67-68). */
 typedef struct colo_colocated_summary {
     uint64_t generated_tokens;
     uint64_t trained_tokens;
@@ -338,6 +338,7 @@ typedef struct colo_colocated_summary {
     double prefetch_wait_seconds;
     uint64_t completed_jobs;
     uint64_t map_fallbacks;
+    uint64_t oom_jobs;          /* SeparateCluster: jobs the trainer could not fit (engine.hpp:841-845) */
     /* extras */
     uint64_t batches;
     uint64_t max_batch_size;
@@ -360,6 +361,9 @@ typedef struct colo_colocated_summary {
 #define COLO_V_ADMITTED (1u << 26)   /* admit_to_store ran for this batch (engine.hpp:317-318);
                                         COLO_V_STREAM / _STREAM_OOR give its streaming flag */
 
+/* SimMode (engine.hpp:23) per device in colo_colocated_opts.d_dev_sim_mode. */
+enum { COLO_SIM_SERVING_ONLY = 0, COLO_SIM_COLOCATED = 1, COLO_SIM_SEPARATE = 2 };
+
 typedef struct colo_colocated_opts {
     double cache_timeout;            /* SimConfig::cache_timeout (engine.hpp:55); the reference default is 60 */
     const double* d_label_delay;     /* [n] seconds; < 0 or NaN = the label never arrives; NULL = default_label_delay */
@@ -376,12 +380,17 @@ typedef struct colo_colocated_opts {
     uint32_t filter_shift;
     uint32_t pad;
     uint64_t filter_prefix[3];
+    const uint8_t* d_dev_sim_mode;   /* [ndev] COLO_SIM_*; NULL = every device Colocated */
 } colo_colocated_opts;
 
-/* Colocated replay (SimMode::Colocated) of every device's trace, one warp per
- * device.  Device d uses map set sets[d_dev_set[d]], whose model, GPU profile
- * and training mode are the simulation's (SimConfig::validate requires the
- * maps to match them, engine.hpp:60-68).  Events are handled in the
+/* Simulation::run of every device's trace, one warp per device, in the
+ * device's SimMode (opts->d_dev_sim_mode; default Colocated).  Device d uses
+ * map set sets[d_dev_set[d]], whose model, GPU profile and training mode are
+ * the simulation's (SimConfig::validate requires the maps to match them,
+ * engine.hpp:60-68).  SeparateCluster devices serve as ServingOnly and their
+ * trainer (engine.hpp:824-903) is folded over the job stream afterwards, in
+ * the reference's enqueue order (finish order for CPT; label arrival, ties in
+ * finish order, for CPA -- a stable segmented sort when label delays vary).  Events are handled in the
  * reference's (time, sequence) order and every f64 operation is the
  * reference's in its order, so each device's report and samples equal
  * Simulation::run's.  EVALIDATION as colo_replay_serving; EBREACH when a

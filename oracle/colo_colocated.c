@@ -23,7 +23,7 @@
 
 #include "colo_oracle.h"
 
-enum { EV_PREFILL, EV_DECODE, EV_LABEL, EV_TIMEOUT, EV_FWD, EV_BWD, EV_LOAD };
+enum { EV_PREFILL, EV_DECODE, EV_LABEL, EV_TIMEOUT, EV_FWD, EV_BWD, EV_LOAD, EV_BLAYER };
 enum { PH_WAITING_LABEL, PH_READY, PH_FORWARD, PH_BACKWARD }; /* engine.hpp:203 */
 
 typedef struct {
@@ -41,10 +41,15 @@ typedef struct { /* memory.hpp:45-52 (host_bytes is write-only for the metrics) 
 } co_layer;
 
 typedef struct {
+    uint64_t p, o, fp;
+} co_bjob; /* engine.hpp:225-232 (passes derived from p, o and the mode) */
+
+typedef struct {
     const orc_model* m;
     const orc_gpu* g;
     const orc_maps* maps;
     int cpa;
+    int sim_mode; /* ORC_SIM_* */
     double cache_timeout;
     const double* arr;
     const uint32_t* p;
@@ -90,6 +95,15 @@ typedef struct {
     double wait_since;
     int training_inflight;
     double train_busy;
+
+    /* separate-cluster trainer (engine.hpp:824-903) */
+    uint64_t t_alloc, t_resv, t_peak; /* MemoryLedger trainer_device_ */
+    co_bjob* bq;
+    size_t bq_head, bq_tail;
+    co_bjob bjob;
+    uint64_t b_pass, b_cursor;
+    int b_backward, b_busy;
+    double b_free_at;
 
     orc_colo_report* r;
     double tau;
@@ -452,7 +466,7 @@ static void co_start_serving(co_sim* s) {
     s->bn = n;
     s->qhead += n;
     double stall = 0;
-    if (s->has_store) {
+    if (s->sim_mode == ORC_SIM_COLOCATED && s->has_store) {
         uint64_t fp = s->kv_held;
         for (uint64_t l = 0; l < s->L; ++l)
             if (s->layers[l].on_device) fp += s->layers[l].recorded;
@@ -460,7 +474,7 @@ static void co_start_serving(co_sim* s) {
     }
     if (!co_alloc(s, need_total)) s->breach = 1;
     int recording = 0;
-    if (n == 1 && !s->has_store) recording = co_admit(s, s->bfirst);
+    if (s->sim_mode == ORC_SIM_COLOCATED && n == 1 && !s->has_store) recording = co_admit(s, s->bfirst);
     s->brec = recording;
     double start = s->now + stall;
     double dur = 0;
@@ -500,6 +514,88 @@ static void co_schedule_decode(co_sim* s) { /* engine.hpp:358-365 */
     co_push(s, s->now + dur, EV_DECODE, 0, 0, dur);
 }
 
+/* ---- separate-cluster trainer, engine.hpp:824-903 ---------------------------- */
+static void co_baseline_layer_schedule(co_sim* s, double at) { /* :860-872 */
+    double dur;
+    int64_t kind_bwd = s->b_backward;
+    if (!s->b_backward) {
+        uint64_t tok = s->cpa ? s->bjob.p + s->bjob.o : s->bjob.p;
+        dur = orc_forward_layer_latency(s->m, tok, NULL);
+    } else {
+        dur = 0;
+        uint64_t np = s->cpa ? 2 : 1;
+        uint64_t tok = s->cpa ? s->bjob.p + s->bjob.o : s->bjob.p;
+        for (uint64_t i = 0; i < np; ++i) dur += orc_backward_layer_latency(s->m, tok, NULL);
+    }
+    co_push(s, at + dur, EV_BLAYER, (int64_t)s->b_cursor, kind_bwd, dur);
+}
+
+static int t_alloc(co_sim* s, uint64_t bytes) { /* memory.hpp:28-35 on trainer_device_ */
+    if (s->t_alloc - s->t_resv + bytes > s->cap) return 0;
+    uint64_t reuse = s->t_resv < bytes ? s->t_resv : bytes;
+    s->t_resv -= reuse;
+    s->t_alloc += bytes - reuse;
+    if (s->t_alloc > s->t_peak) s->t_peak = s->t_alloc;
+    return 1;
+}
+
+static void co_baseline_try_start(co_sim* s) { /* :850-858 */
+    if (s->b_busy || s->bq_head == s->bq_tail) return;
+    s->b_busy = 1;
+    s->bjob = s->bq[s->bq_head++];
+    s->b_pass = 0;
+    s->b_cursor = 0;
+    s->b_backward = 0;
+    if (!t_alloc(s, s->bjob.fp)) s->breach = 1;
+    co_baseline_layer_schedule(s, dmax(s->now, s->b_free_at));
+}
+
+static void co_baseline_enqueue(co_sim* s, uint64_t p, uint64_t o) { /* :826-848 */
+    co_bjob j = {p, o, 0};
+    uint64_t per_token = s->L * s->m->act_bytes_per_token_per_layer + s->m->kv_bytes_per_token;
+    if (!s->cpa) j.fp += p * per_token;
+    else {
+        j.fp += (p + o) * per_token;
+        j.fp += (p + o) * per_token;
+    }
+    if (j.fp > s->r->peak_training_activation_bytes) s->r->peak_training_activation_bytes = j.fp;
+    uint64_t budget = s->cap - s->m->weights_bytes - s->g->runtime_reserve_bytes;
+    if (j.fp > budget) {
+        s->r->oom_jobs++;
+        return;
+    }
+    s->bq[s->bq_tail++] = j;
+    co_baseline_try_start(s);
+}
+
+static void co_on_baseline_layer(co_sim* s, double dur) { /* :874-903 */
+    s->train_busy += dur;
+    s->b_free_at = s->now;
+    if (!s->b_backward) {
+        ++s->b_cursor;
+        if (s->b_cursor == s->L) {
+            s->b_cursor = 0;
+            ++s->b_pass;
+            if (s->b_pass >= (uint64_t)(s->cpa ? 2 : 1)) {
+                s->b_backward = 1;
+                s->b_cursor = s->L - 1;
+            }
+        }
+        co_baseline_layer_schedule(s, s->now);
+        return;
+    }
+    if (s->b_cursor == 0) {
+        s->r->trained_tokens += s->bjob.p + (s->cpa ? 2 * s->bjob.o : 0);
+        ++s->r->completed_jobs;
+        s->t_resv += s->bjob.fp; /* trainer_device_.free_bytes */
+        s->b_busy = 0;
+        co_baseline_try_start(s);
+        return;
+    }
+    --s->b_cursor;
+    co_baseline_layer_schedule(s, s->now);
+}
+
 /* engine.hpp:389-408 */
 static void co_finish_query(co_sim* s, uint64_t q) {
     uint64_t release = co_need(s, q);
@@ -516,6 +612,14 @@ static void co_finish_query(co_sim* s, uint64_t q) {
         }
     }
     co_free(s, release);
+    if (s->sim_mode == ORC_SIM_SEPARATE) { /* engine.hpp:410-416 */
+        if (!s->cpa) {
+            co_baseline_enqueue(s, s->p[q], s->o[q]);
+        } else {
+            double ld = s->label_delay ? s->label_delay[q] : -1.0;
+            if (ld >= 0) co_push(s, s->now + ld, EV_LABEL, -1, (int64_t)q, 0);
+        }
+    }
 }
 
 /* engine.hpp:367-387 (+ the slow label rule) */
@@ -613,11 +717,12 @@ static void co_on_load(co_sim* s, int64_t a, int64_t gen) {
     }
 }
 
-int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* maps, int mode_cpa,
-                         double cache_timeout, const double* arrival, const uint32_t* prompt, const uint32_t* output,
+int orc_replay_sim(const orc_model* m, const orc_gpu* g, const orc_maps* maps, int sim_mode, int mode_cpa,
+                   double cache_timeout, const double* arrival, const uint32_t* prompt, const uint32_t* output,
                          const double* label_delay, uint64_t n, double tau, double* samples, uint8_t* labels,
-                         orc_batch* batches, orc_colo_report* out) {
+                   orc_batch* batches, orc_colo_report* out) {
     memset(out, 0, sizeof *out);
+    if (sim_mode < 0 || sim_mode > 2) return ORC_EINVAL;
     if (orc_validate_profile_pair(m, g) != ORC_OK) return ORC_EVALIDATION; /* engine.hpp:61 */
     co_sim S;
     memset(&S, 0, sizeof S);
@@ -626,6 +731,7 @@ int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* m
     s->g = g;
     s->maps = maps;
     s->cpa = mode_cpa;
+    s->sim_mode = sim_mode;
     s->cache_timeout = cache_timeout;
     s->arr = arrival;
     s->p = prompt;
@@ -646,8 +752,10 @@ int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* m
         if (co_need(s, i) > s->budget) return ORC_EVALIDATION;
     }
     s->layers = (co_layer*)calloc(s->L ? s->L : 1, sizeof(co_layer));
+    s->bq = (co_bjob*)calloc(n ? n : 1, sizeof(co_bjob));
     s->next_seq = n;
     if (!co_alloc(s, m->weights_bytes + g->runtime_reserve_bytes)) s->breach = 1; /* engine.hpp:141-142 */
+    if (sim_mode == ORC_SIM_SEPARATE && !t_alloc(s, m->weights_bytes + g->runtime_reserve_bytes)) s->breach = 1;
     while (!s->breach) {
         /* pop min (time, seq): the next arrival (seq = its index) or a listed event */
         size_t best = (size_t)-1;
@@ -677,6 +785,10 @@ int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* m
                 break;
             case EV_DECODE: co_on_decode(s); break;
             case EV_LABEL: /* engine.hpp:481-496 */
+                if (e.a < 0) {
+                    co_baseline_enqueue(s, s->p[e.b], s->o[e.b]);
+                    break;
+                }
                 if (s->has_store && s->generation == (uint64_t)e.a && s->has_job && s->phase == PH_WAITING_LABEL) {
                     s->phase = PH_READY;
                     co_try_start_training(s);
@@ -693,12 +805,22 @@ int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* m
             case EV_FWD: co_on_forward(s, e.dur); break;
             case EV_BWD: co_on_backward(s, e.a, e.dur); break;
             case EV_LOAD: co_on_load(s, e.a, e.b); break;
+            case EV_BLAYER: co_on_baseline_layer(s, e.dur); break;
         }
     }
     out->training_busy_time = s->train_busy;
-    out->peak_device_bytes = s->peak;
+    out->peak_device_bytes = sim_mode == ORC_SIM_SEPARATE ? s->t_peak : s->peak; /* engine.hpp:159-161 */
     out->status = s->breach ? ORC_EBREACH : ORC_OK;
     free(s->layers);
+    free(s->bq);
     free(s->ev);
     return s->breach ? ORC_EBREACH : ORC_OK;
+}
+
+int orc_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_maps* maps, int mode_cpa,
+                         double cache_timeout, const double* arrival, const uint32_t* prompt, const uint32_t* output,
+                         const double* label_delay, uint64_t n, double tau, double* samples, uint8_t* labels,
+                         orc_batch* batches, orc_colo_report* out) {
+    return orc_replay_sim(m, g, maps, ORC_SIM_COLOCATED, mode_cpa, cache_timeout, arrival, prompt, output,
+                          label_delay, n, tau, samples, labels, batches, out);
 }

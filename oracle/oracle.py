@@ -105,6 +105,7 @@ class ColoReport(C.Structure):
         ("prefetch_wait_seconds", C.c_double),
         ("completed_jobs", C.c_uint64),
         ("map_fallbacks", C.c_uint64),
+        ("oom_jobs", C.c_uint64),
         ("batches", C.c_uint64),
         ("max_batch_size", C.c_uint64),
         ("offload_decisions", C.c_uint64),
@@ -117,7 +118,8 @@ class ColoReport(C.Structure):
 
 
 # MetricsReport fields the reference itself reports (metrics.hpp:17-44)
-METRICS_FIELDS = [f for f, _ in ColoReport._fields_[:14]]
+METRICS_FIELDS = [f for f, _ in ColoReport._fields_[:15]]
+SIM_MODES = {"serving-only": 0, "colocated": 1, "baseline": 2}  # engine.hpp:23-39 names
 
 
 class Dist(C.Structure):
@@ -408,8 +410,8 @@ class OracleLib:
         return res
 
     def replay_colocated(self, m, g, grid, cpa, arrival, prompt, output, label_delay=None, cache_timeout=60.0,
-                         tau=float("inf"), want_samples=True, want_batches=True):
-        """Colocated replay (Simulation::run, SimMode::Colocated; maps from build_maps).
+                         tau=float("inf"), want_samples=True, want_batches=True, sim_mode="colocated"):
+        """Simulation::run in ``sim_mode`` (colocated | baseline | serving-only; maps from build_maps).
         label_delay: per-query seconds, < 0 = nullopt (None = all nullopt).
         Returns dict(report, samples, labels, batches, pctl, rc)."""
         arrival = np.ascontiguousarray(arrival, np.float64)
@@ -426,7 +428,7 @@ class OracleLib:
         pctl = None
         if self.which == "ref":
             pctl = np.full(4, np.nan)
-            rc = self.lib.ref_replay_colocated(C.byref(m), C.byref(g), C.byref(grid), C.c_int(int(cpa)),
+            rc = self.lib.ref_replay_sim(C.byref(m), C.byref(g), C.byref(grid), C.c_int(SIM_MODES[sim_mode]), C.c_int(int(cpa)),
                                                C.c_double(cache_timeout), vp(arrival), vp(prompt), vp(output), vp(ld),
                                                C.c_uint64(n), vp(samples), vp(batches), C.byref(rep), vp(pctl))
             labels = None
@@ -434,7 +436,7 @@ class OracleLib:
             off = self.build_offloading_map(m, g, grid, cpa)
             hed = self.build_hedging_map(m, g, grid.cached_step, grid.max_cached, cpa, 128)
             mp = Maps(grid, off.ctypes.data, grid.cached_step, grid.max_cached, hed.ctypes.data, m.num_layers)
-            rc = self.lib.orc_replay_colocated(C.byref(m), C.byref(g), C.byref(mp), C.c_int(int(cpa)),
+            rc = self.lib.orc_replay_sim(C.byref(m), C.byref(g), C.byref(mp), C.c_int(SIM_MODES[sim_mode]), C.c_int(int(cpa)),
                                                C.c_double(cache_timeout), vp(arrival), vp(prompt), vp(output), vp(ld),
                                                C.c_uint64(n), C.c_double(tau), vp(samples), vp(labels), vp(batches),
                                                C.byref(rep))

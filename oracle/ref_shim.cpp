@@ -415,14 +415,14 @@ int ref_replay_serving(const orc_model* m, const orc_gpu* g, const double* arriv
  * without samples) and the raw samples; returns ORC_EBREACH when the run
  * throws InvariantBreach / std::logic_error, ORC_EVALIDATION for a refused
  * configuration.  batches: (start, end, first, n) from the event log. */
-int ref_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_grid* grid, int cpa, double cache_timeout,
-                         const double* arrival, const uint32_t* prompt, const uint32_t* output,
-                         const double* label_delay, uint64_t n, double* samples, orc_batch* batches,
-                         orc_colo_report* out, double* pctl) {
+int ref_replay_sim(const orc_model* m, const orc_gpu* g, const orc_grid* grid, int sim_mode, int cpa,
+                   double cache_timeout, const double* arrival, const uint32_t* prompt, const uint32_t* output,
+                   const double* label_delay, uint64_t n, double* samples, orc_batch* batches,
+                   orc_colo_report* out, double* pctl) {
     std::memset(out, 0, sizeof *out);
     try {
         SimConfig cfg;
-        cfg.mode = SimMode::Colocated;
+        cfg.mode = sim_mode == 0 ? SimMode::ServingOnly : (sim_mode == 1 ? SimMode::Colocated : SimMode::SeparateCluster);
         cfg.training = to_mode(cpa);
         cfg.model = to_model(m);
         cfg.gpu = to_gpu(g);
@@ -466,6 +466,8 @@ int ref_replay_colocated(const orc_model* m, const orc_gpu* g, const orc_grid* g
         out->prefetch_wait_seconds = rep.prefetch_wait_seconds;
         out->completed_jobs = rep.completed_jobs;
         out->map_fallbacks = rep.map_fallbacks;
+        out->oom_jobs = rep.oom_jobs;
+        if (rep.oom_flag != (rep.oom_jobs > 0)) return ORC_EINVAL;  // oom_flag is derivable
         const double nan = std::nan("");
         if (pctl) {
             pctl[0] = rep.tpt_p50 ? *rep.tpt_p50 : nan;

@@ -111,6 +111,7 @@ class ColocatedSummary(C.Structure):
         ("prefetch_wait_seconds", C.c_double),
         ("completed_jobs", C.c_uint64),
         ("map_fallbacks", C.c_uint64),
+        ("oom_jobs", C.c_uint64),
         ("batches", C.c_uint64),
         ("max_batch_size", C.c_uint64),
         ("offload_decisions", C.c_uint64),
@@ -141,6 +142,7 @@ class ColocatedOpts(C.Structure):
         ("filter_shift", C.c_uint32),
         ("pad", C.c_uint32),
         ("filter_prefix", C.c_uint64 * 3),
+        ("d_dev_sim_mode", C.c_void_p),
     ]
 
 
@@ -159,7 +161,7 @@ class Dist(C.Structure):
 
 assert C.sizeof(Model) == 96 and C.sizeof(Gpu) == 32 and C.sizeof(Grid) == 48
 assert C.sizeof(DeviceSummary) == 88
-assert C.sizeof(ColocatedSummary) == 208
+assert C.sizeof(ColocatedSummary) == 216
 
 # Every symbol include/colo_abi.h declares (checked by tests/test_abi.py).
 EXPORTS = [

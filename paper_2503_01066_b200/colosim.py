@@ -776,12 +776,27 @@ def serving_stats_c(ctx: Context, profiles, arrival, prompt, output, dev_offsets
 # ------------------------------------------------------------- colocated replay
 
 COLOCATED_FIELDS = [f for f, _ in _lib.ColocatedSummary._fields_]
-# MetricsReport fields the reference reports per run (metrics.hpp:17-44)
-METRICS_FIELDS = COLOCATED_FIELDS[:14]
+# MetricsReport fields the reference reports per run (metrics.hpp:17-44; oom_flag = oom_jobs > 0)
+METRICS_FIELDS = COLOCATED_FIELDS[:15]
+
+
+class SimMode(enum.IntEnum):
+    """engine.hpp:23 (names as sim_mode_from_string, :34-39)."""
+
+    SERVING_ONLY = 0
+    COLOCATED = 1
+    SEPARATE_CLUSTER = 2
+
+    @staticmethod
+    def parse(s: str) -> "SimMode":
+        m = {"serving-only": SimMode.SERVING_ONLY, "colocated": SimMode.COLOCATED, "baseline": SimMode.SEPARATE_CLUSTER}
+        if s not in m:
+            raise ColoValidationError(_lib.COLO_EVALIDATION, f"unknown sim mode: {s}")
+        return m[s]
 
 
 def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay, default_label_delay,
-                    cache_timeout, tau, samples, labels, batches, summary, res, keep):
+                    cache_timeout, tau, samples, labels, batches, summary, res, keep, sim_mode=None):
     torch = _torch()
     dev = prompt.device
     _need_cuda(arrival, "arrival", 8)
@@ -816,6 +831,13 @@ def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, la
     if summary:
         res["summary"] = torch.zeros((max(ndev, 1), C.sizeof(_lib.ColocatedSummary)), dtype=torch.uint8, device=dev)
         o.d_summary = res["summary"].data_ptr()
+    if sim_mode is not None:
+        if isinstance(sim_mode, (int, SimMode)):
+            sm = torch.full((max(ndev, 1),), int(sim_mode), dtype=torch.uint8, device=dev)
+        else:
+            sm = sim_mode.to(device=dev, dtype=torch.uint8).contiguous()
+        res["sim_mode"] = sm
+        o.d_dev_sim_mode = sm.data_ptr()
     arr = _sets_array(sets)
     keep.append(arr)
     return o, arr, n, ndev
@@ -824,9 +846,10 @@ def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, la
 def replay_colocated(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                      label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
                      tau: float = math.inf, samples: bool = False, labels: bool = True, batches: bool = False,
-                     summary: bool = True):
-    """Colocated replay of every device (Simulation::run, SimMode::Colocated,
-    engine.hpp:140-822).  Device d runs with map set ``sets[dev_set[d]]`` and
+                     summary: bool = True, sim_mode=None):
+    """Simulation::run of every device (engine.hpp:140-903), by default in
+    SimMode::Colocated; ``sim_mode`` (a SimMode for all devices or a per-device
+    uint8 tensor) selects ServingOnly / Colocated / SeparateCluster.  Device d runs with map set ``sets[dev_set[d]]`` and
     that set's model, GPU profile and training mode (SimConfig::validate,
     engine.hpp:60-68).  ``label_delay``: optional f64 device tensor per query
     (< 0 or NaN = the label never arrives); otherwise every query uses
@@ -838,7 +861,7 @@ def replay_colocated(ctx: Context, sets: Sequence[MapSet], arrival, prompt, outp
     res, keep = {}, []
     o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
                                       default_label_delay, cache_timeout, tau, samples, labels, batches, summary,
-                                      res, keep)
+                                      res, keep, sim_mode)
     try:
         check(lib().colo_replay_colocated(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),
                                           _ptr(output), n, _ptr(dev_offsets), _ptr(dev_set), ndev, C.byref(o)),
@@ -862,13 +885,14 @@ def colocated_summaries(summary_bytes) -> list:
 
 def colocated_stats(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                     label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
-                    tau: float = math.inf):
+                    tau: float = math.inf, sim_mode=None):
     """colo_colocated_stats: colocated replays of every device + exact
     nearest-rank p50/p90/p99 and mean of the union of their TPT samples
     (finalize, metrics.hpp:56-69).  Returns (pctl[4], totals dict)."""
     res, keep = {}, []
     o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
-                                      default_label_delay, cache_timeout, tau, False, False, False, False, res, keep)
+                                      default_label_delay, cache_timeout, tau, False, False, False, False, res, keep,
+                                      sim_mode)
     pctl = (C.c_double * 4)()
     tot = _lib.ColocatedSummary()
     check(lib().colo_colocated_stats(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),

@@ -46,6 +46,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include "colo_internal.h"
 #include "colo_replay.cuh"
 
@@ -87,7 +89,11 @@ struct CoParams {
     uint64_t* hist;
     uint32_t nfilters, hist_shift, filter_shift;
     uint64_t prefix[3];
-    int* err;
+    int* err;      // bit0 validation, bit1 breach, bit2 a SeparateCluster job stream needs sorting
+    const uint8_t* sim_mode;
+    double* job_t;     // SeparateCluster job stream (enqueue time), at dev_off[d] + i
+    uint32_t* job_q;   // ... and its query (device-local index)
+    uint64_t* job_cnt; // [ndev]
 };
 
 struct WarpSmem {
@@ -102,6 +108,12 @@ struct WarpSmem {
 };
 
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v = min(v, __shfl_xor_sync(kFullMask, v, s));
+    return v;
+}
 
 __device__ __forceinline__ double warp_max_f64(double v) {
 #pragma unroll
@@ -128,6 +140,12 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     const uint32_t* __restrict__ po = P.o + lo;
     const double dL = static_cast<double>(L);
     const double gam = m.decode_coef_const, del = m.decode_coef_context;
+    const int smode = P.sim_mode ? P.sim_mode[d] : COLO_SIM_COLOCATED;
+    const bool colocated = smode == COLO_SIM_COLOCATED;  // the slot and the offloader exist only here
+    const bool separate = smode == COLO_SIM_SEPARATE;    // jobs go to the trainer stream
+    uint64_t jc = 0;        // SeparateCluster jobs emitted
+    double last_t = -1.0;   // enqueue time of the last emitted job
+    bool unsorted = false;  // an emitted enqueue time went backwards (label delays vary)
 
     for (uint32_t l = lane; l < kLayerCap; l += 32) {
         S.rec[l] = 0;
@@ -623,10 +641,10 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         qhead = end;
         uint32_t vbits = 0;
         double stall = 0.0;
-        if (has_store && kv_held + ag_dev > 0) stall = apply_offload(max_inc, nb, need_total, vbits);
+        if (colocated && has_store && kv_held + ag_dev > 0) stall = apply_offload(max_inc, nb, need_total, vbits);
         if (!led_alloc(need_total)) breach = true;  // engine.hpp:312-313
         bool rec = false;
-        if (nb == 1 && !has_store) {
+        if (colocated && nb == 1 && !has_store) {
             admit(head, vbits);
             rec = true;
         }
@@ -695,6 +713,55 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 if (i < cnt) sv[r] = S.dk[i] - (i ? S.dk[i - 1] : tnow);
             }
             tnow = S.dk[cnt - 1];
+            if (separate) {
+                // finish_query of the members that finish in this window, in the
+                // reference's order (step, then batch order): CPT enqueues the
+                // job at the finish time, CPA schedules its label at finish +
+                // delay (engine.hpp:410-416)
+                auto member_o = [&](uint64_t j) -> uint32_t { return staged ? S.po[j].y : po[head + j]; };
+                const uint32_t wend = k0 + cnt;
+                uint32_t cur = k0;
+                for (;;) {
+                    uint32_t mn = 0xffffffffu;
+                    for (uint64_t j = lane; j < nb; j += 32) {
+                        const uint32_t f = member_o(j) - 1;
+                        if (f >= cur && f < wend) mn = min(mn, f);
+                    }
+                    mn = warp_min_u32(mn);
+                    if (mn == 0xffffffffu) break;
+                    const double tf = S.dk[mn - k0];
+                    for (uint64_t j0 = 0; j0 < nb; j0 += 32) {
+                        const uint64_t j = j0 + lane;
+                        bool em = false;
+                        double te = tf;
+                        if (j < nb && member_o(j) - 1 == mn) {
+                            if (!cpa) {
+                                em = true;
+                            } else {
+                                const double ldl = P.ld ? P.ld[lo + head + j] : P.ld_default;
+                                if (ldl >= 0.0) {
+                                    em = true;
+                                    te = tf + ldl;
+                                }
+                            }
+                        }
+                        const uint32_t bal = __ballot_sync(kFullMask, em);
+                        if (bal) {
+                            const uint32_t below = bal & ((1u << lane) - 1u);
+                            const double prev_lane = __shfl_sync(kFullMask, te, below ? 31 - __clz(below) : 0);
+                            if (em) {
+                                if (te < (below ? prev_lane : last_t)) unsorted = true;
+                                const uint64_t pos = lo + jc + __popc(below);
+                                P.job_t[pos] = te;
+                                P.job_q[pos] = static_cast<uint32_t>(head + j);
+                            }
+                            last_t = __shfl_sync(kFullMask, te, 31 - __clz(bal));
+                            jc += __popc(bal);
+                        }
+                    }
+                    cur = mn + 1;
+                }
+            }
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -930,6 +997,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         for (int s = 16; s > 0; s >>= 1) flags |= __shfl_xor_sync(kFullMask, flags, s);
     }
     if (breach && lane == 0) atomicOr(P.err, 2);
+    if (__any_sync(kFullMask, unsorted) && lane == 0) atomicOr(P.err, 4);
+    if (P.job_cnt && lane == 0) P.job_cnt[d] = jc;  // every device (0 unless SeparateCluster): sort segments
     if (lane == 0 && P.summary) {
         colo_colocated_summary r;
         r.generated_tokens = g_gen;
@@ -946,6 +1015,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         r.prefetch_wait_seconds = r_wait;
         r.completed_jobs = r_jobs;
         r.map_fallbacks = r_fb;
+        r.oom_jobs = 0;
         r.batches = r_batches;
         r.max_batch_size = r_maxb;
         r.offload_decisions = r_offd;
@@ -960,6 +1030,71 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         r.flags = flags;
         P.summary[d] = r;
     }
+}
+
+// SeparateCluster trainer (engine.hpp:824-903), one thread per device, folded
+// over the job stream in enqueue order.  Jobs run FIFO one at a time: a job
+// starts at max(enqueue, previous job's last layer) (schedule_baseline_layer
+// with trainer_free_at_, :850-858), each layer completes at the previous one's
+// time + its duration (:860-872, 888, 902), and training_busy_time adds every
+// layer's duration in that order (:875).  The trainer ledger peaks at the
+// fixed footprint plus the largest job it ran (memory.hpp:28-35 reuse).
+__global__ void __launch_bounds__(128) k_trainer_fold(const __grid_constant__ CoParams P, const double* __restrict__ jt,
+                                                      const uint32_t* __restrict__ jq) {
+    const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= P.ndev) return;
+    if ((P.sim_mode ? P.sim_mode[d] : COLO_SIM_COLOCATED) != COLO_SIM_SEPARATE) return;
+    const CoProfile& pf = P.prof[P.dev_set[d]];
+    const colo_model& m = pf.m;
+    const uint64_t L = pf.L;
+    const bool cpa = pf.cpa != 0;
+    const uint64_t lo = P.dev_off[d], cnt = P.job_cnt[d];
+    const uint64_t per_token = L * m.act_bytes_per_token_per_layer + m.kv_bytes_per_token;  // :834-835
+    const uint32_t np = cpa ? 2u : 1u;  // passes: {p} (CPT) or {p+o, p+o} (CPA), :830-833
+    double prev_end = 0.0, busy = 0.0;
+    uint64_t trained = 0, done = 0, ptab = 0, oom = 0, maxfp = 0;
+    uint64_t fd_tok = ~0ull;
+    double fd = 0.0, bd = 0.0;
+    for (uint64_t i = 0; i < cnt; ++i) {
+        const uint32_t q = jq[lo + i];
+        const double te = jt[lo + i];
+        const uint64_t p = P.p[lo + q], o = P.o[lo + q];
+        const uint64_t tok = cpa ? p + o : p;
+        uint64_t fp = 0;
+        for (uint32_t k = 0; k < np; ++k) fp += tok * per_token;
+        if (fp > ptab) ptab = fp;
+        if (fp > pf.budget) {  // :841-845 OOM datapoint
+            ++oom;
+            continue;
+        }
+        if (fp > maxfp) maxfp = fp;
+        if (tok != fd_tok) {  // forward_layer_latency / backward sum (:864, 867-868)
+            fd_tok = tok;
+            fd = prefill_latency(m, tok, 1, false) / static_cast<double>(L);
+            bd = 0.0;
+            for (uint32_t k = 0; k < np; ++k) bd += m.backward_to_forward_ratio * fd;
+        }
+        double t = te < prev_end ? prev_end : te;  // std::max(now_, trainer_free_at_)
+        for (uint32_t k = 0; k < np; ++k)
+            for (uint64_t l = 0; l < L; ++l) {
+                t = t + fd;
+                busy += fd;
+            }
+        for (uint64_t l = 0; l < L; ++l) {
+            t = t + bd;
+            busy += bd;
+        }
+        prev_end = t;
+        trained += cpa ? p + 2 * o : p;
+        ++done;
+    }
+    colo_colocated_summary& r = P.summary[d];
+    r.trained_tokens = trained;
+    r.completed_jobs = done;
+    r.training_busy_time = busy;
+    r.peak_device_bytes = pf.fixed + maxfp;  // trainer_device_.peak_allocated (engine.hpp:159-161)
+    r.peak_training_activation_bytes = ptab;
+    r.oom_jobs = oom;
 }
 
 // Trace checks of colo_replay_serving's k_validate (workload.hpp:165-181,
@@ -977,6 +1112,18 @@ __global__ void __launch_bounds__(128) k_co_validate(const __grid_constant__ CoP
         if (j > lo && P.arr[j] < P.arr[j - 1]) bad = true;
     }
     if (__any_sync(kFullMask, bad) && lane == 0) atomicOr(P.err, 1);
+}
+
+size_t align256c(size_t x) { return (x + 255) & ~size_t(255); }
+
+colo_status grow_scratch(colo_ctx* ctx, size_t bytes) {
+    if (ctx->rscratch_bytes >= bytes) return COLO_OK;
+    if (ctx->d_rscratch) cudaFree(ctx->d_rscratch);
+    ctx->d_rscratch = nullptr;
+    ctx->rscratch_bytes = 0;
+    COLO_CK(ctx, cudaMalloc(&ctx->d_rscratch, bytes));
+    ctx->rscratch_bytes = bytes;
+    return COLO_OK;
 }
 
 }  // namespace
@@ -1020,10 +1167,18 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     COLO_CK(ctx, cudaMemcpyAsync(dset.data(), d_dev_set, ndev * 2, cudaMemcpyDeviceToHost, ctx->stream));
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     if (off[0] != 0 || off[ndev] != n) return set_err(ctx, COLO_EINVAL, "device offsets must span [0, n]");
+    std::vector<uint8_t> smode(ndev, COLO_SIM_COLOCATED);
+    if (opts->d_dev_sim_mode) {
+        COLO_CK(ctx, cudaMemcpyAsync(smode.data(), opts->d_dev_sim_mode, ndev, cudaMemcpyDeviceToHost, ctx->stream));
+        COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    bool any_separate = false;
     for (size_t d = 0; d < ndev; ++d) {
         if (off[d + 1] < off[d]) return set_err(ctx, COLO_EINVAL, "device offsets not monotone");
         if (dset[d] >= nsets) return set_err(ctx, COLO_EINVAL, "device map-set index out of range");
-        if (off[d + 1] - off[d] >= (1ull << 32)) return set_err(ctx, COLO_EINVAL, "more than 2^32-1 queries on a device");
+        if (off[d + 1] - off[d] >= (1ull << 31)) return set_err(ctx, COLO_EINVAL, "2^31 or more queries on a device");
+        if (smode[d] > COLO_SIM_SEPARATE) return set_err(ctx, COLO_EINVAL, "sim mode must be 0, 1 or 2");
+        any_separate |= smode[d] == COLO_SIM_SEPARATE;
     }
     P.arr = d_arrival;
     P.p = d_prompt;
@@ -1046,6 +1201,41 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     P.filter_shift = opts->filter_shift;
     for (int f = 0; f < 3; ++f) P.prefix[f] = opts->filter_prefix[f];
     P.err = ctx->d_flag;
+    P.sim_mode = opts->d_dev_sim_mode;
+    // SeparateCluster job streams: (enqueue time, query) per device + sort buffers
+    size_t o_jt = 0, o_jq = 0, o_jc = 0, o_jt2 = 0, o_jq2 = 0, o_beg = 0, o_end = 0, o_tmp = 0, tmp_bytes = 0;
+    if (any_separate) {
+        size_t b = 0;
+        o_jt = b;
+        b += align256c(n * 8 + 8);
+        o_jq = b;
+        b += align256c(n * 4 + 8);
+        o_jc = b;
+        b += align256c(ndev * 8 + 8);
+        o_jt2 = b;
+        b += align256c(n * 8 + 8);
+        o_jq2 = b;
+        b += align256c(n * 4 + 8);
+        o_beg = b;
+        b += align256c(ndev * 8 + 8);
+        o_end = b;
+        b += align256c(ndev * 8 + 8);
+        // cub temp storage for a segmented stable sort of up to n items
+        int ni = static_cast<int>(std::min<size_t>(n, (1u << 31) - 1));
+        cub::DeviceSegmentedSort::StableSortPairs(nullptr, tmp_bytes, static_cast<const double*>(nullptr),
+                                                  static_cast<double*>(nullptr), static_cast<const uint32_t*>(nullptr),
+                                                  static_cast<uint32_t*>(nullptr), ni, static_cast<int>(ndev),
+                                                  static_cast<const uint64_t*>(nullptr),
+                                                  static_cast<const uint64_t*>(nullptr), ctx->stream);
+        o_tmp = b;
+        b += align256c(tmp_bytes + 8);
+        const colo_status st = grow_scratch(ctx, b);
+        if (st != COLO_OK) return st;
+        auto* base = static_cast<uint8_t*>(ctx->d_rscratch);
+        P.job_t = reinterpret_cast<double*>(base + o_jt);
+        P.job_q = reinterpret_cast<uint32_t*>(base + o_jq);
+        P.job_cnt = reinterpret_cast<uint64_t*>(base + o_jc);
+    }
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
     const uint32_t vblocks = static_cast<uint32_t>((ndev + 3) / 4);
     k_co_validate<<<vblocks, 128, 0, ctx->stream>>>(P);
@@ -1060,6 +1250,52 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (any_separate && P.summary) {
+        const double* jt = P.job_t;
+        const uint32_t* jq = P.job_q;
+        if (flag & 4) {  // label delays vary: stable sort of each device's jobs by enqueue time (ties keep finish order)
+            auto* base = static_cast<uint8_t*>(ctx->d_rscratch);
+            std::vector<uint64_t> cnt(ndev), beg(ndev), end(ndev);
+            COLO_CK(ctx, cudaMemcpyAsync(cnt.data(), P.job_cnt, ndev * 8, cudaMemcpyDeviceToHost, ctx->stream));
+            COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+            for (size_t d = 0; d < ndev; ++d) {
+                beg[d] = off[d];
+                end[d] = off[d] + cnt[d];
+            }
+            COLO_CK(ctx, cudaMemcpyAsync(base + o_beg, beg.data(), ndev * 8, cudaMemcpyHostToDevice, ctx->stream));
+            COLO_CK(ctx, cudaMemcpyAsync(base + o_end, end.data(), ndev * 8, cudaMemcpyHostToDevice, ctx->stream));
+            // device groups below 2^31 items (cub's int item count)
+            size_t d0 = 0;
+            while (d0 < ndev) {
+                size_t d1 = d0 + 1;
+                while (d1 < ndev && off[d1 + 1] - off[d0] < (1ull << 31)) ++d1;
+                const uint64_t gb = off[d0];
+                std::vector<uint64_t> gbeg(d1 - d0), gend(d1 - d0);
+                for (size_t d = d0; d < d1; ++d) {
+                    gbeg[d - d0] = beg[d] - gb;
+                    gend[d - d0] = end[d] - gb;
+                }
+                COLO_CK(ctx, cudaMemcpyAsync(base + o_beg, gbeg.data(), gbeg.size() * 8, cudaMemcpyHostToDevice,
+                                             ctx->stream));
+                COLO_CK(ctx, cudaMemcpyAsync(base + o_end, gend.data(), gend.size() * 8, cudaMemcpyHostToDevice,
+                                             ctx->stream));
+                size_t tb = tmp_bytes;
+                COLO_CK(ctx, cub::DeviceSegmentedSort::StableSortPairs(
+                                 base + o_tmp, tb, P.job_t + gb, reinterpret_cast<double*>(base + o_jt2) + gb,
+                                 P.job_q + gb, reinterpret_cast<uint32_t*>(base + o_jq2) + gb,
+                                 static_cast<int>(off[d1] - gb), static_cast<int>(d1 - d0),
+                                 reinterpret_cast<const uint64_t*>(base + o_beg),
+                                 reinterpret_cast<const uint64_t*>(base + o_end), ctx->stream));
+                COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));  // the offset arrays are reused per group
+                d0 = d1;
+            }
+            jt = reinterpret_cast<const double*>(base + o_jt2);
+            jq = reinterpret_cast<const uint32_t*>(base + o_jq2);
+        }
+        k_trainer_fold<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P, jt, jq);
+        COLO_CK(ctx, cudaGetLastError());
+        COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
     if (flag & 2) return set_err(ctx, COLO_EBREACH, "colocated replay: invariant breach on at least one device");
     return COLO_OK;
 }
@@ -1146,6 +1382,7 @@ colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, 
                 t.prefetch_wait_seconds += s.prefetch_wait_seconds;
                 t.completed_jobs += s.completed_jobs;
                 t.map_fallbacks += s.map_fallbacks;
+                t.oom_jobs += s.oom_jobs;
                 t.batches += s.batches;
                 t.max_batch_size = std::max(t.max_batch_size, s.max_batch_size);
                 t.offload_decisions += s.offload_decisions;

@@ -211,19 +211,30 @@ def colocated_cases(ref):
     a, p, o, ld = ref.generate_trace(0.1, 40 / 0.1 + 200, ("uniform", 6519.0, 8610.0), 867572, ("uniform", 0.0, 5.0),
                                      with_labels=True)
     cases["breach_small_cpt"] = (m, g4, Grid(250, 500, 5, 8000, 8000, 50), 0, 60.0, a, p, o, ld)
+    # SeparateCluster ("baseline") and ServingOnly runs of the same engine
+    a, p, o, ld = ref.generate_trace(0.3, 600.0, ("histogram", hv, hp), 41, ("fixed", 0.01), with_labels=True)
+    cases["baseline_q03_cpa"] = (m, g, grid, 1, 60.0, a, p, o, ld, 2)
+    cases["baseline_q03_cpt"] = (m, g, grid, 0, 60.0, a, p, o, ld, 2)
+    cases["serving_q03"] = (m, g, grid, 1, 60.0, a, p, o, ld, 0)
+    a, p, o, ld = ref.generate_trace(0.5, 400.0, ("uniform", 500, 7000), 13, ("uniform", 0.0, 200.0), with_labels=True)
+    ld[::4] = -1.0
+    cases["baseline_varlabels_cpa"] = (m, g, grid, 1, 60.0, a, p, o, ld, 2)  # label delays vary: sorted job stream
+    cases["baseline_oom_phi_cpa"] = (phi14b_model(), g, grid, 1, 60.0, a, p, o, ld, 2)
     return cases
 
 
 def colocated(ref):
     out = {}
     names = []
-    for name, (m, g, grid, cpa, to, a, p, o, ld) in colocated_cases(ref).items():
-        r = ref.replay_colocated(m, g, grid, cpa, a, p, o, ld, to)
+    for name, c in colocated_cases(ref).items():
+        m, g, grid, cpa, to, a, p, o, ld = c[:9]
+        sim = c[9] if len(c) > 9 else 1
+        r = ref.replay_colocated(m, g, grid, cpa, a, p, o, ld, to, sim_mode=["serving-only", "colocated", "baseline"][sim])
         names.append(name)
         out[f"{name}_model"] = np.frombuffer(bytes(m), np.uint8)
         out[f"{name}_gpu"] = np.frombuffer(bytes(g), np.uint8)
         out[f"{name}_grid"] = np.frombuffer(bytes(grid), np.uint8)
-        out[f"{name}_cfg"] = np.array([cpa, to], np.float64)
+        out[f"{name}_cfg"] = np.array([cpa, to, sim], np.float64)
         out[f"{name}_a"], out[f"{name}_p"], out[f"{name}_o"], out[f"{name}_ld"] = a, p, o, ld
         out[f"{name}_rc"] = np.array([r["rc"]])
         out[f"{name}_report"] = np.frombuffer(bytes(_report_struct(r["report"])), np.uint8)
@@ -233,7 +244,8 @@ def colocated(ref):
             b = r["batches"]
             out[f"{name}_batches"] = np.stack([b["start"], b["end"], b["first"].astype(np.float64),
                                                b["n"].astype(np.float64)], 1)
-        print(name, len(a), r["rc"], {k: r["report"][k] for k in ("completed_jobs", "recomputes", "loads", "labels_dropped")})
+        print(name, len(a), r["rc"], {k: r["report"][k] for k in ("completed_jobs", "recomputes", "loads", "labels_dropped",
+                                                                   "oom_jobs")})
     out["names"] = np.array(names)
     np.savez_compressed(os.path.join(HERE, "colocated.npz"), **out)
 

@@ -51,9 +51,10 @@ def case(z, name):
     m = Model.from_buffer_copy(z[f"{name}_model"].tobytes())
     g = Gpu.from_buffer_copy(z[f"{name}_gpu"].tobytes())
     grid = Grid.from_buffer_copy(z[f"{name}_grid"].tobytes())
-    cpa, to = z[f"{name}_cfg"]
+    cpa, to, sim = z[f"{name}_cfg"]
     rep = ColoReport.from_buffer_copy(z[f"{name}_report"].tobytes())
-    return m, g, grid, int(cpa), float(to), z[f"{name}_a"], z[f"{name}_p"], z[f"{name}_o"], z[f"{name}_ld"], rep
+    return (m, g, grid, int(cpa), float(to), z[f"{name}_a"], z[f"{name}_p"], z[f"{name}_o"], z[f"{name}_ld"], rep,
+            ["serving-only", "colocated", "baseline"][int(sim)])
 
 
 def upload(traces):
@@ -87,18 +88,19 @@ def batches_of(raw, lo, nb):
 
 def test_golden_each_case(ctx, gold):
     for name in gold["names"]:
-        m, g, grid, cpa, to, a, p, o, ld, rep = case(gold, name)
+        m, g, grid, cpa, to, a, p, o, ld, rep, sim = case(gold, name)
         ms = mapset(ctx, m, g, grid, cpa)
         da, dp, do, dld, doff, off = upload([(a, p, o, ld)])
         dset = torch.zeros(1, dtype=torch.int16, device="cuda")
         rc = int(gold[f"{name}_rc"][0])
+        sm = cs.SimMode.parse(sim)
         if rc == 3:
             with pytest.raises(cs.ColoBreachError) as ei:
-                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to)
+                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to, sim_mode=sm)
             assert cs.colocated_summaries(ei.value.result["summary"])[0]["status"] == 3, name
             continue
         r = cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to, samples=True,
-                                batches=True)
+                                batches=True, sim_mode=sm)
         s = cs.colocated_summaries(r["summary"])[0]
         assert s["status"] == 0
         assert not diff(s, rep), (name, diff(s, rep))
@@ -126,20 +128,22 @@ def test_golden_one_launch_many_devices(ctx, gold):
     sets, keys, traces, devs = [], {}, [], []
     for rep_i in range(3):
         for n in names:
-            m, g, grid, cpa, to, a, p, o, ld, rep = case(gold, n)
+            m, g, grid, cpa, to, a, p, o, ld, rep, sim = case(gold, n)
             k = (bytes(m), bytes(g), bytes(grid), cpa)
             if k not in keys:
                 keys[k] = len(sets)
                 sets.append(mapset(ctx, m, g, grid, cpa))
             traces.append((a, p, o, ld))
-            devs.append((n, keys[k], rep))
+            devs.append((n, keys[k], rep, int(cs.SimMode.parse(sim))))
     da, dp, do, dld, doff, off = upload(traces)
     dset = torch.tensor([d[1] for d in devs], dtype=torch.int16, device="cuda")
-    r = cs.replay_colocated(ctx, sets, da, dp, do, doff, dset, label_delay=dld, samples=True, batches=True)
+    dmode = torch.tensor([d[3] for d in devs], dtype=torch.uint8, device="cuda")
+    r = cs.replay_colocated(ctx, sets, da, dp, do, doff, dset, label_delay=dld, samples=True, batches=True,
+                            sim_mode=dmode)
     S = cs.colocated_summaries(r["summary"])
     smp = r["samples"].cpu().numpy()
     so = r["sample_offsets"].cpu().numpy()
-    for i, (n, _, rep) in enumerate(devs):
+    for i, (n, _, rep, _) in enumerate(devs):
         assert not diff(S[i], rep), (n, diff(S[i], rep))
         assert np.array_equal(smp[so[i]:so[i + 1]].view(np.uint64), gold[f"{n}_samples"].view(np.uint64)), n
         b = batches_of(r["batches"], int(off[i]), S[i]["batches"])
@@ -218,21 +222,68 @@ def test_colocated_stats_exact(ctx, gold, orc):
     1e-12 relative (exact fixed-point sum vs the sorted sequential sum)."""
     names = [n for n in gold["names"] if int(gold[f"{n}_rc"][0]) == 0 and float(gold[f"{n}_cfg"][1]) == 60.0
              and len(gold[f"{n}_samples"])]
-    sets, keys, traces, dset, allsmp = [], {}, [], [], []
+    sets, keys, traces, dset, dmode, allsmp = [], {}, [], [], [], []
     for n in names:
-        m, g, grid, cpa, to, a, p, o, ld, rep = case(gold, n)
+        m, g, grid, cpa, to, a, p, o, ld, rep, sim = case(gold, n)
         k = (bytes(m), bytes(g), bytes(grid), cpa)
         if k not in keys:
             keys[k] = len(sets)
             sets.append(mapset(ctx, m, g, grid, cpa))
         traces.append((a, p, o, ld))
         dset.append(keys[k])
+        dmode.append(int(cs.SimMode.parse(sim)))
         allsmp.append(gold[f"{n}_samples"])
     da, dp, do, dld, doff, off = upload(traces)
     dset = torch.tensor(dset, dtype=torch.int16, device="cuda")
-    pctl, tot = cs.colocated_stats(ctx, sets, da, dp, do, doff, dset, label_delay=dld)
+    dmode = torch.tensor(dmode, dtype=torch.uint8, device="cuda")
+    pctl, tot = cs.colocated_stats(ctx, sets, da, dp, do, doff, dset, label_delay=dld, sim_mode=dmode)
     u = np.concatenate(allsmp)
     p50, p90, p99, mean = orc.finalize(u)
     assert pctl[:3] == [p50, p90, p99]
     assert abs(pctl[3] - mean) <= 1e-12 * abs(mean)
     assert tot["generated_tokens"] == len(u)
+
+
+def test_modes_vs_oracle_random(ctx, orc):
+    """ServingOnly and SeparateCluster devices (constant, varying and absent
+    label delays: the sorted job-stream path) mixed with Colocated devices in
+    one launch; every device equals the restatement."""
+    rng = np.random.default_rng(5)
+    hv, hp = sharegpt_histogram()
+    m, g, grid = default_model(), default_gpu(), default_grid()
+    phi = phi14b_model()
+    sets = [mapset(ctx, m, g, grid, 1), mapset(ctx, m, g, grid, 0), mapset(ctx, phi, g, grid, 1)]
+    models = [(m, 1), (m, 0), (phi, 1)]
+    traces, dset, dmode, refs = [], [], [], []
+    for it in range(36):
+        si = it % 3
+        mode = ["serving-only", "colocated", "baseline"][(it // 3) % 3]
+        qps = float(rng.choice([0.05, 0.3, 1.0, 2.5]))
+        dist = ("histogram", hv, hp) if it % 2 else ("uniform", 200.0, 7000.0)
+        spec = ("fixed", 0.01) if it % 4 == 0 else ("uniform", 0.0, 100.0)
+        a, p, o, ld = orc.generate_trace(qps, 40 / qps + 60, dist, 300 + it, spec, with_labels=True)
+        if it % 5 == 1:
+            ld[1::3] = -1.0
+        if it % 7 == 3:
+            o = rng.integers(1, 250, len(a)).astype(np.uint32)
+        mm, cpa = models[si]
+        ref = orc.replay_colocated(mm, g, grid, cpa, a, p, o, ld, 60.0, tau=0.05, sim_mode=mode)
+        if ref["rc"]:
+            continue
+        traces.append((a, p, o, ld))
+        dset.append(si)
+        dmode.append(int(cs.SimMode.parse(mode)))
+        refs.append(ref)
+    da, dp, do, dld, doff, off = upload(traces)
+    r = cs.replay_colocated(ctx, sets, da, dp, do, doff, torch.tensor(dset, dtype=torch.int16, device="cuda"),
+                            label_delay=dld, tau=0.05, samples=True,
+                            sim_mode=torch.tensor(dmode, dtype=torch.uint8, device="cuda"))
+    S = cs.colocated_summaries(r["summary"])
+    smp = r["samples"].cpu().numpy()
+    so = r["sample_offsets"].cpu().numpy()
+    lab = r["labels"].cpu().numpy()
+    for i, ref in enumerate(refs):
+        assert not diff(S[i], ref["report"]), (i, dmode[i], diff(S[i], ref["report"]))
+        assert np.array_equal(smp[so[i]:so[i + 1]].view(np.uint64), ref["samples"].view(np.uint64)), i
+        assert np.array_equal(lab[off[i]:off[i + 1]], ref["labels"]), i
+    assert len(refs) >= 30 and {0, 1, 2} <= set(dmode)

@@ -28,9 +28,10 @@ def case(z, name):
     m = Model.from_buffer_copy(z[f"{name}_model"].tobytes())
     g = Gpu.from_buffer_copy(z[f"{name}_gpu"].tobytes())
     grid = Grid.from_buffer_copy(z[f"{name}_grid"].tobytes())
-    cpa, to = z[f"{name}_cfg"]
+    cpa, to, sim = z[f"{name}_cfg"]
     rep = ColoReport.from_buffer_copy(z[f"{name}_report"].tobytes())
-    return m, g, grid, int(cpa), float(to), z[f"{name}_a"], z[f"{name}_p"], z[f"{name}_o"], z[f"{name}_ld"], rep
+    return (m, g, grid, int(cpa), float(to), z[f"{name}_a"], z[f"{name}_p"], z[f"{name}_o"], z[f"{name}_ld"], rep,
+            ["serving-only", "colocated", "baseline"][int(sim)])
 
 
 def same_report(a, b):
@@ -47,7 +48,9 @@ def same_report(a, b):
 
 def test_fixture_inventory(gold):
     names = list(gold["names"])
-    assert len(names) >= 15
+    assert len(names) >= 20
+    modes = {float(gold[f"{n}_cfg"][2]) for n in names}
+    assert modes == {0.0, 1.0, 2.0}
     assert sum(int(gold[f"{n}_rc"][0]) == 3 for n in names) >= 2  # InvariantBreach cases
     assert any(int(ColoReport.from_buffer_copy(gold[f"{n}_report"].tobytes()).loads) > 0 for n in names)
     assert any(int(ColoReport.from_buffer_copy(gold[f"{n}_report"].tobytes()).recomputes) > 0 for n in names)
@@ -58,8 +61,8 @@ def test_oracle_matches_golden(orc, gold):
     """Every MetricsReport field bit-for-bit, samples bit-for-bit, batch
     timeline (start, end, first, n) and the breach verdicts."""
     for name in gold["names"]:
-        m, g, grid, cpa, to, a, p, o, ld, rep = case(gold, name)
-        r = orc.replay_colocated(m, g, grid, cpa, a, p, o, ld, to)
+        m, g, grid, cpa, to, a, p, o, ld, rep, sim = case(gold, name)
+        r = orc.replay_colocated(m, g, grid, cpa, a, p, o, ld, to, sim_mode=sim)
         assert r["rc"] == int(gold[f"{name}_rc"][0]), name
         if r["rc"] != 0:
             continue
@@ -127,6 +130,39 @@ def test_generate_trace_label_delays(orc):
         y = ref.generate_trace(0.3, 500.0, ("uniform", 100, 3000), 11, spec, with_labels=True)
         for u, v in zip(x, y):
             assert np.array_equal(np.asarray(u).view(np.uint8), np.asarray(v).view(np.uint8))
+
+
+def test_oracle_matches_reference_fuzz_modes(orc):
+    """ServingOnly and SeparateCluster runs of the restated engine equal the
+    reference's, including OOM jobs and varying / absent label delays."""
+    if not os.path.exists(PATHS["ref"]):
+        pytest.skip("oracle/_ref not built")
+    ref = OracleLib("ref")
+    rng = np.random.default_rng(99)
+    n_oom = 0
+    for it in range(40):
+        m = default_model() if it % 2 else phi14b_model()
+        g = default_gpu()
+        grid = default_grid()
+        cpa = int(rng.integers(0, 2))
+        mode = "baseline" if it % 4 else "serving-only"
+        qps = float(rng.choice([0.05, 0.3, 1.0, 3.0]))
+        lo_, hi_ = sorted(rng.integers(1, 8000, 2))
+        a, p, o, ld = orc.generate_trace(qps, 30 / qps + 60, ("uniform", float(lo_), float(hi_ + 1)),
+                                         int(rng.integers(1 << 30)), ("uniform", 0.0, float(rng.choice([0.01, 300]))),
+                                         with_labels=True)
+        if it % 3 == 0:
+            ld[::3] = -1.0
+        try:
+            r1 = ref.replay_colocated(m, g, grid, cpa, a, p, o, ld, 60.0, sim_mode=mode)
+        except ValueError:
+            continue
+        r2 = orc.replay_colocated(m, g, grid, cpa, a, p, o, ld, 60.0, sim_mode=mode)
+        assert r1["rc"] == r2["rc"] == 0
+        assert not same_report(r2["report"], r1["report"]), (it, same_report(r2["report"], r1["report"]))
+        assert np.array_equal(r1["samples"].view(np.uint64), r2["samples"].view(np.uint64))
+        n_oom += r1["report"]["oom_jobs"] > 0
+    assert n_oom >= 3
 
 
 def test_oracle_matches_reference_fuzz(orc):
