@@ -8,6 +8,8 @@
 //   GpuMaps::hedge_lookup(cached, freed)                             maps.hpp:276-280 (std::optional)
 //   GpuMaps::decide(tuples) / decide_exact(...)                      engine.hpp:434-448, 513-557 in bulk
 //   colosim_gpu::replay_serving(...)                                 engine.hpp:140-387 (ServingOnly)
+//   colosim_gpu::run_simulation<MetricsReport>(ctx, cfg)             engine.hpp:938-941 (every SimMode)
+//   colosim_gpu::run_simulations<MetricsReport>(ctx, cfgs)           many runs as one device fleet
 // and throws the reference's exception types for the reference's error
 // cases: std::runtime_error for validation (COLO_EVALIDATION),
 // std::invalid_argument for contract violations (COLO_EINVAL).  Any struct
@@ -15,7 +17,10 @@
 // converts, so colosim's own profile objects can be passed unchanged.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <limits>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -205,6 +210,217 @@ ServingReplay replay_serving(Context& ctx, const ModelProfile& m, const GpuProfi
     }
     for (void* p : {d_a, d_p, d_o, d_off, d_soff, d_prof, d_s, d_l, d_sum}) colo_dev_free(c, p);
     return r;
+}
+
+/// The reference throws InvariantBreach (engine.hpp:43-46), a std::runtime_error.
+struct invariant_breach : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+
+template <class SimConfig>
+int sim_mode_of(const SimConfig& cfg) {
+    using M = decltype(cfg.mode);
+    if (cfg.mode == M::Colocated) return COLO_SIM_COLOCATED;
+    if (cfg.mode == M::SeparateCluster) return COLO_SIM_SEPARATE;
+    return COLO_SIM_SERVING_ONLY;
+}
+
+template <class SimConfig>
+bool is_cpa(const SimConfig& cfg) {
+    return cfg.training == decltype(cfg.training)::CPA;
+}
+
+// The config's own maps as device cells (OffloadingMap::cell / HedgingMap::cell,
+// maps.hpp:89-94, 269-270).  Non-colocated runs never consult them
+// (SimConfig::validate checks maps only in Colocated mode, engine.hpp:62-68):
+// those get freshly built maps of their profile.
+template <class SimConfig>
+colo_mapset* mapset_of(Context& ctx, const SimConfig& cfg) {
+    const colo_model m = to_c_model(cfg.model);
+    const colo_gpu g = to_c_gpu(cfg.gpu);
+    const colo_mode mode = is_cpa(cfg) ? COLO_CPA : COLO_CPT;
+    colo_mapset* ms = nullptr;
+    if (sim_mode_of(cfg) != COLO_SIM_COLOCATED) {
+        const colo_grid grid{500, 500, 5, 8000, 8000, 50};
+        check(colo_mapset_build(ctx.get(), &m, &g, &grid, mode, 500, 8000, 128, &ms), ctx.get(), "build_maps");
+        return ms;
+    }
+    const auto& om = cfg.offload_map;
+    const auto& hm = cfg.hedge_map;
+    const colo_grid grid = to_c_grid(om.steps, om.bounds);
+    if (om.mode != cfg.training || hm.mode != cfg.training)
+        throw std::runtime_error("sim config: map training mode does not match sim.training");  // engine.hpp:66-67
+    if (hm.profile_hash_value != om.profile_hash_value)
+        throw std::runtime_error("sim config: map profile hash does not match the profiles");  // engine.hpp:63-65
+    std::vector<std::uint8_t> off(om.cached_count() * om.incoming_count() * om.batch_count());
+    for (std::size_t ci = 0; ci < om.cached_count(); ++ci)
+        for (std::size_t ii = 0; ii < om.incoming_count(); ++ii)
+            for (std::size_t bi = 0; bi < om.batch_count(); ++bi) {
+                const auto& d = om.cell(ci, ii, bi);
+                using A = decltype(d.action);
+                off[(ci * om.incoming_count() + ii) * om.batch_count() + bi] =
+                    d.action == A::NoAction ? 0 : (d.action == A::AllToHost ? 1 : static_cast<std::uint8_t>(2 + d.layers));
+            }
+    std::vector<std::uint8_t> hed(hm.cached_count() * hm.freed_count());
+    for (std::size_t ci = 0; ci < hm.cached_count(); ++ci)
+        for (std::size_t fi = 0; fi < hm.freed_count(); ++fi)
+            hed[ci * hm.freed_count() + fi] = hm.cell(ci, fi) == decltype(hm.cell(ci, fi))::Recompute ? 1 : 0;
+    // refuses a hash other than profile_hash(model, gpu) (engine.hpp:63-65)
+    check(colo_mapset_from_cells(ctx.get(), &m, &g, &grid, mode, hm.cached_token_step, hm.max_cached_tokens,
+                                 hm.assumed_output_tokens, om.profile_hash_value, off.data(), off.size(), hed.data(),
+                                 hed.size(), &ms),
+          ctx.get(), "sim config maps");
+    return ms;
+}
+
+}  // namespace detail
+
+/// Simulation::run (engine.hpp:131-164) for every config, as one fleet of
+/// devices on the GPU (one launch per group of <= 16 distinct profiles and one
+/// cache timeout).  Returns the reference's own report type, finalized as
+/// metrics.hpp:56-69 does; equal (operator==) to run_simulation(cfg) on the
+/// CPU.  Throws std::runtime_error where the reference's constructor does and
+/// invariant_breach where its run() does.
+template <class Report, class SimConfig>
+std::vector<Report> run_simulations(Context& ctx, const std::vector<SimConfig>& cfgs) {
+    colo_ctx* c = ctx.get();
+    std::vector<Report> out(cfgs.size());
+    std::vector<std::size_t> todo;
+    for (std::size_t i = 0; i < cfgs.size(); ++i) {
+        const colo_model m = to_c_model(cfgs[i].model);
+        const colo_gpu g = to_c_gpu(cfgs[i].gpu);
+        check(colo_validate_profile_pair(&m, &g), c, "sim config");  // engine.hpp:61
+        todo.push_back(i);
+    }
+    while (!todo.empty()) {
+        // one launch: a shared cache timeout, at most 16 map sets
+        const double timeout = cfgs[todo[0]].cache_timeout;
+        std::vector<std::size_t> batch, rest;
+        std::vector<colo_mapset*> sets;
+        std::vector<std::uint16_t> dset;
+        for (std::size_t i : todo) {
+            if (cfgs[i].cache_timeout != timeout || sets.size() == 16) {
+                rest.push_back(i);
+                continue;
+            }
+            sets.push_back(detail::mapset_of(ctx, cfgs[i]));
+            dset.push_back(static_cast<std::uint16_t>(sets.size() - 1));
+            batch.push_back(i);
+        }
+        todo.swap(rest);
+        std::vector<double> a, ld;
+        std::vector<std::uint32_t> p, o;
+        std::vector<std::uint64_t> off{0}, soff{0};
+        std::vector<std::uint8_t> sm;
+        for (std::size_t i : batch) {
+            for (const auto& r : cfgs[i].trace.records) {
+                a.push_back(r.arrival_time);
+                p.push_back(static_cast<std::uint32_t>(r.prompt_tokens));
+                o.push_back(static_cast<std::uint32_t>(r.output_tokens));
+                ld.push_back(r.label_delay ? *r.label_delay : -1.0);
+            }
+            std::uint64_t ns = soff.back();
+            for (const auto& r : cfgs[i].trace.records) ns += r.output_tokens;
+            off.push_back(a.size());
+            soff.push_back(ns);
+            sm.push_back(static_cast<std::uint8_t>(detail::sim_mode_of(cfgs[i])));
+        }
+        const std::size_t n = a.size(), nd = batch.size(), ns = soff.back();
+        void *d_a, *d_p, *d_o, *d_ld, *d_off, *d_soff, *d_set, *d_sm, *d_s, *d_sum;
+        check(colo_dev_alloc(c, n * 8 + 8, &d_a), c, "alloc");
+        check(colo_dev_alloc(c, n * 4 + 4, &d_p), c, "alloc");
+        check(colo_dev_alloc(c, n * 4 + 4, &d_o), c, "alloc");
+        check(colo_dev_alloc(c, n * 8 + 8, &d_ld), c, "alloc");
+        check(colo_dev_alloc(c, (nd + 1) * 8, &d_off), c, "alloc");
+        check(colo_dev_alloc(c, (nd + 1) * 8, &d_soff), c, "alloc");
+        check(colo_dev_alloc(c, nd * 2 + 2, &d_set), c, "alloc");
+        check(colo_dev_alloc(c, nd + 1, &d_sm), c, "alloc");
+        check(colo_dev_alloc(c, ns * 8 + 8, &d_s), c, "alloc");
+        check(colo_dev_alloc(c, nd * sizeof(colo_colocated_summary), &d_sum), c, "alloc");
+        std::vector<colo_colocated_summary> sum(nd);
+        std::vector<double> smp(ns);
+        colo_status st = COLO_OK;
+        try {
+            check(colo_memcpy_h2d(c, d_a, a.data(), n * 8), c, "h2d");
+            check(colo_memcpy_h2d(c, d_p, p.data(), n * 4), c, "h2d");
+            check(colo_memcpy_h2d(c, d_o, o.data(), n * 4), c, "h2d");
+            check(colo_memcpy_h2d(c, d_ld, ld.data(), n * 8), c, "h2d");
+            check(colo_memcpy_h2d(c, d_off, off.data(), (nd + 1) * 8), c, "h2d");
+            check(colo_memcpy_h2d(c, d_soff, soff.data(), (nd + 1) * 8), c, "h2d");
+            check(colo_memcpy_h2d(c, d_set, dset.data(), nd * 2), c, "h2d");
+            check(colo_memcpy_h2d(c, d_sm, sm.data(), nd), c, "h2d");
+            colo_colocated_opts opt{};
+            opt.cache_timeout = timeout;
+            opt.d_label_delay = static_cast<const double*>(d_ld);
+            opt.tau = std::numeric_limits<double>::infinity();
+            opt.d_samples = static_cast<double*>(d_s);
+            opt.d_sample_offsets = static_cast<const std::uint64_t*>(d_soff);
+            opt.d_summary = static_cast<colo_colocated_summary*>(d_sum);
+            opt.d_dev_sim_mode = static_cast<const std::uint8_t*>(d_sm);
+            st = colo_replay_colocated(c, sets.data(), sets.size(), static_cast<double*>(d_a),
+                                       static_cast<std::uint32_t*>(d_p), static_cast<std::uint32_t*>(d_o), n,
+                                       static_cast<std::uint64_t*>(d_off), static_cast<std::uint16_t*>(d_set), nd, &opt);
+            if (st != COLO_OK && st != COLO_EBREACH) check(st, c, "run_simulation");
+            check(colo_memcpy_d2h(c, sum.data(), d_sum, nd * sizeof(colo_colocated_summary)), c, "d2h");
+            check(colo_memcpy_d2h(c, smp.data(), d_s, ns * 8), c, "d2h");
+        } catch (...) {
+            for (void* q : {d_a, d_p, d_o, d_ld, d_off, d_soff, d_set, d_sm, d_s, d_sum}) colo_dev_free(c, q);
+            for (auto* ms : sets) colo_mapset_destroy(ms);
+            throw;
+        }
+        for (void* q : {d_a, d_p, d_o, d_ld, d_off, d_soff, d_set, d_sm, d_s, d_sum}) colo_dev_free(c, q);
+        for (auto* ms : sets) colo_mapset_destroy(ms);
+        for (std::size_t k = 0; k < nd; ++k) {
+            const colo_colocated_summary& s = sum[k];
+            if (s.status == COLO_EBREACH) throw invariant_breach("colo-b200: invariant breach in run_simulation");
+            const SimConfig& cfg = cfgs[batch[k]];
+            Report& r = out[batch[k]];
+            r.tpt_samples.assign(smp.begin() + soff[k], smp.begin() + soff[k] + s.generated_tokens);
+            r.trained_tokens = s.trained_tokens;
+            r.training_busy_time = s.training_busy_time;
+            r.peak_device_bytes = s.peak_device_bytes;
+            r.peak_training_activation_bytes = s.peak_training_activation_bytes;
+            r.oom_flag = s.oom_jobs > 0;
+            r.preemptions = s.preemptions;
+            r.layers_freed = s.layers_freed;
+            r.loads = s.loads;
+            r.recomputes = s.recomputes;
+            r.copy_stall_seconds = s.copy_stall_seconds;
+            r.labels_dropped = s.labels_dropped;
+            r.prefetch_wait_seconds = s.prefetch_wait_seconds;
+            r.completed_jobs = s.completed_jobs;
+            r.oom_jobs = s.oom_jobs;
+            r.map_fallbacks = s.map_fallbacks;
+            r.generated_tokens = s.generated_tokens;
+            r.trace_hash = cfg.trace.content_hash();                                   // engine.hpp:157
+            r.mode_tag = std::string(to_string(cfg.mode)) + "/" + to_string(cfg.training);  // :158
+            // finalize (metrics.hpp:56-69) on the host copy of the samples
+            if (!r.tpt_samples.empty()) {
+                std::vector<double> sorted = r.tpt_samples;
+                std::sort(sorted.begin(), sorted.end());
+                auto rank = [&](double q) {
+                    std::size_t k2 = static_cast<std::size_t>(std::ceil(q * static_cast<double>(sorted.size())));
+                    return sorted[(k2 == 0 ? 1 : k2) - 1];
+                };
+                r.tpt_p50 = rank(0.50);
+                r.tpt_p90 = rank(0.90);
+                r.tpt_p99 = rank(0.99);
+                double acc = 0;
+                for (double v : sorted) acc += v;
+                r.tpt_mean = acc / static_cast<double>(sorted.size());
+            }
+            if (r.training_busy_time > 0)
+                r.training_throughput = static_cast<double>(r.trained_tokens) / r.training_busy_time;
+        }
+    }
+    return out;
+}
+
+template <class Report, class SimConfig>
+Report run_simulation(Context& ctx, const SimConfig& cfg) {
+    return run_simulations<Report>(ctx, std::vector<SimConfig>{cfg})[0];
 }
 
 }  // namespace colosim_gpu

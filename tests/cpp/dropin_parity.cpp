@@ -120,6 +120,61 @@ int main() {
             EXPECT(g.summary.generated_tokens == rep.generated_tokens, "generated tokens");
         }
     }
+    // Simulation::run in every mode: the reference's MetricsReport, operator== (samples,
+    // finalize results, counters, mode tag, trace hash), from one GPU fleet launch
+    {
+        const GpuProfile gpu;
+        std::vector<SimConfig> cfgs;
+        std::vector<BuiltMaps> keep;
+        for (ModelProfile model : {ModelProfile{}, ModelProfile::phi14b_like()})
+            for (TrainingMode tm : {TrainingMode::CPA, TrainingMode::CPT}) {
+                BuiltMaps maps = build_maps(model, gpu, GridSteps{}, GridBounds{}, tm);
+                int k = 0;
+                for (double qps : {0.05, 0.3, 1.2})
+                    for (SimMode sm : {SimMode::Colocated, SimMode::SeparateCluster, SimMode::ServingOnly}) {
+                        std::optional<LengthDistribution> ld = LengthDistribution::fixed(0.01);
+                        if (++k % 3 == 0) ld = LengthDistribution::uniform(0.0, 60.0);
+                        Trace t = generate_trace(qps, 60.0 / qps + 200.0, LengthDistribution::uniform(300, 7000), ld,
+                                                 100 + k);
+                        cfgs.push_back(make_sim_config(model, gpu, sm, tm, maps, t, 60.0));
+                    }
+            }
+        // the engine tests' offload / stream cases (tests/test_engine.cpp:213-248)
+        BuiltMaps cpa = build_maps(ModelProfile{}, gpu, GridSteps{}, GridBounds{}, TrainingMode::CPA);
+        Trace burst;
+        burst.records = {QueryRecord{0, 0.0, 4000, 128, 0.01}};
+        for (std::uint64_t i = 1; i <= 10; ++i)
+            burst.records.push_back(QueryRecord{i, 4.6 + 0.001 * double(i), 2000, 128, std::nullopt});
+        cfgs.push_back(make_sim_config(ModelProfile{}, gpu, SimMode::Colocated, TrainingMode::CPA, cpa, burst));
+        cfgs.push_back(make_sim_config(ModelProfile{}, gpu, SimMode::Colocated, TrainingMode::CPA, cpa,
+                                       uncontended_trace(6000, 2, 2000.0)));
+        cfgs.push_back(make_sim_config(ModelProfile{}, gpu, SimMode::SeparateCluster, TrainingMode::CPA, cpa,
+                                       uncontended_trace(4000, 2, 2000.0)));  // trainer OOM datapoint
+        std::vector<MetricsReport> got = colosim_gpu::run_simulations<MetricsReport>(ctx, cfgs);
+        size_t bad = 0;
+        for (size_t i = 0; i < cfgs.size(); ++i) {
+            MetricsReport want = run_simulation(cfgs[i]);
+            if (!(got[i] == want)) {
+                ++bad;
+                std::printf("  run %zu (%s): generated %llu/%llu trained %llu/%llu jobs %llu/%llu\n", i,
+                            want.mode_tag.c_str(), (unsigned long long)got[i].generated_tokens,
+                            (unsigned long long)want.generated_tokens, (unsigned long long)got[i].trained_tokens,
+                            (unsigned long long)want.trained_tokens, (unsigned long long)got[i].completed_jobs,
+                            (unsigned long long)want.completed_jobs);
+            }
+        }
+        EXPECT(bad == 0, "%zu of %zu MetricsReports differ from Simulation::run", bad, cfgs.size());
+        EXPECT(got.back().oom_flag && got.back().oom_jobs == 2, "trainer OOM datapoint");
+        // the constructor's refusals (engine.hpp:60-75)
+        SimConfig badhash = cfgs[0];
+        badhash.offload_map.profile_hash_value ^= 1;
+        badhash.hedge_map.profile_hash_value ^= 1;
+        try {
+            colosim_gpu::run_simulation<MetricsReport>(ctx, badhash);
+            EXPECT(false, "map hash mismatch accepted");
+        } catch (const std::runtime_error&) {
+        }
+    }
     // the reference's error contract through the shim
     try {
         GpuProfile tiny;
