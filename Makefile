@@ -3,10 +3,11 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 PKG := paper_2503_01066_b200
-SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu $(PKG)/csrc/colo_colocated.cu
+SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu $(PKG)/csrc/colo_colocated.cu $(PKG)/csrc/colo_report.cpp
 HDR := include/colo_abi.h $(PKG)/csrc/colo_common.cuh $(PKG)/csrc/colo_internal.h $(PKG)/csrc/colo_replay.cuh
 # -fmad=false: no FMA contraction anywhere (bit-exact f64 vs the x86 reference)
-NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Iinclude -Xcompiler -fPIC,-O2 -Xptxas -v
+JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+NVFLAGS := $(ARCH) -O3 -lineinfo -fmad=false -std=c++17 -Iinclude -I$(JSON_DIR) -Xcompiler -fPIC,-O2 -Xptxas -v
 
 all: $(PKG)/libcolo_b200.so oracle dropin
 
@@ -25,7 +26,6 @@ clean:
 # C++ drop-in parity program: the unchanged reference headers + colosim_gpu.hpp
 # (build-time dependency on /root/reference; the binary travels to the GPU box)
 REF ?= /root/reference/proj
-JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 dropin: build/dropin_parity
 
 build/dropin_parity: tests/cpp/dropin_parity.cpp $(PKG)/cpp/colosim_gpu.hpp include/colo_abi.h $(PKG)/libcolo_b200.so

@@ -411,6 +411,21 @@ colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, 
                                  const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev,
                                  const colo_colocated_opts* opts, double* pctl, colo_colocated_summary* totals);
 
+/* ------------------------------------------------------------ report helpers */
+/* Trace::content_hash (workload.hpp:140-161): FNV-1a over (query_id, arrival
+ * bits, prompt, output, label_delay bits -- -1.0 for nullopt) per record.
+ * label_delay may be NULL (all nullopt); a negative or NaN entry is nullopt. */
+uint64_t colo_trace_hash(const uint64_t* query_id, const double* arrival, const uint32_t* prompt,
+                         const uint32_t* output, const double* label_delay, size_t n);
+/* Ascending sort of n f64 values on the device (the sorted TPT samples of
+ * finalize / export_tpt_cdf, metrics.hpp:59-60, 280-288).  d_in and d_out may
+ * not alias.  Synchronous. */
+colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size_t n);
+/* n doubles formatted as nlohmann::json::dump() writes them (the reference's
+ * report serializer, metrics.hpp:191-226), comma-separated, NUL-terminated
+ * into out when cap exceeds the length.  Returns the length (without NUL). */
+int64_t colo_json_doubles(const double* v, size_t n, char* out, size_t cap);
+
 /* --------------------------------------------------------- trace synthesis */
 /* generate_trace (workload.hpp:193-220) on the host, bit-exact (mt19937_64 +
  * libm log).  dist kind: 0 fixed, 1 uniform, 2 histogram.  Returns the query

@@ -410,7 +410,7 @@ class OracleLib:
         return res
 
     def replay_colocated(self, m, g, grid, cpa, arrival, prompt, output, label_delay=None, cache_timeout=60.0,
-                         tau=float("inf"), want_samples=True, want_batches=True, sim_mode="colocated"):
+                         tau=float("inf"), want_samples=True, want_batches=True, sim_mode="colocated", cells=None):
         """Simulation::run in ``sim_mode`` (colocated | baseline | serving-only; maps from build_maps).
         label_delay: per-query seconds, < 0 = nullopt (None = all nullopt).
         Returns dict(report, samples, labels, batches, pctl, rc)."""
@@ -433,8 +433,10 @@ class OracleLib:
                                                C.c_uint64(n), vp(samples), vp(batches), C.byref(rep), vp(pctl))
             labels = None
         else:
-            off = self.build_offloading_map(m, g, grid, cpa)
-            hed = self.build_hedging_map(m, g, grid.cached_step, grid.max_cached, cpa, 128)
+            if cells is None:
+                cells = (self.build_offloading_map(m, g, grid, cpa),
+                         self.build_hedging_map(m, g, grid.cached_step, grid.max_cached, cpa, 128))
+            off, hed = cells
             mp = Maps(grid, off.ctypes.data, grid.cached_step, grid.max_cached, hed.ctypes.data, m.num_layers)
             rc = self.lib.orc_replay_sim(C.byref(m), C.byref(g), C.byref(mp), C.c_int(SIM_MODES[sim_mode]), C.c_int(int(cpa)),
                                                C.c_double(cache_timeout), vp(arrival), vp(prompt), vp(output), vp(ld),

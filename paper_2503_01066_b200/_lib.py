@@ -174,7 +174,8 @@ EXPORTS = [
     "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
     "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
     "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
-    "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats",
+    "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats", "colo_trace_hash",
+    "colo_sort_f64", "colo_json_doubles",
 ]
 
 
@@ -228,6 +229,9 @@ def lib() -> C.CDLL:
         "colo_nearest_rank_index": (u64, [dbl, u64]),
         "colo_serving_stats": (i32, [vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp, C.POINTER(DeviceSummary)]),
         "colo_generate_trace": (C.c_int64, [dbl, dbl, C.POINTER(Dist), C.POINTER(Dist), u64, vp, vp, vp, vp, sz]),
+        "colo_trace_hash": (u64, [vp, vp, vp, vp, vp, sz]),
+        "colo_sort_f64": (i32, [vp, vp, vp, sz]),
+        "colo_json_doubles": (C.c_int64, [vp, sz, C.c_char_p, sz]),
         "colo_replay_colocated": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts)]),
         "colo_colocated_stats": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts), vp,
                                        C.POINTER(ColocatedSummary)]),

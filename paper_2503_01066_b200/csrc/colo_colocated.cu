@@ -46,6 +46,7 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "colo_internal.h"
@@ -1297,6 +1298,21 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
         COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     }
     if (flag & 2) return set_err(ctx, COLO_EBREACH, "colocated replay: invariant breach on at least one device");
+    return COLO_OK;
+}
+
+colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size_t n) {
+    if (!ctx || (n && (!d_in || !d_out)) || d_in == d_out) return COLO_EINVAL;
+    if (n == 0) return COLO_OK;
+    if (n >= (1ull << 31)) return set_err(ctx, COLO_EINVAL, "colo_sort_f64: at most 2^31-1 values");
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    size_t tb = 0;
+    COLO_CK(ctx, cub::DeviceRadixSort::SortKeys(nullptr, tb, d_in, d_out, static_cast<int>(n), 0, 64, ctx->stream));
+    const colo_status st = grow_scratch(ctx, tb + 256);
+    if (st != COLO_OK) return st;
+    COLO_CK(ctx, cub::DeviceRadixSort::SortKeys(ctx->d_rscratch, tb, d_in, d_out, static_cast<int>(n), 0, 64,
+                                                ctx->stream));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return COLO_OK;
 }
 

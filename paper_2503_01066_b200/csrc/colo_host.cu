@@ -322,3 +322,28 @@ extern "C" int64_t colo_generate_trace(double qps, double duration, const colo_d
     }
     return static_cast<int64_t>(n);
 }
+
+// Trace::content_hash, workload.hpp:140-161
+extern "C" uint64_t colo_trace_hash(const uint64_t* query_id, const double* arrival, const uint32_t* prompt,
+                                    const uint32_t* output, const double* label_delay, size_t n) {
+    uint64_t h = 14695981039346656037ull;
+    auto mix = [&h](uint64_t v) {
+        for (int i = 0; i < 8; ++i) {
+            h ^= (v >> (i * 8)) & 0xff;
+            h *= 1099511628211ull;
+        }
+    };
+    for (size_t i = 0; i < n; ++i) {
+        mix(query_id ? query_id[i] : static_cast<uint64_t>(i));
+        uint64_t bits;
+        std::memcpy(&bits, &arrival[i], 8);
+        mix(bits);
+        mix(prompt[i]);
+        mix(output[i]);
+        double d = label_delay ? label_delay[i] : -1.0;
+        if (!(d >= 0.0)) d = -1.0;
+        std::memcpy(&bits, &d, 8);
+        mix(bits);
+    }
+    return h;
+}
