@@ -46,3 +46,20 @@ def run_all(engine, tmp):
         check_dir(d, exp["compare"])
     finally:
         os.chdir(cwd)
+
+
+def run_cli_profile(tmp):
+    """`python -m paper_2503_01066_b200 profile` vs the reference CLI's map files."""
+    from paper_2503_01066_b200.__main__ import main
+
+    exp = json.load(open(os.path.join(CLI, "expected.json")))
+    cwd = os.getcwd()
+    os.chdir(CLI)
+    try:
+        d = os.path.join(tmp, "profile")
+        assert main(["profile", "--model", "llama8b.model", "--gpu", "b80.gpu", "--cached-step", "250", "--out", d]) == 0
+        check_dir(d, exp["profile"])
+        # the exit-code contract (tools/colosim.cpp:23-24, 347-353)
+        assert main(["run", "--config", "missing.config", "--out", os.path.join(tmp, "x")]) == 2
+    finally:
+        os.chdir(cwd)

@@ -51,11 +51,12 @@ def main():
     out = {}
     with tempfile.TemporaryDirectory() as tmp:
         jobs = {"run_colocated": ["run"], "run_baseline": ["run", "--mode", "baseline"],
-                "run_serving": ["run", "--mode", "serving-only"], "compare": ["compare"]}
+                "run_serving": ["run", "--mode", "serving-only"], "compare": ["compare"],
+                "profile": ["profile", "--model", "llama8b.model", "--gpu", "b80.gpu", "--cached-step", "250"]}
         for name, args in jobs.items():
             d = os.path.join(tmp, name)
-            subprocess.run([BIN, args[0], "--config", "small.config", "--out", d] + args[1:], cwd=CLI, check=True,
-                           capture_output=True)
+            cfg = [] if name == "profile" else ["--config", "small.config"]
+            subprocess.run([BIN, args[0]] + cfg + ["--out", d] + args[1:], cwd=CLI, check=True, capture_output=True)
             out[name] = {f: digest(os.path.join(d, f)) for f in sorted(os.listdir(d))}
     with open(os.path.join(CLI, "expected.json"), "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
