@@ -33,6 +33,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "colo_internal.h"
 #include "colo_replay.cuh"
 
@@ -104,6 +106,23 @@ struct ReplayParams {
     uint32_t nfilters, hist_shift, filter_shift;
     uint64_t prefix[3];
     int* err;
+    // Saturated fast path of the resolve pass (see k_sat_partition): per
+    // query q, the batch start_serving_batch forms at q when every query has
+    // already arrived -- [q, sat_end[q]) -- with its step count, prefill and
+    // per-step decode durations.  sat_end == 0: no record at q.
+    uint32_t* sat_end;     // [dev_off[d] + q]
+    uint32_t* sat_maxo;
+    uint64_t* sat_doff;    // first step duration in sat_dk
+    double* sat_pre;
+    const Seg* psegs;      // partition segments (longer than the replay segments: the greedy
+    uint32_t npsegs;       // partition from a segment's start needs a few batches to meet the true one)
+    uint64_t* sat_seg;     // [pseg] step durations of the segment's records, then their base (exclusive scan)
+    uint64_t* sat_exit;    // [pseg] pass 1: where the segment's own partition leaves it
+    uint32_t sat_pass;     // k_sat_partition pass (1 or 2)
+    uint64_t* sat_seg_start;  // [pseg] first recorded batch (pass 2)
+    double* sat_dk;
+    uint32_t sat_on;
+    unsigned long long* dbg;  // COLO_REPLAY_TIMING: [0] fast-path batches, [1] other batches of the resolve pass
 };
 
 enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
@@ -157,6 +176,110 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             tail = head + 1;
             tail_ptr = head + 1;
         } else {  // queued: every arrival with time <= T has been popped
+            if (MODE == RUN_RESOLVE && P.sat_on) {
+                // Saturated fast path: a record at head whose last member has
+                // already arrived is exactly the batch start_serving_batch forms
+                // (engine.hpp:292-306 never reaches the queue's end), so only the
+                // absolute-time chain remains: now = (T + 0.0) + prefill, then
+                // now += d_k for every step, in order.  Consecutive recorded
+                // batches run in a loop that loads batch i+1's record and
+                // durations while lane 0 chains batch i.
+                const uint32_t* __restrict__ se = P.sat_end + lo;
+                const uint32_t* __restrict__ smo = P.sat_maxo + lo;
+                const uint64_t* __restrict__ sdo = P.sat_doff + lo;
+                const double* __restrict__ spre = P.sat_pre + lo;
+                const double* __restrict__ pool = P.sat_dk;
+                uint64_t bend = se[head];
+                bool progressed = false;
+                if (bend != 0) {
+                    uint32_t K = smo[head];
+                    uint64_t dof = sdo[head];
+                    double pre = spre[head];
+                    double alast = arr[bend - 1];
+                    double cur[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t i = 32 * r + lane;
+                        cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
+                    }
+                    for (;;) {
+                        if (!(alast <= T)) break;  // a member has not arrived: form it the slow way
+                        const bool more = bend < stop && bend < N;
+                        const uint64_t nend = more ? se[bend] : 0;
+                        const bool hn = nend != 0;
+                        uint64_t ndof = 0;
+                        uint32_t nK = 0;
+                        double npre = 0.0, nalast = 0.0, nxt[4] = {0.0, 0.0, 0.0, 0.0};
+                        {  // records and durations stream forward: keep ~4 batches ahead in L2
+                            const char* q;
+                            if (lane < 16) q = reinterpret_cast<const char*>(pool + dof + 512) + lane * 128;
+                            else if (lane < 20) q = reinterpret_cast<const char*>(se + bend + 256) + (lane - 16) * 128;
+                            else if (lane < 24) q = reinterpret_cast<const char*>(smo + bend + 256) + (lane - 20) * 128;
+                            else if (lane < 28) q = reinterpret_cast<const char*>(sdo + bend + 256) + (lane - 24) * 256;
+                            else q = reinterpret_cast<const char*>(spre + bend + 256) + (lane - 28) * 256;
+                            if (bend + 1024 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                        }
+                        if (hn) {  // the next record and its durations, in flight during this chain
+                            nK = smo[bend];
+                            ndof = sdo[bend];
+                            npre = spre[bend];
+                            nalast = arr[nend - 1];
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) {
+                                const uint32_t i = 32 * r + lane;
+                                if (nK <= 128 && i < nK) nxt[r] = pool[ndof + i];
+                            }
+                        }
+                        double now = (T + 0.0) + pre;
+                        if (K <= 128) {
+#pragma unroll
+                            for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = cur[r];
+                            __syncwarp();
+                            if (lane == 0) {
+                                double t = now;
+#pragma unroll 8
+                                for (uint32_t i = 0; i < K; ++i) t = t + sDK[i];
+                                sDK[0] = t;
+                            }
+                            __syncwarp();
+                            now = sDK[0];
+                            __syncwarp();
+                        } else {
+                            for (uint32_t k0 = 0; k0 < K; k0 += 128) {
+                                const uint32_t c = min(128u, K - k0);
+#pragma unroll
+                                for (int r = 0; r < 4; ++r) {
+                                    const uint32_t i = 32 * r + lane;
+                                    if (i < c) sDK[i] = pool[dof + k0 + i];
+                                }
+                                __syncwarp();
+                                if (lane == 0) {
+                                    double t = now;
+                                    for (uint32_t i = 0; i < c; ++i) t = t + sDK[i];
+                                    sDK[0] = t;
+                                }
+                                __syncwarp();
+                                now = sDK[0];
+                                __syncwarp();
+                            }
+                        }
+                        T = now;
+                        head = bend;
+                        progressed = true;
+                        if (P.dbg && lane == 0) atomicAdd(P.dbg, 1ull);
+                        if (!hn) break;
+                        bend = nend;
+                        K = nK;
+                        dof = ndof;
+                        pre = npre;
+                        alast = nalast;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
+                    }
+                }
+                if (progressed) continue;
+            }
+            if (MODE == RUN_RESOLVE && P.dbg && lane == 0) atomicAdd(P.dbg + 1, 1ull);
             tail_ptr = find_tail(arr, N, tail_ptr < head ? head : tail_ptr, T);
             tail = tail_ptr;
         }
@@ -261,17 +384,25 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
 #pragma unroll
             for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = dk[r];
             __syncwarp();
+            // absolute-time chain now_k = now_{k-1} + d_k, sequential on one
+            // lane; the durations are overwritten by the absolute times
+            const uint32_t cnt = min(128u, maxo - k0);
+            if (lane == 0) {
+                double t = now;
+#pragma unroll 8
+                for (uint32_t i = 0; i < cnt; ++i) {
+                    t = t + sDK[i];
+                    sDK[i] = t;
+                }
+            }
+            __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                    if (k0 + 32 * r + l < maxo) {
-                        const double nw = now + sDK[32 * r + l];
-                        if (lane == static_cast<uint32_t>(l)) sv[r] = nw - now;  // now - last_token_time
-                        now = nw;
-                    }
-                }
+            for (int r = 0; r < 4; ++r) {  // sample = now - last_token_time
+                const uint32_t i = 32 * r + lane;
+                if (i < cnt) sv[r] = sDK[i] - (i ? sDK[i - 1] : now);
+            }
+            now = sDK[cnt - 1];
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
@@ -343,6 +474,200 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         __syncwarp();
     }
     if (MODE == RUN_SPEC && lane == 0) sp->nregen = ridx;
+}
+
+// All-queued ("saturated") batch records.  The batch start_serving_batch
+// forms at head q when every query up to its end has arrived depends on q
+// alone (FIFO, at least one, sum(need) <= budget: engine.hpp:292-306 without
+// reaching the queue's end), so any greedy partition yields valid records.
+// One warp per partition segment walks a greedy partition in 256-query
+// windows (lane l holds queries base+8l..+7, a warp scan gives the need
+// prefix, one ballot cuts each batch).  Pass 1 starts at the segment's first
+// query and only notes where its partition leaves the segment; pass 2 starts
+// at the previous segment's pass-1 exit and records every batch that starts
+// inside the segment.  Greedy partitions from different starts meet after
+// some batches (and then coincide), so pass 2 continues, segment after
+// segment, the partition the true run follows while the queue stays full.
+__global__ void __launch_bounds__(kWarps * 32) k_sat_partition(const __grid_constant__ ReplayParams P) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w >= P.npsegs) return;
+    const Seg sg = P.psegs[w];
+    const uint32_t d = sg.dev;
+    const uint32_t pi = P.dev_prof[d];
+    const colo_model& m = P.prof[pi].m;
+    const uint64_t budget = P.prof[pi].budget;
+    const uint64_t lo = P.dev_off[d], N = P.dev_off[d + 1] - lo;
+    const uint32_t* __restrict__ pp = P.p + lo;
+    const uint32_t* __restrict__ po = P.o + lo;
+    const bool rec = P.sat_pass == 2;
+    uint64_t h = sg.start, steps = 0;
+    if (rec && sg.start > 0) h = P.sat_exit[w - 1];  // the previous segment of this device (same device: start > 0)
+    if (lane == 0 && rec) P.sat_seg_start[w] = h;
+    auto record = [&](uint64_t start, uint64_t end, uint32_t mo) {
+        if (rec && lane == 0) {
+            P.sat_end[lo + start] = static_cast<uint32_t>(end);
+            P.sat_maxo[lo + start] = mo;
+        }
+        steps += mo;
+    };
+    while (h < sg.end) {
+        const uint64_t base = h;
+        uint64_t pre[8];
+        uint32_t oo[8];
+        uint64_t s = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const uint64_t j = base + lane * 8 + r;
+            const bool v = j < N;
+            const uint32_t pj = v ? pp[j] : 0u, oj = v ? po[j] : 0u;
+            s += v ? serving_memory(m, static_cast<uint64_t>(pj) + oj, 1) : 0ull;
+            pre[r] = s;
+            oo[r] = oj;
+        }
+        uint64_t incl = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        const uint64_t excl = incl - s;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) pre[r] += excl;  // need over [base, base + 8 lane + r]
+        const uint64_t wend = min(base + 256, N);
+        uint64_t hoff = 0;  // need over [base, h)
+        while (h < wend && h < sg.end) {
+            const uint64_t thr = hoff + budget;
+            uint32_t fr = 8;
+#pragma unroll
+            for (int r = 7; r >= 0; --r) {
+                const uint64_t j = base + lane * 8 + r;
+                if (j > h && j < wend && pre[r] > thr) fr = r;
+            }
+            const uint32_t bal = __ballot_sync(FULL, fr < 8);
+            uint64_t e;
+            if (bal) {
+                const uint32_t fl = __ffs(bal) - 1;
+                e = base + fl * 8 + __shfl_sync(FULL, fr, fl);
+            } else if (wend == N) {
+                e = N;
+            } else {
+                break;  // the batch runs past the window: reload from h
+            }
+            uint32_t mo = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const uint64_t j = base + lane * 8 + r;
+                if (j >= h && j < e) mo = max(mo, oo[r]);
+            }
+            mo = static_cast<uint32_t>(warp_max_u64(mo));
+            record(h, e, mo);
+            const uint64_t idx = e - 1 - base;
+            uint64_t v = 0;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) v = (idx & 7) == static_cast<uint64_t>(r) ? pre[r] : v;
+            hoff = __shfl_sync(FULL, v, static_cast<int>(idx >> 3));
+            h = e;
+        }
+        if (h == base) {  // one batch longer than the window: form it chunk by chunk
+            uint64_t end = h, need_total = 0;
+            uint32_t mo = 0;
+            while (end < N) {
+                const uint64_t j = end + lane;
+                const bool valid = j < N;
+                const uint32_t pj = valid ? pp[j] : 0u, oj = valid ? po[j] : 0u;
+                const uint64_t nd = valid ? serving_memory(m, static_cast<uint64_t>(pj) + oj, 1) : 0ull;
+                uint64_t in2 = nd;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t y = __shfl_up_sync(FULL, in2, o);
+                    if (lane >= static_cast<uint32_t>(o)) in2 += y;
+                }
+                in2 += need_total;
+                const bool ok = valid && (j == h || in2 <= budget);
+                const uint32_t c = __popc(__ballot_sync(FULL, ok));
+                mo = max(mo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
+                if (c) need_total = __shfl_sync(FULL, in2, c - 1);
+                end += c;
+                if (c < 32) break;
+            }
+            record(h, end, mo);
+            h = end;
+        }
+    }
+    if (lane == 0) {
+        if (rec) P.sat_seg[w] = steps;
+        else P.sat_exit[w] = h;
+    }
+}
+
+// Prefill and per-step decode durations of every record, one warp per
+// segment walking its records (the same folds, in the same order, as
+// run_batches); the segment's step durations start at sat_seg[w].
+__global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_constant__ ReplayParams P) {
+    __shared__ uint2 spo[kWarps][kStage];
+    __shared__ double spd[kWarps][kStage];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w >= P.npsegs) return;
+    const Seg sg = P.psegs[w];
+    const uint32_t d = sg.dev;
+    const uint32_t pi = P.dev_prof[d];
+    const colo_model& m = P.prof[pi].m;
+    const uint64_t lo = P.dev_off[d];
+    const uint32_t* __restrict__ pp = P.p + lo;
+    const uint32_t* __restrict__ po = P.o + lo;
+    const double gam = m.decode_coef_const, del = m.decode_coef_context;
+    uint2* sPO = spo[warp];
+    double* sPD = spd[warp];
+    uint64_t doff = P.sat_seg[w];
+    uint64_t head = P.sat_seg_start[w];
+    while (head < sg.end) {
+        const uint64_t end = P.sat_end[lo + head];
+        const uint64_t nb = end - head;
+        const bool staged = nb <= kStage;
+        if (staged)
+            for (uint64_t j = lane; j < nb; j += 32) {
+                const uint32_t pj = pp[head + j];
+                sPO[j] = make_uint2(pj, po[head + j]);
+                sPD[j] = static_cast<double>(pj);
+            }
+        __syncwarp();
+        auto member_pd = [&](uint64_t j) -> double { return staged ? sPD[j] : static_cast<double>(pp[head + j]); };
+        double dur = 0.0;  // engine.hpp:321-325 (cost_model.hpp:18-25, batch 1, unrecorded)
+#pragma unroll 4
+        for (uint64_t j = 0; j < nb; ++j) {
+            const double t = member_pd(j);
+            dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
+        }
+        const uint32_t maxo = P.sat_maxo[lo + head];
+        double* dk = P.sat_dk + doff;
+        for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {  // engine.hpp:358-365 per step
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            const uint32_t kb = k0 + lane;
+            double kd[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
+#pragma unroll 4
+            for (uint64_t j = 0; j < nb; ++j) {
+                const uint32_t oj = staged ? sPO[j].y : po[head + j];
+                const double pj = member_pd(j);
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (kb + 32 * r < oj) acc[r] += gam + del * (pj + kd[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                if (kb + 32 * r < maxo) dk[kb + 32 * r] = acc[r];
+        }
+        if (lane == 0) {
+            P.sat_pre[lo + head] = dur;
+            P.sat_doff[lo + head] = doff;
+        }
+        doff += maxo;
+        head = end;
+        __syncwarp();
+    }
 }
 
 __global__ void __launch_bounds__(kWarps * 32) k_validate(const __grid_constant__ ReplayParams P) {
@@ -565,6 +890,94 @@ __global__ void __launch_bounds__(kWarps * 32) k_batches(const __grid_constant__
     }
 }
 
+// Device memory of the saturated fast path for one replay call.
+struct SatBuffers {
+    void* rec = nullptr;  // per-query records
+    void* tmp = nullptr;  // scan scratch
+    double* dk = nullptr;
+    ~SatBuffers() {
+        if (dk) cudaFree(dk);
+        if (tmp) cudaFree(tmp);
+        if (rec) cudaFree(rec);
+    }
+};
+
+// Builds the all-queued records and their durations when they fit in memory
+// (COLO_SAT=0 disables the fast path); leaves P.sat_on = 0 otherwise.
+constexpr uint64_t kPSeg = 131072;  // queries per partition segment
+
+colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64_t>& off, SatBuffers& sb,
+                        cudaStream_t st) {
+    P.sat_on = 0;
+    const size_t ndev = P.ndev, n = off[ndev];
+    const char* env = std::getenv("COLO_SAT");
+    if ((env && env[0] == '0') || n >= (1ull << 32) || n == 0) return COLO_OK;
+    std::vector<Seg> ps;
+    for (size_t d = 0; d < ndev; ++d) {
+        const uint64_t N = off[d + 1] - off[d];
+        for (uint64_t s0 = 0; s0 < N; s0 += kPSeg) ps.push_back(Seg{static_cast<uint32_t>(d), 0, s0, std::min(N, s0 + kPSeg)});
+    }
+    const size_t ns = ps.size();
+    size_t freeb = 0, totb = 0;
+    COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
+    if (n * 24 + ns * 64 + (4ull << 30) > freeb) return COLO_OK;  // no room: the resolve pass replays every batch
+    COLO_CK(ctx, cudaMalloc(&sb.rec, n * 24 + ns * 64 + 512));
+    auto* bp = static_cast<uint8_t*>(sb.rec);
+    P.sat_doff = reinterpret_cast<uint64_t*>(bp);
+    P.sat_pre = reinterpret_cast<double*>(bp + n * 8);
+    P.sat_end = reinterpret_cast<uint32_t*>(bp + n * 16);
+    P.sat_maxo = reinterpret_cast<uint32_t*>(bp + n * 20);
+    P.sat_seg = reinterpret_cast<uint64_t*>(bp + n * 24 + 128);
+    const size_t s8 = (ns * 8 + 127) & ~size_t(127);
+    Seg* dps = reinterpret_cast<Seg*>(bp + n * 24 + 128 + s8);
+    P.sat_exit = reinterpret_cast<uint64_t*>(bp + n * 24 + 128 + s8 + ((ns * sizeof(Seg) + 127) & ~size_t(127)));
+    P.sat_seg_start = P.sat_exit + ((ns + 15) & ~size_t(15));
+    COLO_CK(ctx, cudaMemcpyAsync(dps, ps.data(), ns * sizeof(Seg), cudaMemcpyHostToDevice, st));
+    P.psegs = dps;
+    P.npsegs = static_cast<uint32_t>(ns);
+    const bool timing = std::getenv("COLO_REPLAY_TIMING") != nullptr;
+    cudaEvent_t ev[3];
+    if (timing) {
+        for (auto& e : ev) cudaEventCreate(&e);
+        cudaEventRecord(ev[0], st);
+    }
+    COLO_CK(ctx, cudaMemsetAsync(P.sat_end, 0, n * 4, st));
+    const uint32_t blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
+    P.sat_pass = 1;
+    k_sat_partition<<<blocks, kWarps * 32, 0, st>>>(P);
+    P.sat_pass = 2;
+    k_sat_partition<<<blocks, kWarps * 32, 0, st>>>(P);
+    // segment step counts -> exclusive bases (in place) and the pool size
+    size_t tb = 0;
+    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
+    COLO_CK(ctx, cudaMalloc(&sb.tmp, tb + 16));
+    uint64_t last_in = 0, last_base = 0;
+    COLO_CK(ctx, cudaMemcpyAsync(&last_in, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(sb.tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
+    COLO_CK(ctx, cudaMemcpyAsync(&last_base, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    COLO_CK(ctx, cudaStreamSynchronize(st));
+    const uint64_t np = last_base + last_in;
+    COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
+    if (np * 8 + (2ull << 30) > freeb) return COLO_OK;  // no room for the step durations
+    if (timing) cudaEventRecord(ev[1], st);
+    COLO_CK(ctx, cudaMalloc(reinterpret_cast<void**>(&sb.dk), np * 8 + 8));
+    P.sat_dk = sb.dk;
+    k_sat_durations<<<blocks, kWarps * 32, 0, st>>>(P);
+    COLO_CK(ctx, cudaGetLastError());
+    P.sat_on = 1;
+    if (timing) {
+        cudaEventRecord(ev[2], st);
+        cudaEventSynchronize(ev[2]);
+        float a, b;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        std::fprintf(stderr, "colo sat: %llu step durations; records %.3f ms, durations %.3f ms\n",
+                     static_cast<unsigned long long>(np), a, b);
+        for (auto& x : ev) cudaEventDestroy(x);
+    }
+    return COLO_OK;
+}
+
 colo_status grow_rscratch(colo_ctx* ctx, size_t bytes) {
     if (ctx->rscratch_bytes >= bytes) return COLO_OK;
     if (ctx->d_rscratch) cudaFree(ctx->d_rscratch);
@@ -706,8 +1119,15 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (timing)
             for (auto& e : ev) cudaEventCreate(&e);
         if (timing) cudaEventRecord(ev[0], ctx->stream);
+        SatBuffers sat;  // all-queued batch records for the resolve pass's fast path
+        const colo_status sst = sat_prepare(ctx, P, off, sat, ctx->stream);
+        if (sst != COLO_OK) return sst;
         k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[1], ctx->stream);
+        if (timing) {
+            P.dbg = reinterpret_cast<unsigned long long*>(ctx->d_counters);
+            cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream);
+        }
         k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[2], ctx->stream);
         k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
@@ -718,8 +1138,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             cudaEventElapsedTime(&a, ev[0], ev[1]);
             cudaEventElapsedTime(&b, ev[1], ev[2]);
             cudaEventElapsedTime(&c, ev[2], ev[3]);
-            std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms, replay %.3f ms\n",
-                         ns, static_cast<unsigned long long>(seg), a, b, c);
+            unsigned long long hits[2] = {0, 0};
+            cudaMemcpy(hits, ctx->d_counters, 16, cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms (%llu fast / "
+                                 "%llu formed batches), replay %.3f ms\n",
+                         ns, static_cast<unsigned long long>(seg), a, b, hits[0], hits[1], c);
             for (auto& e : ev) cudaEventDestroy(e);
         }
     }

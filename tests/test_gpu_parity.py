@@ -398,3 +398,36 @@ def test_mapset_save_load_roundtrip(ctx, tmp_path):  # maps.hpp:118-191, 284-332
             cs.load_mapset(ctx, other, G, po, ph)
         ms.offload.save(str(tmp_path / "o2.map"))
         assert open(str(tmp_path / "o2.map"), "rb").read() == open(po, "rb").read()
+
+
+def test_replay_saturated_fast_path_large(ctx, orc, monkeypatch):
+    """Saturated devices long enough to span several partition segments
+    (131072 queries each): the resolve pass's all-queued fast path
+    (COLO_SAT, default on) gives the same bits as forming every batch
+    (COLO_SAT=0) and as the oracle; outputs beyond 128 steps included."""
+    hv, hp = sharegpt_histogram()
+    traces = []
+    for d, q in enumerate([2.5, 1.2, 3.0]):
+        a, p, o = orc.generate_trace(q, 330000.0 / q, ("histogram", hv, hp), 900 + d)
+        if d == 1:
+            o = np.random.default_rng(5).integers(1, 300, len(o)).astype(np.uint32)
+        traces.append((a, p, o))
+    a = np.concatenate([t[0] for t in traces])
+    p = np.concatenate([t[1] for t in traces]).astype(np.uint32)
+    o = np.concatenate([t[2] for t in traces]).astype(np.uint32)
+    offs = np.concatenate([[0], np.cumsum([len(t[1]) for t in traces])]).astype(np.int64)
+    assert min(len(t[0]) for t in traces) > 2 * 131072
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("COLO_SAT", flag)
+        r = run_replay(ctx, a, p, o, 0.05, offs=offs)
+        outs[flag] = {k: r[k].cpu().numpy() for k in ("samples", "labels", "summary")}
+    for k in ("samples", "labels", "summary"):
+        assert outs["1"][k].tobytes() == outs["0"][k].tobytes(), k
+    d = 1  # the variable-output device against the oracle
+    ref = orc.replay_serving(default_model(), OG, traces[d][0], traces[d][1], traces[d][2], tau=0.05)
+    S = cs.summaries_to_numpy(outs["1"]["summary"])
+    lo, hi = int(offs[d]), int(offs[d + 1])
+    assert (outs["1"]["labels"][lo:hi] == ref["labels"]).all()
+    assert S[d]["end_time"] == ref["summary"]["end_time"]
+    assert int(S[d]["generated_tokens"]) == ref["summary"]["generated_tokens"]
