@@ -23,6 +23,10 @@ struct colo_ctx {
     uint64_t* d_counters = nullptr; // COLO_NCOUNTERS scratch
     void* d_rscratch = nullptr;     // replay segment state (lazily grown)
     size_t rscratch_bytes = 0;
+    void* d_sat = nullptr;          // serving replay: all-queued batch records (lazily grown)
+    size_t sat_bytes = 0;
+    void* d_satpool = nullptr;      // serving replay: their step durations (lazily grown)
+    size_t satpool_bytes = 0;
 };
 
 struct colo_mapset {

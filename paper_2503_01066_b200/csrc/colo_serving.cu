@@ -192,42 +192,58 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 uint64_t bend = se[head];
                 bool progressed = false;
                 if (bend != 0) {
+                    // batch i = [head, bend): its record, its durations (cur) and
+                    // its last arrival; batch i+1 = [bend, e1): its record (n1*),
+                    // with its last arrival and durations loaded during batch i's
+                    // chain together with batch i+2's record -- no load waits in
+                    // front of a chain
                     uint32_t K = smo[head];
-                    uint64_t dof = sdo[head];
                     double pre = spre[head];
                     double alast = arr[bend - 1];
                     double cur[4];
+                    {
+                        const uint64_t dof = sdo[head];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const uint32_t i = 32 * r + lane;
-                        cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
+                        for (int r = 0; r < 4; ++r) {
+                            const uint32_t i = 32 * r + lane;
+                            cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
+                        }
+                        if (K > 128) cur[0] = __longlong_as_double(static_cast<long long>(dof));
                     }
+                    const bool in1 = bend < stop && bend < N;
+                    uint64_t e1 = in1 ? se[bend] : 0;
+                    uint32_t K1 = in1 ? smo[bend] : 0;
+                    uint64_t dof1 = in1 ? sdo[bend] : 0;
+                    double pre1 = in1 ? spre[bend] : 0.0;
                     for (;;) {
                         if (!(alast <= T)) break;  // a member has not arrived: form it the slow way
-                        const bool more = bend < stop && bend < N;
-                        const uint64_t nend = more ? se[bend] : 0;
-                        const bool hn = nend != 0;
-                        uint64_t ndof = 0;
-                        uint32_t nK = 0;
-                        double npre = 0.0, nalast = 0.0, nxt[4] = {0.0, 0.0, 0.0, 0.0};
-                        {  // records and durations stream forward: keep ~4 batches ahead in L2
-                            const char* q;
-                            if (lane < 16) q = reinterpret_cast<const char*>(pool + dof + 512) + lane * 128;
-                            else if (lane < 20) q = reinterpret_cast<const char*>(se + bend + 256) + (lane - 16) * 128;
-                            else if (lane < 24) q = reinterpret_cast<const char*>(smo + bend + 256) + (lane - 20) * 128;
-                            else if (lane < 28) q = reinterpret_cast<const char*>(sdo + bend + 256) + (lane - 24) * 256;
-                            else q = reinterpret_cast<const char*>(spre + bend + 256) + (lane - 28) * 256;
-                            if (bend + 1024 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-                        }
-                        if (hn) {  // the next record and its durations, in flight during this chain
-                            nK = smo[bend];
-                            ndof = sdo[bend];
-                            npre = spre[bend];
-                            nalast = arr[nend - 1];
+                        const bool hn = e1 != 0;
+                        double alast1 = 0.0, nxt[4] = {0.0, 0.0, 0.0, 0.0};
+                        uint64_t e2 = 0, dof2 = 0;
+                        uint32_t K2 = 0;
+                        double pre2 = 0.0;
+                        if (hn) {
+                            alast1 = arr[e1 - 1];
 #pragma unroll
                             for (int r = 0; r < 4; ++r) {
                                 const uint32_t i = 32 * r + lane;
-                                if (nK <= 128 && i < nK) nxt[r] = pool[ndof + i];
+                                if (K1 <= 128 && i < K1) nxt[r] = pool[dof1 + i];
+                            }
+                            if (K1 > 128) nxt[0] = __longlong_as_double(static_cast<long long>(dof1));
+                            if (e1 < stop && e1 < N) {
+                                e2 = se[e1];
+                                K2 = smo[e1];
+                                dof2 = sdo[e1];
+                                pre2 = spre[e1];
+                            }
+                            {  // records and durations stream forward: keep a few batches ahead in L2
+                                const char* q;
+                                if (lane < 16) q = reinterpret_cast<const char*>(pool + dof1 + 512) + lane * 128;
+                                else if (lane < 20) q = reinterpret_cast<const char*>(se + e1 + 256) + (lane - 16) * 128;
+                                else if (lane < 24) q = reinterpret_cast<const char*>(smo + e1 + 256) + (lane - 20) * 128;
+                                else if (lane < 28) q = reinterpret_cast<const char*>(sdo + e1 + 256) + (lane - 24) * 256;
+                                else q = reinterpret_cast<const char*>(spre + e1 + 256) + (lane - 28) * 256;
+                                if (e1 + 1024 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
                             }
                         }
                         double now = (T + 0.0) + pre;
@@ -245,6 +261,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                             now = sDK[0];
                             __syncwarp();
                         } else {
+                            const uint64_t dof = static_cast<uint64_t>(__double_as_longlong(cur[0]));
                             for (uint32_t k0 = 0; k0 < K; k0 += 128) {
                                 const uint32_t c = min(128u, K - k0);
 #pragma unroll
@@ -268,13 +285,16 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         progressed = true;
                         if (P.dbg && lane == 0) atomicAdd(P.dbg, 1ull);
                         if (!hn) break;
-                        bend = nend;
-                        K = nK;
-                        dof = ndof;
-                        pre = npre;
-                        alast = nalast;
+                        bend = e1;
+                        K = K1;
+                        pre = pre1;
+                        alast = alast1;
 #pragma unroll
                         for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
+                        e1 = e2;
+                        K1 = K2;
+                        dof1 = dof2;
+                        pre1 = pre2;
                     }
                 }
                 if (progressed) continue;
@@ -890,20 +910,34 @@ __global__ void __launch_bounds__(kWarps * 32) k_batches(const __grid_constant__
     }
 }
 
-// Device memory of the saturated fast path for one replay call.
-struct SatBuffers {
-    void* rec = nullptr;  // per-query records
-    void* tmp = nullptr;  // scan scratch
-    double* dk = nullptr;
+// Grow-only context buffers (allocating tens of GB per call costs more than
+// the passes themselves).
+colo_status grow_buf(colo_ctx* ctx, void** buf, size_t* have, size_t bytes) {
+    if (*have >= bytes) return COLO_OK;
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *have = 0;
+    COLO_CK(ctx, cudaMalloc(buf, bytes));
+    *have = bytes;
+    return COLO_OK;
+}
+
+// Segments whose speculative run never went idle after its first batch: the
+// queue stayed non-empty, which is where the all-queued fast path pays.
+__global__ void k_count_saturated(const SpecOut* __restrict__ spec, uint32_t nsegs, unsigned long long* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool sat = i < nsegs && spec[i].nregen <= 1;
+    const uint32_t b = __ballot_sync(0xffffffffu, sat);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, static_cast<unsigned long long>(__popc(b)));
+}
+
+struct SatBuffers {  // per-call scratch of sat_prepare
+    void* tmp = nullptr;
     ~SatBuffers() {
-        if (dk) cudaFree(dk);
         if (tmp) cudaFree(tmp);
-        if (rec) cudaFree(rec);
     }
 };
 
-// Builds the all-queued records and their durations when they fit in memory
-// (COLO_SAT=0 disables the fast path); leaves P.sat_on = 0 otherwise.
 constexpr uint64_t kPSeg = 131072;  // queries per partition segment
 
 colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64_t>& off, SatBuffers& sb,
@@ -918,11 +952,27 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         for (uint64_t s0 = 0; s0 < N; s0 += kPSeg) ps.push_back(Seg{static_cast<uint32_t>(d), 0, s0, std::min(N, s0 + kPSeg)});
     }
     const size_t ns = ps.size();
-    size_t freeb = 0, totb = 0;
-    COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
-    if (n * 24 + ns * 64 + (4ull << 30) > freeb) return COLO_OK;  // no room: the resolve pass replays every batch
-    COLO_CK(ctx, cudaMalloc(&sb.rec, n * 24 + ns * 64 + 512));
-    auto* bp = static_cast<uint8_t*>(sb.rec);
+    // only when a noticeable share of segments stayed saturated (k_speculate ran first)
+    {
+        unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx->d_counters);
+        COLO_CK(ctx, cudaMemsetAsync(cnt, 0, 8, st));
+        k_count_saturated<<<(P.nsegs + 255) / 256, 256, 0, st>>>(P.spec, P.nsegs, cnt);
+        unsigned long long nsat = 0;
+        COLO_CK(ctx, cudaMemcpyAsync(&nsat, cnt, 8, cudaMemcpyDeviceToHost, st));
+        COLO_CK(ctx, cudaStreamSynchronize(st));
+        if (nsat * 50 < P.nsegs || nsat < 2) return COLO_OK;
+    }
+    const size_t need_rec = n * 24 + ns * 64 + 512;
+    if (ctx->sat_bytes < need_rec) {
+        size_t freeb = 0, totb = 0;
+        COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
+        if (need_rec + (4ull << 30) > freeb + ctx->sat_bytes) return COLO_OK;  // no room: replay every batch
+    }
+    {
+        const colo_status g = grow_buf(ctx, &ctx->d_sat, &ctx->sat_bytes, need_rec);
+        if (g != COLO_OK) return g;
+    }
+    auto* bp = static_cast<uint8_t*>(ctx->d_sat);
     P.sat_doff = reinterpret_cast<uint64_t*>(bp);
     P.sat_pre = reinterpret_cast<double*>(bp + n * 8);
     P.sat_end = reinterpret_cast<uint32_t*>(bp + n * 16);
@@ -957,11 +1007,17 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
     COLO_CK(ctx, cudaMemcpyAsync(&last_base, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
     COLO_CK(ctx, cudaStreamSynchronize(st));
     const uint64_t np = last_base + last_in;
-    COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
-    if (np * 8 + (2ull << 30) > freeb) return COLO_OK;  // no room for the step durations
+    if (ctx->satpool_bytes < np * 8 + 8) {
+        size_t freeb = 0, totb = 0;
+        COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
+        if (np * 8 + (2ull << 30) > freeb + ctx->satpool_bytes) return COLO_OK;  // no room for the step durations
+    }
     if (timing) cudaEventRecord(ev[1], st);
-    COLO_CK(ctx, cudaMalloc(reinterpret_cast<void**>(&sb.dk), np * 8 + 8));
-    P.sat_dk = sb.dk;
+    {
+        const colo_status g = grow_buf(ctx, &ctx->d_satpool, &ctx->satpool_bytes, np * 8 + 8);
+        if (g != COLO_OK) return g;
+    }
+    P.sat_dk = static_cast<double*>(ctx->d_satpool);
     k_sat_durations<<<blocks, kWarps * 32, 0, st>>>(P);
     COLO_CK(ctx, cudaGetLastError());
     P.sat_on = 1;
@@ -1119,10 +1175,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (timing)
             for (auto& e : ev) cudaEventCreate(&e);
         if (timing) cudaEventRecord(ev[0], ctx->stream);
+        k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         SatBuffers sat;  // all-queued batch records for the resolve pass's fast path
         const colo_status sst = sat_prepare(ctx, P, off, sat, ctx->stream);
         if (sst != COLO_OK) return sst;
-        k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[1], ctx->stream);
         if (timing) {
             P.dbg = reinterpret_cast<unsigned long long*>(ctx->d_counters);
