@@ -201,14 +201,11 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                     double pre = spre[head];
                     double alast = arr[bend - 1];
                     double cur[4];
-                    {
-                        const uint64_t dof = sdo[head];
+                    uint64_t dof = sdo[head];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r) {
-                            const uint32_t i = 32 * r + lane;
-                            cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
-                        }
-                        if (K > 128) cur[0] = __longlong_as_double(static_cast<long long>(dof));
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t i = 32 * r + lane;
+                        cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
                     }
                     const bool in1 = bend < stop && bend < N;
                     uint64_t e1 = in1 ? se[bend] : 0;
@@ -229,7 +226,6 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                 const uint32_t i = 32 * r + lane;
                                 if (K1 <= 128 && i < K1) nxt[r] = pool[dof1 + i];
                             }
-                            if (K1 > 128) nxt[0] = __longlong_as_double(static_cast<long long>(dof1));
                             if (e1 < stop && e1 < N) {
                                 e2 = se[e1];
                                 K2 = smo[e1];
@@ -261,7 +257,6 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                             now = sDK[0];
                             __syncwarp();
                         } else {
-                            const uint64_t dof = static_cast<uint64_t>(__double_as_longlong(cur[0]));
                             for (uint32_t k0 = 0; k0 < K; k0 += 128) {
                                 const uint32_t c = min(128u, K - k0);
 #pragma unroll
@@ -287,6 +282,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         if (!hn) break;
                         bend = e1;
                         K = K1;
+                        dof = dof1;
                         pre = pre1;
                         alast = alast1;
 #pragma unroll
