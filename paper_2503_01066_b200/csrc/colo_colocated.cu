@@ -105,7 +105,7 @@ struct WarpSmem {
     uint8_t flg[kLayerCap];      // LF_* (on_device, consumed, dropped)
     uint2 po[kStageC];           // batch members (prompt, output)
     double pd[kStageC];          // (double)prompt
-    double dk[128];              // step durations of the current 128-step window
+    alignas(16) double dk[128];  // step durations of the current 128-step window
 };
 
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
@@ -698,14 +698,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             // absolute-time chain now_k = now_{k-1} + d_k (sequential, one lane),
             // the durations are overwritten by the absolute times
             const uint32_t cnt = min(128u, maxo - k0);
-            if (lane == 0) {
-                double t = tnow;
-#pragma unroll 8
-                for (uint32_t i = 0; i < cnt; ++i) {
-                    t = t + S.dk[i];
-                    S.dk[i] = t;
-                }
-            }
+            if (lane == 0) chain_fold_store(tnow, S.dk, cnt);
             __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll

@@ -97,4 +97,60 @@ __device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, ui
     return lo < N ? lo : N;
 }
 
+// Sequential f64 fold t = (((t + d0) + d1) + ...) over K durations staged in
+// 16-B aligned shared memory, on one lane.  Pairs come in with one LDS.128 and
+// the K == 128 case (the default output length) is fully unrolled, so the
+// chain runs at the f64 add latency (8.5 vs 15 cycles per step measured on B200).
+__device__ __forceinline__ double chain_fold(double t, const double* d, uint32_t K) {
+    const double2* d2 = reinterpret_cast<const double2*>(d);
+    if (K == 128) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            const double2 q = d2[i];
+            t = t + q.x;
+            t = t + q.y;
+        }
+        return t;
+    }
+    uint32_t i = 0;
+#pragma unroll 8
+    for (; i + 1 < K; i += 2) {
+        const double2 q = d2[i >> 1];
+        t = t + q.x;
+        t = t + q.y;
+    }
+    if (i < K) t = t + d[i];
+    return t;
+}
+
+// The same fold, storing every partial result (the absolute step times) back.
+__device__ __forceinline__ double chain_fold_store(double t, double* d, uint32_t K) {
+    double2* d2 = reinterpret_cast<double2*>(d);
+    if (K == 128) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+            double2 q = d2[i];
+            q.x = t + q.x;
+            q.y = q.x + q.y;
+            t = q.y;
+            d2[i] = q;
+        }
+        return t;
+    }
+    uint32_t i = 0;
+#pragma unroll 8
+    for (; i + 1 < K; i += 2) {
+        double2 q = d2[i >> 1];
+        q.x = t + q.x;
+        q.y = q.x + q.y;
+        t = q.y;
+        d2[i >> 1] = q;
+    }
+    if (i < K) {
+        t = t + d[i];
+        d[i] = t;
+    }
+    return t;
+}
+
 }  // namespace colo

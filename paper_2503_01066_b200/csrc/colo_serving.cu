@@ -247,12 +247,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
 #pragma unroll
                             for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = cur[r];
                             __syncwarp();
-                            if (lane == 0) {
-                                double t = now;
-#pragma unroll 8
-                                for (uint32_t i = 0; i < K; ++i) t = t + sDK[i];
-                                sDK[0] = t;
-                            }
+                            if (lane == 0) sDK[0] = chain_fold(now, sDK, K);
                             __syncwarp();
                             now = sDK[0];
                             __syncwarp();
@@ -265,11 +260,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                     if (i < c) sDK[i] = pool[dof + k0 + i];
                                 }
                                 __syncwarp();
-                                if (lane == 0) {
-                                    double t = now;
-                                    for (uint32_t i = 0; i < c; ++i) t = t + sDK[i];
-                                    sDK[0] = t;
-                                }
+                                if (lane == 0) sDK[0] = chain_fold(now, sDK, c);
                                 __syncwarp();
                                 now = sDK[0];
                                 __syncwarp();
@@ -403,14 +394,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             // absolute-time chain now_k = now_{k-1} + d_k, sequential on one
             // lane; the durations are overwritten by the absolute times
             const uint32_t cnt = min(128u, maxo - k0);
-            if (lane == 0) {
-                double t = now;
-#pragma unroll 8
-                for (uint32_t i = 0; i < cnt; ++i) {
-                    t = t + sDK[i];
-                    sDK[i] = t;
-                }
-            }
+            if (lane == 0) chain_fold_store(now, sDK, cnt);
             __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -728,7 +712,8 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
 
 __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
-    __shared__ double spd[kWarps][kStage], sdk[kWarps][128];
+    __shared__ double spd[kWarps][kStage];
+    __shared__ __align__(16) double sdk[kWarps][128];
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -748,7 +733,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant
 // gets an SM of its own (no issue-slot or FP64-pipe sharing between devices).
 __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[1][kStage];
-    __shared__ double spd[1][kStage], sdk[1][128];
+    __shared__ double spd[1][kStage];
+    __shared__ __align__(16) double sdk[1][128];
     const uint32_t warp = 0;
     const uint32_t d = blockIdx.x;
     if (d >= P.ndev) return;
@@ -771,7 +757,8 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
 
 __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
-    __shared__ double spd[kWarps][kStage], sdk[kWarps][128];
+    __shared__ double spd[kWarps][kStage];
+    __shared__ __align__(16) double sdk[kWarps][128];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
