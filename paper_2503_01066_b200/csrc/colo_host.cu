@@ -186,6 +186,7 @@ void colo_ctx_destroy(colo_ctx* ctx) {
     if (ctx->d_rscratch) cudaFree(ctx->d_rscratch);
     if (ctx->d_sat) cudaFree(ctx->d_sat);
     if (ctx->d_satpool) cudaFree(ctx->d_satpool);
+    if (ctx->d_dtab) cudaFree(ctx->d_dtab);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     delete ctx;

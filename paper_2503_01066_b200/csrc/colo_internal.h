@@ -27,6 +27,8 @@ struct colo_ctx {
     size_t sat_bytes = 0;
     void* d_satpool = nullptr;      // serving replay: their step durations (lazily grown)
     size_t satpool_bytes = 0;
+    void* d_dtab = nullptr;         // serving replay: decode-latency tables (lazily grown)
+    size_t dtab_bytes = 0;
 };
 
 struct colo_mapset {

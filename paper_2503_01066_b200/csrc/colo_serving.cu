@@ -123,6 +123,13 @@ struct ReplayParams {
     double* sat_dk;
     uint32_t sat_on;
     unsigned long long* dbg;  // COLO_REPLAY_TIMING: [0] fast-path batches, [1] other batches of the resolve pass
+    // decode-step latency table per profile: dtab[pi][x] = gamma + delta * x for
+    // every context x < dtab_n (cost_model.hpp:28-35 with batch 1, the same f64
+    // ops); k_sat_durations' folds load a term instead of computing it (in the
+    // replay passes computing it is as fast: B200's f64 pipe keeps up with L1)
+    const double* dtab[kMaxSets];
+    uint64_t dtab_n;        // 0 = no table
+    unsigned long long* maxctx;  // k_validate: max p + o over the trace
 };
 
 enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
@@ -476,6 +483,14 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
     if (MODE == RUN_SPEC && lane == 0) sp->nregen = ridx;
 }
 
+// dtab[pi][x] = gamma + delta * (double)x: decode_step_latency(x, 1, false)
+// (cost_model.hpp:28-35; 1.0 * v == v), the same f64 ops as the folds.
+__global__ void k_fill_dtab(double* tab, uint64_t n, double gam, double del) {
+    for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < n;
+         x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        tab[x] = gam + del * static_cast<double>(x);
+}
+
 // All-queued ("saturated") batch records.  The batch start_serving_batch
 // forms at head q when every query up to its end has arrived depends on q
 // alone (FIFO, at least one, sum(need) <= budget: engine.hpp:292-306 without
@@ -626,12 +641,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
         const uint64_t end = P.sat_end[lo + head];
         const uint64_t nb = end - head;
         const bool staged = nb <= kStage;
+        uint64_t mi = 0;  // max p + o of the members (table coverage)
         if (staged)
             for (uint64_t j = lane; j < nb; j += 32) {
-                const uint32_t pj = pp[head + j];
-                sPO[j] = make_uint2(pj, po[head + j]);
+                const uint32_t pj = pp[head + j], oj = po[head + j];
+                sPO[j] = make_uint2(pj, oj);
                 sPD[j] = static_cast<double>(pj);
+                mi = max(mi, static_cast<uint64_t>(pj) + oj);
             }
+        const bool tab_ok = warp_max_u64(mi) < P.dtab_n;
         __syncwarp();
         auto member_pd = [&](uint64_t j) -> double { return staged ? sPD[j] : static_cast<double>(pp[head + j]); };
         double dur = 0.0;  // engine.hpp:321-325 (cost_model.hpp:18-25, batch 1, unrecorded)
@@ -648,13 +666,24 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
             double kd[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
+            if (staged && tab_ok) {
+                const double* __restrict__ dt = P.dtab[pi] + kb;
 #pragma unroll 4
-            for (uint64_t j = 0; j < nb; ++j) {
-                const uint32_t oj = staged ? sPO[j].y : po[head + j];
-                const double pj = member_pd(j);
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint2 po_j = sPO[j];
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
-                    if (kb + 32 * r < oj) acc[r] += gam + del * (pj + kd[r]);
+                    for (int r = 0; r < 4; ++r)
+                        if (kb + 32 * r < po_j.y) acc[r] += dt[po_j.x + 32 * r];
+                }
+            } else {
+#pragma unroll 4
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint32_t oj = staged ? sPO[j].y : po[head + j];
+                    const double pj = member_pd(j);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if (kb + 32 * r < oj) acc[r] += gam + del * (pj + kd[r]);
+                }
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r)
@@ -678,13 +707,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_validate(const __grid_constant_
     const colo_model& m = P.prof[pi].m;
     const uint64_t lo = P.dev_off[sg.dev];
     bool bad = false;
+    unsigned long long mx = 0;
     for (uint64_t j = sg.start + lane; j < sg.end; j += 32) {
         const uint32_t pj = P.p[lo + j], oj = P.o[lo + j];
         if (pj == 0 || oj == 0) bad = true;  // workload.hpp:176-181
         else if (serving_memory(m, static_cast<uint64_t>(pj) + oj, 1) > P.prof[pi].budget) bad = true;  // engine.hpp:70-74
         if (j > 0 && P.arr[lo + j] < P.arr[lo + j - 1]) bad = true;  // sorted by arrival (workload.hpp:165-169)
+        mx = max(mx, static_cast<unsigned long long>(pj) + oj);
     }
     if (__any_sync(FULL, bad) && lane == 0) atomicOr(P.err, 1);
+    mx = warp_max_u64(mx);
+    if (lane == 0 && P.maxctx && mx) atomicMax(P.maxctx, mx);
 }
 
 // samples: device-local output-token prefix at each segment start
@@ -1139,6 +1172,8 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     for (int f = 0; f < 3; ++f) P.prefix[f] = opts->filter_prefix[f];
     P.err = ctx->d_flag;
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
+    P.maxctx = reinterpret_cast<unsigned long long*>(ctx->d_counters) + 2;
+    COLO_CK(ctx, cudaMemsetAsync(P.maxctx, 0, 8, ctx->stream));
     const uint32_t seg_blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
     const uint32_t dev_blocks = static_cast<uint32_t>((ndev + kWarps - 1) / kWarps);
     if (ns) {
@@ -1149,6 +1184,30 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (flag)
             return set_err(ctx, COLO_EVALIDATION,
                            "trace rejected: unsorted arrivals, zero tokens, or a query that cannot fit the device alone");
+        {  // decode-latency tables up to the trace's largest context
+            unsigned long long mctx = 0;
+            COLO_CK(ctx, cudaMemcpy(&mctx, P.maxctx, 8, cudaMemcpyDeviceToHost));
+            P.dtab_n = 0;
+            if (mctx > 0 && mctx < (1ull << 20)) {
+                const uint64_t tn = mctx + 1;
+                const size_t tb = ((tn * 8 + 255) & ~size_t(255)) * nprofiles;
+                if (ctx->dtab_bytes < tb) {
+                    if (ctx->d_dtab) cudaFree(ctx->d_dtab);
+                    ctx->d_dtab = nullptr;
+                    ctx->dtab_bytes = 0;
+                    COLO_CK(ctx, cudaMalloc(&ctx->d_dtab, tb));
+                    ctx->dtab_bytes = tb;
+                }
+                for (size_t i = 0; i < nprofiles; ++i) {
+                    double* t = reinterpret_cast<double*>(static_cast<uint8_t*>(ctx->d_dtab) +
+                                                          i * ((tn * 8 + 255) & ~size_t(255)));
+                    k_fill_dtab<<<256, 256, 0, ctx->stream>>>(t, tn, models[i].decode_coef_const,
+                                                              models[i].decode_coef_context);
+                    P.dtab[i] = t;
+                }
+                P.dtab_n = tn;
+            }
+        }
         if (P.samples) {
             k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
