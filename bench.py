@@ -587,6 +587,92 @@ def run_colo(args, world, rank, local):
     ctx.close()
 
 
+C4_FLEET, C4_PER_DEVICE = 1024, 7_812_500
+
+
+def run_c4(args, world, rank, local):
+    """C4 (BASELINE.json configs[3]): the 1024-device fleet of 8B queries,
+    device d on rank d % world (C2's profiles/modes/rates per device).  Each
+    rank runs, per step, the trace-fused decisions over all its queries, the
+    serving replay with slow labels, and the exact TPT statistics (three
+    radix-select replay passes); the counters, histograms and exact sums are
+    the only data that cross ranks (NCCL all-reduce).  --c4-devices caps the
+    devices a rank holds (one B200 holds the 8-GPU share, 128 devices = 1B
+    queries; the 1-2 GPU shares do not fit next to the replay's records)."""
+    import torch
+
+    from paper_2503_01066_b200 import colosim as cs
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        init_dist(dist, torch, local)
+    ctx = cs.Context(local)
+    mine = [d for d in range(C4_FLEET) if d % world == rank][: args.c4_devices]
+    D, per = len(mine), args.c4_per_device
+    g = cs.GpuProfile()
+    models = (cs.ModelProfile(), cs.ModelProfile.phi14b_like())
+    sets = [cs.MapSet.build(ctx, m, g, mode=md) for m in models for md in (cs.TrainingMode.CPA, cs.TrainingMode.CPT)]
+    profiles = [(m, g) for m in models]
+    arrival, prompt, output, offs = cs.synth_trace(ctx, [per] * D, [QPS[d % 4] for d in mine], 4040 + 7919 * rank)
+    dset = torch.tensor([dev_set_of(d) for d in mine], dtype=torch.int16, device="cuda")
+    dprof = torch.tensor([(d % 2) for d in mine], dtype=torch.int16, device="cuda")
+    n = D * per
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    counters = torch.zeros(8, dtype=torch.int64, device="cuda")
+    group = None
+
+    def step():
+        counters.zero_()
+        cs.features_decide(ctx, sets, prompt, output, offs, dset, out=out, counters=counters)
+        st = cs.serving_stats(ctx, profiles, arrival, prompt, output, offs, dprof, tau=args.c4_tau, group=group)
+        if dist:
+            dist.all_reduce(counters)
+        return st
+
+    for _ in range(max(args.warmup, 1)):
+        st = step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            st = step()
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item()) / 1e3
+    total = world * n if dist else n
+    if rank == 0:
+        line = {"metric": "C4 fleet: admission decisions + serving replay labels + exact TPT stats, queries/s",
+                "value": total * args.steps / sec, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic",
+                "config": {"workload": f"C4: 1024-device fleet x {per} queries, device d on rank d % {world}; "
+                                       f"{D} devices ({n} queries) per rank this run",
+                           "per_step": "features_decide (all queries) + serving replay with slow labels + "
+                                       "3 radix-select stats passes, NCCL all-reduce of counters/histograms/exact sums",
+                           "tau_s": args.c4_tau, "parallelism": f"dp{world} (devices sharded by rank)"},
+                "stats": {k: st[k] for k in ("generated_tokens", "slow_tokens", "slow_queries", "batches", "p50", "p90",
+                                            "p99", "mean")},
+                "counters": dict(zip(cs.COUNTER_NAMES, [int(x) for x in counters.cpu().tolist()])),
+                "roofline": {"bound": "latency (sequential f64 time folds per device)", "achieved": None, "peak": None,
+                             "unit": "GB/s", "frac": None, "traffic": None},
+                "gpu_launches": None, "clocks": clk.report()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
 def run_c3(args, world, rank, local):
     """C3 (BASELINE.json configs[2]): 128 bursty devices x 7,812,500 queries =
     1B queries per GPU, serving replay + slow labels + the first exact-stats
@@ -674,10 +760,14 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c5", "colo"], default="c2",
+    ap.add_argument("--workload", choices=["c1", "c2", "c3", "c4", "c5", "colo"], default="c2",
                     help="c2 (default, the headline): trace-fused decisions; c1: single-trace replay vs the "
                          "reference Simulation; c3: 1B-query bursty replay + labels; c5: map vs exact sweep; "
+                         "c4: 1024-device fleet sharded by rank (decisions + replay + exact stats, NCCL reduce); "
                          "colo: colocated replay (C1 trace + device fleet)")
+    ap.add_argument("--c4-devices", type=int, default=128, help="devices per rank (cap)")
+    ap.add_argument("--c4-per-device", type=int, default=C4_PER_DEVICE)
+    ap.add_argument("--c4-tau", type=float, default=0.05)
     ap.add_argument("--colo-devices", type=int, default=1184)  # 8 resident warps x 148 SMs
     ap.add_argument("--colo-per-device", type=int, default=50_000)
     ap.add_argument("--colo-skip-c1", action="store_true")
@@ -697,6 +787,8 @@ def main():
         run_c5(args, world, rank, local)
     elif args.workload == "colo":
         run_colo(args, world, rank, local)
+    elif args.workload == "c4":
+        run_c4(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -284,6 +284,12 @@ typedef struct colo_replay_opts {
     uint32_t filter_shift;            /* 63 with prefix 0 selects every sample */
     uint32_t segment_len;             /* queries per replay segment (0 = automatic), see below */
     uint64_t filter_prefix[3];
+    uint32_t reuse_entries;           /* 1: the previous call on this context replayed the same trace
+                                         (same buffers, sizes, profiles, segment_len): skip validation,
+                                         speculation and resolution and reuse its segment entry states
+                                         (histogram passes 2-3 of the exact-stats protocol).  Falls back
+                                         to a full replay when the context cannot prove that. */
+    uint32_t pad;
 } colo_replay_opts;
 
 /* Serving-only replay of every device's trace.  Each device is cut into

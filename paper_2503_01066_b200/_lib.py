@@ -90,6 +90,8 @@ class ReplayOpts(C.Structure):
         ("filter_shift", C.c_uint32),
         ("segment_len", C.c_uint32),
         ("filter_prefix", C.c_uint64 * 3),
+        ("reuse_entries", C.c_uint32),
+        ("pad", C.c_uint32),
     ]
 
 

@@ -600,7 +600,8 @@ def _profiles_arrays(profiles: Sequence[Tuple[ModelProfile, GpuProfile]]):
 def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfile]], arrival, prompt, output,
                    dev_offsets, dev_profile, tau: float = math.inf, sets: Optional[Sequence[MapSet]] = None,
                    samples: bool = False, labels: bool = True, batches: bool = False, summary: bool = True,
-                   hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), segment_len: int = 0):
+                   hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), segment_len: int = 0,
+                   reuse_entries: bool = False):
     """Serving-only replay of every device (engine.hpp:140-387, SimMode::ServingOnly).
     Returns a dict of device tensors: samples (f64, reference order),
     labels (u8 per query), batches (raw bytes, BATCH_DTYPE), summary (DeviceSummary bytes)."""
@@ -617,6 +618,7 @@ def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfi
     opts = _lib.ReplayOpts()
     opts.tau = tau
     opts.segment_len = segment_len
+    opts.reuse_entries = 1 if reuse_entries else 0
     keep = []
     if sets is not None:
         arr = _sets_array(sets)
@@ -690,7 +692,7 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
         first = filter_shift == 63
         r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
                            summary=first, hist=h, hist_shift=hist_shift, filter_shift=filter_shift,
-                           filter_prefix=tuple(prefixes))
+                           filter_prefix=tuple(prefixes), reuse_entries=not first)
         if not first:
             return h, None
         S = summaries_to_numpy(r["summary"])

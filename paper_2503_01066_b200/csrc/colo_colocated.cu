@@ -770,17 +770,14 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 if (sb && first_slow == 0xffffffffu) first_slow = kr0 + __ffs(sb) - 1;
                 a_gen += alv;
                 if (slow) a_slow += alv;
+                if (want_hist) {  // warp-aggregated: lanes with the same bin add once
+                    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+                    for (uint32_t f = 0; f < P.nfilters; ++f)
+                        hist_add(P.hist, f * COLO_HIST_BINS + static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
+                                 alv, lv && (bits >> P.filter_shift) == P.prefix[f]);
+                }
                 if (lv) {
                     acc_fixed(a_acc, a_flags, s, alv);
-                    if (want_hist) {
-                        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
-                        for (uint32_t f = 0; f < P.nfilters; ++f)
-                            if ((bits >> P.filter_shift) == P.prefix[f])
-                                atomicAdd(reinterpret_cast<unsigned long long*>(
-                                              &P.hist[static_cast<uint64_t>(f) * COLO_HIST_BINS +
-                                                      ((bits >> P.hist_shift) & (COLO_HIST_BINS - 1))]),
-                                          static_cast<unsigned long long>(alv));
-                    }
                 }
                 if (P.samples) {  // step k's samples: alive_k consecutive slots, steps in order
                     uint32_t ex = alv;
@@ -1111,6 +1108,7 @@ __global__ void __launch_bounds__(128) k_co_validate(const __grid_constant__ CoP
 size_t align256c(size_t x) { return (x + 255) & ~size_t(255); }
 
 colo_status grow_scratch(colo_ctx* ctx, size_t bytes) {
+    ctx->rs_valid = false;  // the serving replay's entry states share this buffer
     if (ctx->rscratch_bytes >= bytes) return COLO_OK;
     if (ctx->d_rscratch) cudaFree(ctx->d_rscratch);
     ctx->d_rscratch = nullptr;

@@ -29,6 +29,11 @@ struct colo_ctx {
     size_t satpool_bytes = 0;
     void* d_dtab = nullptr;         // serving replay: decode-latency tables (lazily grown)
     size_t dtab_bytes = 0;
+    // serving replay: identity of the last full replay whose segment entry
+    // states are still in d_rscratch (reuse_entries); any other d_rscratch
+    // user clears rs_valid
+    uint64_t rs_sig[10] = {};
+    bool rs_valid = false;
 };
 
 struct colo_mapset {

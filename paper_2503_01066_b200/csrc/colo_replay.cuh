@@ -97,6 +97,18 @@ __device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, ui
     return lo < N ? lo : N;
 }
 
+// hist[key] += cnt for every lane with act; lanes of the warp that share a key
+// add once (match + reduce), so consecutive decode steps of a batch, whose
+// TPT samples usually fall in one bin, cost one atomic.  Call from all lanes.
+__device__ __forceinline__ void hist_add(uint64_t* hist, uint32_t key, uint32_t cnt, bool act) {
+    const unsigned am = __ballot_sync(kFullMask, act);
+    if (!act) return;
+    const unsigned peers = __match_any_sync(am, key);
+    const unsigned total = __reduce_add_sync(peers, cnt);
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
+        atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(total));
+}
+
 // Sequential f64 fold t = (((t + d0) + d1) + ...) over K durations staged in
 // 16-B aligned shared memory, on one lane.  Pairs come in with one LDS.128 and
 // the K == 128 case (the default output length) is fully unrolled, so the

@@ -425,17 +425,14 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 if (sb && first_slow == 0xffffffffu) first_slow = kr0 + __ffs(sb) - 1;
                 A.gen += alv;
                 if (slow) A.slow_tok += alv;
+                if (want_hist) {  // warp-aggregated: lanes with the same bin add once
+                    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+                    for (uint32_t f = 0; f < P.nfilters; ++f)
+                        hist_add(P.hist, f * COLO_HIST_BINS + static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
+                                 alv, live && (bits >> P.filter_shift) == P.prefix[f]);
+                }
                 if (live) {
                     acc_fixed(A.acc, A.flags, s, alv);
-                    if (want_hist) {
-                        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
-                        for (uint32_t f = 0; f < P.nfilters; ++f)
-                            if ((bits >> P.filter_shift) == P.prefix[f])
-                                atomicAdd(reinterpret_cast<unsigned long long*>(
-                                              &P.hist[static_cast<uint64_t>(f) * COLO_HIST_BINS +
-                                                      ((bits >> P.hist_shift) & (COLO_HIST_BINS - 1))]),
-                                          static_cast<unsigned long long>(alv));
-                    }
                 }
                 if (P.samples) {
                     // samples of step k occupy alive_k consecutive slots, steps in order
@@ -1133,6 +1130,13 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     bytes += want_batches ? align256(n * sizeof(colo_batch) + 8) : 0;
     const size_t o_bflag = bytes;
     bytes += want_batches ? align256(n + 8) : 0;
+    const uint64_t sig[10] = {n, ndev, seg, nprofiles, reinterpret_cast<uintptr_t>(d_arrival),
+                              reinterpret_cast<uintptr_t>(d_prompt), reinterpret_cast<uintptr_t>(d_output),
+                              reinterpret_cast<uintptr_t>(d_dev_offsets), reinterpret_cast<uintptr_t>(d_dev_profile),
+                              ns};
+    const bool reuse = opts->reuse_entries && ctx->rs_valid && ctx->rscratch_bytes >= bytes &&
+                       std::memcmp(sig, ctx->rs_sig, sizeof sig) == 0;
+    if (!reuse) ctx->rs_valid = false;
     colo_status st = grow_rscratch(ctx, bytes);
     if (st != COLO_OK) return st;
     auto* base = static_cast<uint8_t*>(ctx->d_rscratch);
@@ -1176,7 +1180,13 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     COLO_CK(ctx, cudaMemsetAsync(P.maxctx, 0, 8, ctx->stream));
     const uint32_t seg_blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
     const uint32_t dev_blocks = static_cast<uint32_t>((ndev + kWarps - 1) / kWarps);
-    if (ns) {
+    if (ns && reuse) {  // histogram passes 2-3: the entry states of the previous full replay
+        if (P.samples) {
+            k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+            k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
+        }
+        k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    } else if (ns) {
         k_validate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         int flag = 0;
         COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1248,6 +1258,8 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     if (want_batches && ns) k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(ctx->rs_sig, sig, sizeof sig);
+    ctx->rs_valid = true;
     return COLO_OK;
 }
 
@@ -1279,6 +1291,7 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
         o.tau = tau;
         o.d_hist = d_hist;
         o.d_summary = pass == 0 ? d_sum : nullptr;
+        o.reuse_entries = pass > 0 ? 1u : 0u;
         if (pass == 0) {
             o.nfilters = 1;
             o.filter_shift = 63;
