@@ -102,9 +102,19 @@ __device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, ui
 // TPT samples usually fall in one bin, cost one atomic.  Call from all lanes.
 __device__ __forceinline__ void hist_add(uint64_t* hist, uint32_t key, uint32_t cnt, bool act) {
     const unsigned am = __ballot_sync(kFullMask, act);
+    if (!am) return;
+    const int first = __ffs(am) - 1;
+    const uint32_t k0 = __shfl_sync(kFullMask, key, first);
+    if (__all_sync(kFullMask, !act || key == k0)) {  // the common case: one bin for the whole warp
+        const unsigned total = __reduce_add_sync(kFullMask, act ? cnt : 0u);
+        if ((threadIdx.x & 31) == static_cast<unsigned>(first))
+            atomicAdd(reinterpret_cast<unsigned long long*>(&hist[k0]), static_cast<unsigned long long>(total));
+        return;
+    }
     if (!act) return;
     const unsigned peers = __match_any_sync(am, key);
-    const unsigned total = __reduce_add_sync(peers, cnt);
+    unsigned total = 0;  // sum over the peers by shuffles within the active mask
+    for (unsigned b = peers; b; b &= b - 1) total += __shfl_sync(peers, cnt, __ffs(b) - 1);
     if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
         atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(total));
 }

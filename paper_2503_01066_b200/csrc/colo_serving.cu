@@ -740,7 +740,7 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_speculate(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32, 5) k_replay_full(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
