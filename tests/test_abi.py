@@ -98,3 +98,44 @@ def test_context_without_gpu_fails_loudly():
         cs.Context(0)
     h = C.c_void_p()
     assert _lib.lib().colo_ctx_create(0, C.byref(h)) == _lib.COLO_ECUDA
+
+
+def test_generate_trace_label_delays_match_reference_fixture():
+    """The label-delay output of colo_generate_trace (workload.hpp:118-120, 214-216)
+    against the golden colocated fixtures written by the reference."""
+    z = np.load(os.path.join(ROOT, "tests", "golden", "colocated.npz"))
+    a, p, o, ld = cs.generate_trace(0.14, 1200.0, ("uniform", 4000, 7000), 5, ("uniform", 0.0, 30.0), with_labels=True)
+    assert np.array_equal(a, z["long_q014_cpa_t5_a"]) and np.array_equal(ld.view(np.uint64),
+                                                                           z["long_q014_cpa_t5_ld"].view(np.uint64))
+    _, _, _, none = cs.generate_trace(0.3, 100.0, ("fixed", 100), 3, None, with_labels=True)
+    assert (none == -1.0).all()
+
+
+def test_trace_hash_matches_reference_report():
+    """colo_trace_hash == Trace::content_hash (workload.hpp:140-161): the hash the
+    reference CLI printed for tests/golden/cli/small.config's trace."""
+    import json
+
+    from paper_2503_01066_b200 import experiment as ex
+
+    cli = os.path.join(ROOT, "tests", "golden", "cli")
+    want = json.loads(json.load(open(os.path.join(cli, "expected.json")))["run_colocated"]["report.jsonl"]["head"][0])
+    cwd = os.getcwd()
+    os.chdir(cli)
+    try:
+        tr = ex.ExperimentConfig.from_file("small.config").trace_spec.realize()
+    finally:
+        os.chdir(cwd)
+    assert tr.content_hash() == want["trace_hash"]
+    # NaN and negative label delays are both nullopt (-1.0 in the hash)
+    t2 = ex.Trace(tr.arrival, tr.prompt, tr.output, np.where(tr.label_delay < 0, np.nan, tr.label_delay), tr.query_id)
+    assert t2.content_hash() == tr.content_hash()
+
+
+def test_json_doubles_match_nlohmann_dump():
+    """colo_json_doubles uses the reference's JSON library; a value where its
+    Grisu2 output is not the shortest round trip stays 17 digits."""
+    from paper_2503_01066_b200 import experiment as ex
+
+    assert ex.json_doubles([0.020685999999997762, 0.5, 1e-05, 2.0]) == "0.020685999999997762,0.5,1e-05,2.0"
+    assert repr(0.020685999999997762) == "0.02068599999999776"  # Python's shortest form differs

@@ -431,3 +431,39 @@ def test_replay_saturated_fast_path_large(ctx, orc, monkeypatch):
     assert (outs["1"]["labels"][lo:hi] == ref["labels"]).all()
     assert S[d]["end_time"] == ref["summary"]["end_time"]
     assert int(S[d]["generated_tokens"]) == ref["summary"]["generated_tokens"]
+
+
+def test_sort_f64_matches_numpy(ctx):
+    """colo_sort_f64 (the device sort of TPT samples for export_tpt_cdf)."""
+    import ctypes as C
+
+    x = np.random.default_rng(3).exponential(0.05, 1_000_003)
+    x[::7] = 0.0
+    d_in = torch.from_numpy(x).cuda()
+    d_out = torch.empty_like(d_in)
+    cs.check(cs.lib().colo_sort_f64(ctx.h, C.c_void_p(d_in.data_ptr()), C.c_void_p(d_out.data_ptr()), len(x)), ctx.h)
+    assert np.array_equal(d_out.cpu().numpy().view(np.uint64), np.sort(x).view(np.uint64))
+
+
+def test_replay_reuse_entries_guarded(orc):
+    """reuse_entries only reuses a previous replay of the same trace buffers;
+    otherwise (fresh context, other buffers) the call replays in full."""
+    hv, hp = sharegpt_histogram()
+    fresh = cs.Context(0)
+    a1, p1, o1 = orc.generate_trace(0.8, 2000.0, ("histogram", hv, hp), 21)
+    a2, p2, o2 = orc.generate_trace(1.5, 2000.0, ("histogram", hv, hp), 22)
+
+    def run(a, p, o, reuse):
+        r = cs.replay_serving(fresh, [(cs.ModelProfile(), G)], torch.from_numpy(a).cuda(), i32(p), i32(o),
+                              torch.tensor([0, len(a)], dtype=torch.int64, device="cuda"),
+                              torch.zeros(1, dtype=torch.int16, device="cuda"), tau=0.05, samples=True,
+                              reuse_entries=reuse)
+        return r["samples"].cpu().numpy(), r["labels"].cpu().numpy()
+
+    ref1 = orc.replay_serving(default_model(), OG, a1, p1, o1, tau=0.05)
+    ref2 = orc.replay_serving(default_model(), OG, a2, p2, o2, tau=0.05)
+    s, lab = run(a1, p1, o1, True)  # nothing to reuse on a fresh context
+    assert np.array_equal(s.view(np.uint64), ref1["samples"].view(np.uint64)) and np.array_equal(lab, ref1["labels"])
+    s, lab = run(a2, p2, o2, True)  # different buffers: replays in full
+    assert np.array_equal(s.view(np.uint64), ref2["samples"].view(np.uint64)) and np.array_equal(lab, ref2["labels"])
+    fresh.close()
