@@ -299,7 +299,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         }
         // ---- batch formation: FIFO, at least one, sum(need) <= budget (engine.hpp:292-306)
         uint64_t end = head, need_total = 0, max_inc = 0;
-        uint32_t maxo = 0;
+        uint32_t maxo = 0, mino = 0xffffffffu;
         while (end < tail) {
             const uint64_t j = end + lane;
             const bool valid = j < tail;
@@ -320,12 +320,22 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             }
             max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
             maxo = max(maxo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
+            if (MODE == RUN_FULL) {
+                uint32_t mo = ok ? oj : 0xffffffffu;
+#pragma unroll
+                for (int s2 = 16; s2 > 0; s2 >>= 1) mo = min(mo, __shfl_xor_sync(FULL, mo, s2));
+                mino = min(mino, mo);
+            }
             if (cnt) need_total = __shfl_sync(FULL, incl, cnt - 1);
             end += cnt;
             if (cnt < 32) break;
         }
         __syncwarp();
         const uint64_t nb = end - head;
+        // FULL pass: a batch the all-queued records describe exactly takes its
+        // prefill and step durations from them (the same folds, done once)
+        const bool recd = MODE == RUN_FULL && P.sat_on && P.sat_end[lo + head] == end;
+        const double* __restrict__ rdk = recd ? P.sat_dk + P.sat_doff[lo + head] : nullptr;
         // The replay walks each array sequentially: keep the next ~1K queries of
         // prompt/output and the arrivals around the queue tail warm in L2 so the
         // dependent loads of later batches hit L2 instead of DRAM.
@@ -346,10 +356,14 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         // ---- prefill: left fold in batch order (engine.hpp:321-325) -------------
         // cost_model.hpp:18-25 with batch 1: 1.0 * (lin*t + (quad*t)*t) == lin*t + (quad*t)*t
         double dur = 0.0;
+        if (recd) {
+            dur = P.sat_pre[lo + head];
+        } else {
 #pragma unroll 4
-        for (uint64_t j = 0; j < nb; ++j) {
-            const double t = member_pd(j);
-            dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
+            for (uint64_t j = 0; j < nb; ++j) {
+                const double t = member_pd(j);
+                dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
+            }
         }
         const double start = T + 0.0;  // prefill_start = now_ + stall, stall = 0
         double now = start + dur;      // PrefillDone time = every member's last_token_time
@@ -369,7 +383,23 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             double kd[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
-            if (staged) {
+            if (MODE == RUN_FULL && recd) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t k = kb + 32 * r;
+                    if (k < maxo) dk[r] = rdk[k];
+                }
+                if (mino == maxo) {  // every member alive at every step
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) alive[r] = kb + 32 * r < maxo ? static_cast<uint32_t>(nb) : 0u;
+                } else {
+                    for (uint64_t j = 0; j < nb; ++j) {
+                        const uint32_t oj = member(j).y;
+#pragma unroll
+                        for (int r = 0; r < 4; ++r) alive[r] += kb + 32 * r < oj;
+                    }
+                }
+            } else if (staged) {
 #pragma unroll 4
                 for (uint64_t j = 0; j < nb; ++j) {
                     const uint32_t oj = sPO[j].y;
@@ -740,7 +770,7 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 5) k_speculate(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
@@ -785,7 +815,7 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 5) k_replay_full(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
