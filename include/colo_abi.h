@@ -167,6 +167,11 @@ void colo_ctx_destroy(colo_ctx* ctx);
 colo_status colo_ctx_set_stream(colo_ctx* ctx, void* cuda_stream);
 void* colo_ctx_stream(colo_ctx* ctx);
 colo_status colo_sync(colo_ctx* ctx);
+/* Frees the context's grow-only scratch (replay segment state, the serving
+ * replay's all-queued records and step durations -- tens of GB after a
+ * billion-query replay -- decode tables, host-pipeline buffers).  They are
+ * re-created on demand; colo_ctx_destroy frees them too. */
+colo_status colo_ctx_release_scratch(colo_ctx* ctx);
 const char* colo_last_error(const colo_ctx* ctx);
 int colo_ctx_sm_count(const colo_ctx* ctx);
 int colo_abi_version(void);

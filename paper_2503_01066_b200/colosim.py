@@ -223,6 +223,10 @@ class Context:
     def sync(self) -> None:
         check(lib().colo_sync(self.h), self.h)
 
+    def release_scratch(self) -> None:
+        """Free the context's grow-only device scratch (colo_ctx_release_scratch)."""
+        check(lib().colo_ctx_release_scratch(self.h), self.h)
+
     def close(self) -> None:
         if getattr(self, "h", None):
             lib().colo_ctx_destroy(self.h)

@@ -192,6 +192,25 @@ void colo_ctx_destroy(colo_ctx* ctx) {
     delete ctx;
 }
 
+colo_status colo_ctx_release_scratch(colo_ctx* ctx) {
+    if (!ctx) return COLO_EINVAL;
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->aux) COLO_CK(ctx, cudaStreamSynchronize(ctx->aux));
+    auto drop = [](void*& p, size_t& n) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    };
+    drop(ctx->d_pipe, ctx->pipe_bytes);
+    drop(ctx->d_rscratch, ctx->rscratch_bytes);
+    drop(ctx->d_sat, ctx->sat_bytes);
+    drop(ctx->d_satpool, ctx->satpool_bytes);
+    drop(ctx->d_dtab, ctx->dtab_bytes);
+    ctx->rs_valid = false;
+    return COLO_OK;
+}
+
 colo_status colo_ctx_set_stream(colo_ctx* ctx, void* s) {
     if (!ctx) return COLO_EINVAL;
     ctx->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream

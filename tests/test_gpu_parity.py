@@ -424,6 +424,10 @@ def test_replay_saturated_fast_path_large(ctx, orc, monkeypatch):
         outs[flag] = {k: r[k].cpu().numpy() for k in ("samples", "labels", "summary")}
     for k in ("samples", "labels", "summary"):
         assert outs["1"][k].tobytes() == outs["0"][k].tobytes(), k
+    ctx.release_scratch()  # caches are dropped and rebuilt on demand
+    monkeypatch.setenv("COLO_SAT", "1")
+    r = run_replay(ctx, a, p, o, 0.05, offs=offs)
+    assert r["samples"].cpu().numpy().tobytes() == outs["1"]["samples"].tobytes()
     d = 1  # the variable-output device against the oracle
     ref = orc.replay_serving(default_model(), OG, traces[d][0], traces[d][1], traces[d][2], tau=0.05)
     S = cs.summaries_to_numpy(outs["1"]["summary"])
