@@ -3,7 +3,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 PKG := paper_2503_01066_b200
-SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu $(PKG)/csrc/colo_colocated.cu $(PKG)/csrc/colo_report.cpp
+SRC := $(PKG)/csrc/colo_host.cu $(PKG)/csrc/colo_runtime.cu $(PKG)/csrc/colo_decide.cu $(PKG)/csrc/colo_serving.cu $(PKG)/csrc/colo_sweep.cu $(PKG)/csrc/colo_io.cu $(PKG)/csrc/colo_colocated.cu $(PKG)/csrc/colo_report.cpp $(PKG)/csrc/colo_nccl.cu
 HDR := include/colo_abi.h $(PKG)/csrc/colo_common.cuh $(PKG)/csrc/colo_internal.h $(PKG)/csrc/colo_replay.cuh
 # -fmad=false: no FMA contraction anywhere (bit-exact f64 vs the x86 reference)
 JSON_DIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
@@ -13,7 +13,7 @@ all: $(PKG)/libcolo_b200.so oracle dropin
 
 $(PKG)/libcolo_b200.so: $(SRC) $(HDR)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build/ptxas.log || (cat build/ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -ldl 2> build/ptxas.log || (cat build/ptxas.log; false)
 
 oracle:
 	$(MAKE) -s -C oracle
@@ -30,8 +30,8 @@ dropin: build/dropin_parity
 
 build/dropin_parity: tests/cpp/dropin_parity.cpp $(PKG)/cpp/colosim_gpu.hpp include/colo_abi.h $(PKG)/libcolo_b200.so
 	@if [ -d "$(REF)/include/colosim" ]; then mkdir -p build && \
-	  g++ -std=c++20 -O2 -ffp-contract=off -I$(REF)/include -I$(JSON_DIR) -Iinclude -I$(PKG)/cpp \
-	    -o $@ tests/cpp/dropin_parity.cpp -L$(PKG) -lcolo_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
+	  g++ -std=c++20 -O2 -ffp-contract=off -I$(REF)/include -I$(JSON_DIR) -Iinclude -I$(PKG)/cpp -I/usr/local/cuda/include \
+	    -o $@ tests/cpp/dropin_parity.cpp -L$(PKG) -lcolo_b200 -lnccl -Wl,-rpath,'$$ORIGIN/../$(PKG)'; \
 	else echo "dropin: $(REF) absent, keeping prebuilt build/dropin_parity"; fi
 
 .PHONY: dropin

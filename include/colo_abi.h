@@ -44,6 +44,8 @@
  *                                                                    include/colosim/metrics.hpp:56-69
  *   colo_hist_select / percentiles  finalize / nearest_rank          include/colosim/metrics.hpp:48-69
  *   colo_generate_trace             generate_trace (host, bit-exact) include/colosim/workload.hpp:193-220
+ *   colo_stats_allreduce /          the fleet-wide statistics exchange (no reference
+ *   colo_serving_stats_nccl         counterpart: the reference is single-process)
  */
 #ifndef COLO_ABI_H
 #define COLO_ABI_H
@@ -436,6 +438,21 @@ colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size
  * report serializer, metrics.hpp:191-226), comma-separated, NUL-terminated
  * into out when cap exceeds the length.  Returns the length (without NUL). */
 int64_t colo_json_doubles(const double* v, size_t n, char* out, size_t cap);
+
+/* ------------------------------------------------------- multi-GPU stats */
+/* The one cross-GPU exchange.  nccl_comm is the caller's
+ * ncclComm_t (passed as void*; NCCL is resolved at run time, so this library
+ * does not link it).  colo_stats_allreduce sums n u64 in place on the
+ * context's stream.  colo_serving_stats_nccl is colo_serving_stats over a
+ * device-sharded fleet: each rank replays its own devices and the histograms,
+ * counters and exact sums are all-reduced between the passes, so every rank
+ * returns the fleet-wide p50/p90/p99/mean and totals. */
+colo_status colo_stats_allreduce(colo_ctx* ctx, void* nccl_comm, uint64_t* d_buf, size_t n);
+colo_status colo_serving_stats_nccl(colo_ctx* ctx, void* nccl_comm, const colo_model* models, const colo_gpu* gpus,
+                                    size_t nprofiles, const double* d_arrival, const uint32_t* d_prompt,
+                                    const uint32_t* d_output, size_t n, const uint64_t* d_dev_offsets,
+                                    const uint16_t* d_dev_profile, size_t ndev, double tau, double* pctl,
+                                    colo_device_summary* totals);
 
 /* --------------------------------------------------------- trace synthesis */
 /* generate_trace (workload.hpp:193-220) on the host, bit-exact (mt19937_64 +

@@ -177,7 +177,8 @@ EXPORTS = [
     "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
     "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
     "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats", "colo_trace_hash",
-    "colo_sort_f64", "colo_json_doubles", "colo_ctx_release_scratch",
+    "colo_sort_f64", "colo_json_doubles", "colo_ctx_release_scratch", "colo_stats_allreduce",
+    "colo_serving_stats_nccl",
 ]
 
 
@@ -205,6 +206,9 @@ def lib() -> C.CDLL:
         "colo_ctx_stream": (vp, [vp]),
         "colo_sync": (i32, [vp]),
         "colo_ctx_release_scratch": (i32, [vp]),
+        "colo_stats_allreduce": (i32, [vp, vp, vp, sz]),
+        "colo_serving_stats_nccl": (i32, [vp, vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp,
+                                         C.POINTER(DeviceSummary)]),
         "colo_last_error": (C.c_char_p, [vp]),
         "colo_ctx_sm_count": (i32, [vp]),
         "colo_abi_version": (i32, []),

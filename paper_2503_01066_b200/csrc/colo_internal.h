@@ -61,6 +61,8 @@ colo_status check_model_limits(const colo_model* m);
 // correctly rounded (sum * 2^-96) / n from a 192-bit little-endian fixed-point sum
 double fixed_mean(const uint64_t sum[3], uint64_t n);
 void fixed_add(uint64_t acc[3], const uint64_t v[3]);
+// in-place ncclAllReduce on the context's stream (NCCL resolved at run time)
+colo_status nccl_allreduce_raw(colo_ctx* ctx, void* comm, void* d_buf, size_t count, int dtype, int op);
 
 }  // namespace colo
 

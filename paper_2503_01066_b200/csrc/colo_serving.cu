@@ -1089,6 +1089,58 @@ colo_status grow_rscratch(colo_ctx* ctx, size_t bytes) {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Cross-rank totals of the first stats pass (colo_serving_stats_nccl): sums
+// of the counters and of the exact 192-bit TPT sum, the latter as six 32-bit
+// chunks so no carry is lost in the u64 reduction; max of the peaks.
+colo_status dist_totals(colo_ctx* ctx, void* comm, colo_device_summary* t) {
+    uint64_t hs[12] = {t->generated_tokens, t->slow_tokens, t->slow_queries, t->batches};
+    for (int i = 0; i < 6; ++i) hs[4 + i] = (t->tpt_sum[i / 2] >> (32 * (i & 1))) & 0xffffffffull;
+    uint64_t hm[4] = {t->peak_device_bytes, t->max_batch_size, t->flags, 0};
+    double he = t->end_time;
+    uint64_t* d = nullptr;
+    COLO_CK(ctx, cudaMalloc(&d, 17 * 8));
+    colo_status st = COLO_OK;
+    do {
+        if (cudaMemcpy(d, hs, 10 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(d + 10, hm, 4 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(d + 14, &he, 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+            st = set_err(ctx, COLO_ECUDA, "dist_totals staging");
+            break;
+        }
+        if ((st = colo_stats_allreduce(ctx, comm, d, 10)) != COLO_OK) break;
+        if ((st = nccl_allreduce_raw(ctx, comm, d + 10, 4, /*ncclUint64*/ 5, /*ncclMax*/ 2)) != COLO_OK) break;
+        if ((st = nccl_allreduce_raw(ctx, comm, d + 14, 1, /*ncclFloat64*/ 8, /*ncclMax*/ 2)) != COLO_OK) break;
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || cudaMemcpy(hs, d, 10 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(hm, d + 10, 4 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(&he, d + 14, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            st = set_err(ctx, COLO_ECUDA, "dist_totals readback");
+            break;
+        }
+        t->generated_tokens = hs[0];
+        t->slow_tokens = hs[1];
+        t->slow_queries = hs[2];
+        t->batches = hs[3];
+        uint64_t acc[3] = {0, 0, 0};
+        for (int i = 0; i < 6; ++i) {  // chunk i weighs 2^(32 i); each chunk sum < 2^64
+            const uint64_t v = hs[4 + i];
+            uint64_t add[3] = {0, 0, 0};
+            const int limb = i / 2, sh = 32 * (i & 1);
+            add[limb] = v << sh;
+            if (sh && limb + 1 < 3) add[limb + 1] = v >> (64 - sh);
+            fixed_add(acc, add);
+        }
+        t->tpt_sum[0] = acc[0];
+        t->tpt_sum[1] = acc[1];
+        t->tpt_sum[2] = acc[2];
+        t->peak_device_bytes = hm[0];
+        t->max_batch_size = hm[1];
+        t->flags = hm[2];
+        t->end_time = he;
+    } while (false);
+    cudaFree(d);
+    return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1293,10 +1345,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     return COLO_OK;
 }
 
-colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const colo_gpu* gpus, size_t nprofiles,
-                               const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
-                               const uint64_t* d_dev_offsets, const uint16_t* d_dev_profile, size_t ndev, double tau,
-                               double* pctl, colo_device_summary* totals) {
+static colo_status serving_stats_impl(colo_ctx* ctx, void* comm, const colo_model* models, const colo_gpu* gpus,
+                                      size_t nprofiles, const double* d_arrival, const uint32_t* d_prompt,
+                                      const uint32_t* d_output, size_t n, const uint64_t* d_dev_offsets,
+                                      const uint16_t* d_dev_profile, size_t ndev, double tau, double* pctl,
+                                      colo_device_summary* totals) {
     if (!ctx || !pctl || !totals) return COLO_EINVAL;
     COLO_CK(ctx, cudaSetDevice(ctx->device));
     const size_t hbytes = sizeof(uint64_t) * 3 * COLO_HIST_BINS;
@@ -1340,6 +1393,10 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
         st = colo_replay_serving(ctx, models, gpus, nprofiles, d_arrival, d_prompt, d_output, n, d_dev_offsets,
                                  d_dev_profile, ndev, &o);
         if (st != COLO_OK) break;
+        if (comm) {  // every rank holds its own device shard: sum the histograms
+            st = colo_stats_allreduce(ctx, comm, d_hist, static_cast<size_t>(o.nfilters) * COLO_HIST_BINS);
+            if (st != COLO_OK) break;
+        }
         e = cudaMemcpy(h.data(), d_hist, sizeof(uint64_t) * o.nfilters * COLO_HIST_BINS, cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) {
             st = cuda_err(ctx, e, "hist D2H");
@@ -1361,6 +1418,10 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
                 totals->end_time = std::max(totals->end_time, s.end_time);
                 fixed_add(totals->tpt_sum, s.tpt_sum);
                 totals->flags |= s.flags;
+            }
+            if (comm) {  // counters and the exact sum (as 32-bit chunks) summed; peaks and end time maxed
+                st = dist_totals(ctx, comm, totals);
+                if (st != COLO_OK) break;
             }
             ntot = totals->generated_tokens;
             if (ntot == 0) break;
@@ -1390,6 +1451,25 @@ colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const co
     cudaFree(d_hist);
     cudaFree(d_sum);
     return st;
+}
+
+
+colo_status colo_serving_stats(colo_ctx* ctx, const colo_model* models, const colo_gpu* gpus, size_t nprofiles,
+                               const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
+                               const uint64_t* d_dev_offsets, const uint16_t* d_dev_profile, size_t ndev, double tau,
+                               double* pctl, colo_device_summary* totals) {
+    return serving_stats_impl(ctx, nullptr, models, gpus, nprofiles, d_arrival, d_prompt, d_output, n, d_dev_offsets,
+                              d_dev_profile, ndev, tau, pctl, totals);
+}
+
+colo_status colo_serving_stats_nccl(colo_ctx* ctx, void* nccl_comm, const colo_model* models, const colo_gpu* gpus,
+                                    size_t nprofiles, const double* d_arrival, const uint32_t* d_prompt,
+                                    const uint32_t* d_output, size_t n, const uint64_t* d_dev_offsets,
+                                    const uint16_t* d_dev_profile, size_t ndev, double tau, double* pctl,
+                                    colo_device_summary* totals) {
+    if (!nccl_comm) return COLO_EINVAL;
+    return serving_stats_impl(ctx, nccl_comm, models, gpus, nprofiles, d_arrival, d_prompt, d_output, n, d_dev_offsets,
+                              d_dev_profile, ndev, tau, pctl, totals);
 }
 
 }  // extern "C"

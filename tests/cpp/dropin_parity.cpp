@@ -8,6 +8,8 @@
 #include <cstring>
 #include <random>
 
+#include <nccl.h>
+
 #include "colosim/engine.hpp"
 #include "colosim/experiment.hpp"
 #include "colosim_gpu.hpp"
@@ -174,6 +176,57 @@ int main() {
             EXPECT(false, "map hash mismatch accepted");
         } catch (const std::runtime_error&) {
         }
+    }
+    // fleet statistics over an NCCL communicator (one rank here): the same
+    // bits as the single-process colo_serving_stats
+    {
+        ncclUniqueId id;
+        ncclComm_t comm;
+        EXPECT(ncclGetUniqueId(&id) == ncclSuccess, "ncclGetUniqueId");
+        EXPECT(ncclCommInitRank(&comm, 1, id, 0) == ncclSuccess, "ncclCommInitRank");
+        Trace trace = generate_trace(0.9, 3000.0, LengthDistribution::uniform(100, 4000), std::nullopt, 23);
+        std::vector<double> a;
+        std::vector<uint32_t> p, o;
+        for (const auto& r : trace.records) {
+            a.push_back(r.arrival_time);
+            p.push_back(uint32_t(r.prompt_tokens));
+            o.push_back(uint32_t(r.output_tokens));
+        }
+        colo_ctx* c = ctx.get();
+        const size_t n = a.size();
+        void *d_a, *d_p, *d_o, *d_off, *d_prof;
+        colosim_gpu::check(colo_dev_alloc(c, n * 8, &d_a), c, "alloc");
+        colosim_gpu::check(colo_dev_alloc(c, n * 4, &d_p), c, "alloc");
+        colosim_gpu::check(colo_dev_alloc(c, n * 4, &d_o), c, "alloc");
+        colosim_gpu::check(colo_dev_alloc(c, 16, &d_off), c, "alloc");
+        colosim_gpu::check(colo_dev_alloc(c, 2, &d_prof), c, "alloc");
+        const uint64_t offs[2] = {0, n};
+        const uint16_t prof = 0;
+        colo_memcpy_h2d(c, d_a, a.data(), n * 8);
+        colo_memcpy_h2d(c, d_p, p.data(), n * 4);
+        colo_memcpy_h2d(c, d_o, o.data(), n * 4);
+        colo_memcpy_h2d(c, d_off, offs, 16);
+        colo_memcpy_h2d(c, d_prof, &prof, 2);
+        colo_model cm = colosim_gpu::to_c_model(ModelProfile{});
+        colo_gpu cg = colosim_gpu::to_c_gpu(GpuProfile{});
+        double p1[4], p2[4];
+        colo_device_summary t1{}, t2{};
+        EXPECT(colo_serving_stats(c, &cm, &cg, 1, (double*)d_a, (uint32_t*)d_p, (uint32_t*)d_o, n, (uint64_t*)d_off,
+                                  (uint16_t*)d_prof, 1, 0.05, p1, &t1) == COLO_OK, "serving_stats");
+        EXPECT(colo_serving_stats_nccl(c, comm, &cm, &cg, 1, (double*)d_a, (uint32_t*)d_p, (uint32_t*)d_o, n,
+                                       (uint64_t*)d_off, (uint16_t*)d_prof, 1, 0.05, p2, &t2) == COLO_OK,
+               "serving_stats_nccl: %s", colo_last_error(c));
+        EXPECT(std::memcmp(p1, p2, sizeof p1) == 0, "NCCL stats percentiles differ");
+        EXPECT(std::memcmp(&t1, &t2, sizeof t1) == 0, "NCCL stats totals differ");
+        MetricsReport rep = run_simulation([&] {
+            SimConfig cfg;
+            cfg.mode = SimMode::ServingOnly;
+            cfg.trace = trace;
+            return cfg;
+        }());
+        EXPECT(p2[0] == *rep.tpt_p50 && p2[1] == *rep.tpt_p90 && p2[2] == *rep.tpt_p99, "NCCL stats vs finalize");
+        for (void* q : {d_a, d_p, d_o, d_off, d_prof}) colo_dev_free(c, q);
+        ncclCommDestroy(comm);
     }
     // the reference's error contract through the shim
     try {
