@@ -391,7 +391,9 @@ typedef struct colo_colocated_opts {
     uint32_t nfilters;
     uint32_t hist_shift;
     uint32_t filter_shift;
-    uint32_t pad;
+    uint32_t seg_len;                /* 0: automatic -- with fewer devices than the GPU holds warps, long devices
+                                        run in parallel segments split at idle arrivals (bit-identical results);
+                                        0xffffffff: never; else the segment length in queries */
     uint64_t filter_prefix[3];
     const uint8_t* d_dev_sim_mode;   /* [ndev] COLO_SIM_*; NULL = every device Colocated */
 } colo_colocated_opts;

@@ -142,7 +142,7 @@ class ColocatedOpts(C.Structure):
         ("nfilters", C.c_uint32),
         ("hist_shift", C.c_uint32),
         ("filter_shift", C.c_uint32),
-        ("pad", C.c_uint32),
+        ("seg_len", C.c_uint32),
         ("filter_prefix", C.c_uint64 * 3),
         ("d_dev_sim_mode", C.c_void_p),
     ]

@@ -802,7 +802,7 @@ class SimMode(enum.IntEnum):
 
 
 def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay, default_label_delay,
-                    cache_timeout, tau, samples, labels, batches, summary, res, keep, sim_mode=None):
+                    cache_timeout, tau, samples, labels, batches, summary, res, keep, sim_mode=None, seg_len=None):
     torch = _torch()
     dev = prompt.device
     _need_cuda(arrival, "arrival", 8)
@@ -816,6 +816,7 @@ def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, la
     o.cache_timeout = cache_timeout
     o.default_label_delay = default_label_delay
     o.tau = tau
+    o.seg_len = 0 if seg_len is None else (0xFFFFFFFF if seg_len == 0 else int(seg_len))
     if label_delay is not None:
         _need_cuda(label_delay, "label_delay", 8)
         o.d_label_delay = label_delay.data_ptr()
@@ -852,7 +853,7 @@ def _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, la
 def replay_colocated(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                      label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
                      tau: float = math.inf, samples: bool = False, labels: bool = True, batches: bool = False,
-                     summary: bool = True, sim_mode=None):
+                     summary: bool = True, sim_mode=None, seg_len=None):
     """Simulation::run of every device (engine.hpp:140-903), by default in
     SimMode::Colocated; ``sim_mode`` (a SimMode for all devices or a per-device
     uint8 tensor) selects ServingOnly / Colocated / SeparateCluster.  Device d runs with map set ``sets[dev_set[d]]`` and
@@ -862,12 +863,15 @@ def replay_colocated(ctx: Context, sets: Sequence[MapSet], arrival, prompt, outp
     ``default_label_delay`` (the reference's TraceSpec default is fixed 0.01 s,
     experiment.hpp:45).  Raises ColoBreachError if a device's run breaches an
     invariant (the reference throws InvariantBreach).
+    ``seg_len``: None = automatic (with fewer devices than the GPU holds
+    warps, long devices replay in parallel segments split at idle arrivals --
+    same bits), 0 = never segment, else the segment length in queries.
     Returns a dict of device tensors: samples, labels, batches (BATCH_DTYPE
     bytes at d_dev_offsets[d] + b), summary (ColocatedSummary bytes)."""
     res, keep = {}, []
     o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
                                       default_label_delay, cache_timeout, tau, samples, labels, batches, summary,
-                                      res, keep, sim_mode)
+                                      res, keep, sim_mode, seg_len)
     try:
         check(lib().colo_replay_colocated(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),
                                           _ptr(output), n, _ptr(dev_offsets), _ptr(dev_set), ndev, C.byref(o)),
@@ -891,14 +895,14 @@ def colocated_summaries(summary_bytes) -> list:
 
 def colocated_stats(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                     label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
-                    tau: float = math.inf, sim_mode=None):
+                    tau: float = math.inf, sim_mode=None, seg_len=None):
     """colo_colocated_stats: colocated replays of every device + exact
     nearest-rank p50/p90/p99 and mean of the union of their TPT samples
     (finalize, metrics.hpp:56-69).  Returns (pctl[4], totals dict)."""
     res, keep = {}, []
     o, arr, n, ndev = _colocated_opts(ctx, sets, arrival, prompt, output, dev_offsets, dev_set, label_delay,
                                       default_label_delay, cache_timeout, tau, False, False, False, False, res, keep,
-                                      sim_mode)
+                                      sim_mode, seg_len)
     pctl = (C.c_double * 4)()
     tot = _lib.ColocatedSummary()
     check(lib().colo_colocated_stats(ctx.h, C.cast(arr, C.c_void_p), len(sets), _ptr(arrival), _ptr(prompt),

@@ -43,6 +43,8 @@
 // /root/reference/proj/.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -70,6 +72,56 @@ struct CoProfile {
     uint32_t cpa, L;
 };
 
+// ---- one device's trace in parallel segments ----------------------------------
+// At an arrival popped while no batch is serving, no training layer is in
+// flight, the queue is empty (arrivals queued behind a training layer wait for
+// the next arrival, engine.hpp:273), there is no slot / job (has_store_
+// false), no label pending and the d2h channel is free (busy_until <= now),
+// the state is *fresh-equivalent*:
+// the rest of the run equals a run started fresh at that arrival.  Pending
+// cache timeouts are stale (generation mismatch) and prefetch plans cancelled,
+// so both are no-ops; sequence numbers only order events relative to each
+// other; the ledger's live bytes are the fixed footprint, and allocated_ =
+// max(allocated_ before, live) makes peak_allocated the max over segments.
+// So (speculate) every segment j runs fresh from s_j and records the idle
+// arrivals it meets in [s_j, s_{j+1}) (head) and past s_{j+1} (tail); (resolve)
+// the true run enters segment j at b_j = the first arrival idle in both
+// segment j-1's tail and segment j's head (b_0 = 0, by induction the truth is
+// idle there and equals segment j's run); (out) every segment replays
+// [b_j, b_{j+1}) with all outputs at offsets from the recorded counters.  The
+// three f64 sums of the report are sequential folds; the segments log their
+// addends and k_fold_* fold the logs exactly in the reference's order.
+constexpr int kSegPts = 32;  // idle arrivals kept per head / tail list
+enum { TM_DIRECT = 0, TM_SPEC = 1, TM_OUT = 2 };
+
+struct SegTask {
+    uint32_t dev, mode;
+    uint64_t start;  // first query (device-local)
+    uint64_t next;   // SPEC: the next segment's start; OUT: the stop arrival (b_{j+1}, or N)
+    uint64_t xend;   // SPEC: give up past this query
+    uint64_t batch_base, job_base, sample_base;
+    uint64_t log_base[3];  // absolute positions in P.log[k]
+    uint64_t expect[5];    // OUT: batches, jobs, log entries the speculation counted (a mismatch is an error)
+};
+
+struct SegPoint {  // counters at an idle arrival (relative to the segment start)
+    uint64_t idx, samples, batches, jobs, nlog[3];
+};
+
+struct SegSpec {
+    uint32_t nhead, ntail, err, pad;
+    SegPoint end;  // counters at the end of the trace (idx = ~0: not reached)
+    SegPoint head[kSegPts];
+    SegPoint tail[kSegPts];
+};
+
+struct SegOut {
+    colo_colocated_summary s;
+    uint64_t jobs;
+    uint64_t err;     // 0, or why the segment disagreed with its speculation (1 busy / 2 not idle at the stop, 3 counts)
+    uint64_t nlog[3];
+};
+
 struct CoParams {
     CoProfile prof[kMaxSets];
     MapView sets[kMaxSets];
@@ -95,6 +147,12 @@ struct CoParams {
     double* job_t;     // SeparateCluster job stream (enqueue time), at dev_off[d] + i
     uint32_t* job_q;   // ... and its query (device-local index)
     uint64_t* job_cnt; // [ndev]
+    // segmented runs (NULL tasks: warp w = device w, whole trace)
+    const SegTask* tasks;
+    uint32_t ntasks;
+    SegSpec* spec;     // [task] (SPEC)
+    SegOut* segout;    // [task] (OUT)
+    double* log[3];    // addends of training_busy_time, copy_stall_seconds, prefetch_wait_seconds (OUT)
 };
 
 struct WarpSmem {
@@ -125,8 +183,19 @@ __device__ __forceinline__ double warp_max_f64(double v) {
 __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constant__ CoParams P) {
     __shared__ WarpSmem SM[kWarpsC];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t d = blockIdx.x * kWarpsC + wib;
-    if (d >= P.ndev) return;
+    const uint32_t w = blockIdx.x * kWarpsC + wib;
+    uint32_t d = w;
+    int tmode = TM_DIRECT;
+    uint64_t q0 = 0;
+    if (P.tasks) {
+        if (w >= P.ntasks) return;
+        d = P.tasks[w].dev;
+        tmode = static_cast<int>(P.tasks[w].mode);
+        q0 = P.tasks[w].start;
+    } else if (d >= P.ndev) {
+        return;
+    }
+    const bool spec = tmode == TM_SPEC;
     WarpSmem& S = SM[wib];
     const uint32_t pi = P.dev_set[d];
     const CoProfile& pf = P.prof[pi];
@@ -158,7 +227,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     // ---- state (warp-uniform) ----------------------------------------------
     double now = 0.0;
     uint64_t seq = N;          // arrivals own 0..N-1
-    uint64_t ai = 0, qhead = 0;  // queue_ = [qhead, ai)
+    uint64_t ai = q0, qhead = q0;  // queue_ = [qhead, ai)
     uint64_t alloc = 0, resv = 0, peak = 0;  // MemoryLedger device_
     double d2h_busy = 0.0;                   // TransferChannel d2h_
     bool breach = false;
@@ -195,15 +264,26 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     // per-pass constants (recomputed bit-identically when the key changes)
     uint64_t fwd_tok = ~0ull, cp_bytes = ~0ull;
     double fwd_val = 0.0, cp_val = 0.0;
-    double na = N ? arr[0] : 0.0;  // arrival time of query ai
+    double na = q0 < N ? arr[q0] : 0.0;  // arrival time of query ai
     // report (uniform) + per-lane sample partials
     uint64_t r_trained = 0, r_ptab = 0, r_pre = 0, r_freed = 0, r_loads = 0, r_recomp = 0, r_dropped = 0, r_jobs = 0,
              r_fb = 0, r_batches = 0, r_maxb = 0, r_offd = 0, r_adm = 0;
     double r_stall = 0.0, r_wait = 0.0, r_end = 0.0;
     uint64_t a_gen = 0, a_slow = 0, a_slowq = 0, a_acc[3] = {0, 0, 0};
     uint32_t a_flags = 0;
-    uint64_t sample_pos = P.samples ? P.sample_off[d] : 0;
-    const bool want_hist = P.hist != nullptr;
+    // outputs (a speculative segment writes none; an OUT segment at its offsets)
+    double* const samples_out = spec ? nullptr : P.samples;
+    uint8_t* const labels_out = spec ? nullptr : P.labels;
+    colo_batch* const batches_out =
+        spec || !P.batches ? nullptr : P.batches + lo + (tmode == TM_OUT ? P.tasks[w].batch_base : 0);
+    const uint64_t job_base = lo + (tmode == TM_OUT ? P.tasks[w].job_base : 0);
+    uint64_t sample_pos = samples_out ? P.sample_off[d] + (tmode == TM_OUT ? P.tasks[w].sample_base : 0) : 0;
+    const bool want_hist = !spec && P.hist != nullptr;
+    // addends of the three f64 sums (counted by SPEC, logged by OUT)
+    uint64_t nl0 = 0, nl1 = 0, nl2 = 0;
+    bool seg_err = false, stopped = false;
+    uint32_t seg_why = 0;
+    uint32_t nhead = 0, ntail = 0;
 
     auto live = [&]() -> uint64_t { return alloc - resv; };
     auto led_alloc = [&](uint64_t bytes) -> bool {  // memory.hpp:28-35
@@ -217,6 +297,22 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     auto led_free = [&](uint64_t bytes) {  // memory.hpp:37-40
         if (bytes > alloc - resv) breach = true;  // std::logic_error
         resv += bytes;
+    };
+    // training_busy_time / copy_stall_seconds / prefetch_wait_seconds += x
+    auto add_busy = [&](double x) {
+        tbusy += x;
+        if (tmode == TM_OUT && lane == 0 && nl0 < P.tasks[w].expect[2]) P.log[0][P.tasks[w].log_base[0] + nl0] = x;
+        ++nl0;
+    };
+    auto add_stall = [&](double x) {
+        r_stall += x;
+        if (tmode == TM_OUT && lane == 0 && nl1 < P.tasks[w].expect[3]) P.log[1][P.tasks[w].log_base[1] + nl1] = x;
+        ++nl1;
+    };
+    auto add_wait = [&](double x) {
+        r_wait += x;
+        if (tmode == TM_OUT && lane == 0 && nl2 < P.tasks[w].expect[4]) P.log[2][P.tasks[w].log_base[2] + nl2] = x;
+        ++nl2;
     };
     auto pass_tok = [&](uint64_t i) -> uint64_t { return i == 0 ? pass0 : (i == 1 ? pass1 : pass2); };
     uint64_t cur_tok = 0;  // passes[pass_index] of the running forward pass (set by begin_pass)
@@ -530,8 +626,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             return 0.0;
         }
         const double stall = dmax(0.0, ready - now);
-        r_stall += stall;
-        tbusy += stall;
+        add_stall(stall);
+        add_busy(stall);
         vbits = COLO_V_EVALUATED | pack_verdict(action, layers, free_now, 0, fallback, hedge_oor, COLO_VD_FREE_LOADBACK);
         return stall;
     };
@@ -745,9 +841,11 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                             const double prev_lane = __shfl_sync(kFullMask, te, below ? 31 - __clz(below) : 0);
                             if (em) {
                                 if (te < (below ? prev_lane : last_t)) unsorted = true;
-                                const uint64_t pos = lo + jc + __popc(below);
-                                P.job_t[pos] = te;
-                                P.job_q[pos] = static_cast<uint32_t>(head + j);
+                                if (!spec && (tmode != TM_OUT || jc + __popc(below) < P.tasks[w].expect[1])) {
+                                    const uint64_t pos = job_base + jc + __popc(below);
+                                    P.job_t[pos] = te;
+                                    P.job_q[pos] = static_cast<uint32_t>(head + j);
+                                }
                             }
                             last_t = __shfl_sync(kFullMask, te, 31 - __clz(bal));
                             jc += __popc(bal);
@@ -779,7 +877,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 if (lv) {
                     acc_fixed(a_acc, a_flags, s, alv);
                 }
-                if (P.samples) {  // step k's samples: alive_k consecutive slots, steps in order
+                if (samples_out) {  // step k's samples: alive_k consecutive slots, steps in order
                     uint32_t ex = alv;
 #pragma unroll
                     for (int sft = 1; sft < 32; sft <<= 1) {
@@ -788,7 +886,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                     }
                     const uint32_t tot = __shfl_sync(kFullMask, ex, 31);
                     const uint64_t pos = sample_pos + ex - alv;
-                    for (uint32_t a = 0; a < alv; ++a) P.samples[pos + a] = s;
+                    for (uint32_t a = 0; a < alv; ++a) samples_out[pos + a] = s;
                     sample_pos += tot;
                 }
             }
@@ -797,9 +895,9 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             const uint32_t oj = staged ? S.po[j].y : po[head + j];
             const bool slowq = oj > first_slow;
             a_slowq += slowq;
-            if (P.labels) P.labels[lo + head + j] = slowq ? 1 : 0;
+            if (labels_out) labels_out[lo + head + j] = slowq ? 1 : 0;
         }
-        if (lane == 0 && P.batches) {
+        if (lane == 0 && batches_out && (tmode != TM_OUT || r_batches < P.tasks[w].expect[0])) {
             colo_batch b;
             b.start = start;
             b.end = tnow;
@@ -808,7 +906,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             b.need_total = need_total;
             b.max_incoming = max_inc < 0xffffffffull ? static_cast<uint32_t>(max_inc) : 0xffffffffu;
             b.verdict = vbits;
-            P.batches[lo + r_batches] = b;
+            batches_out[r_batches] = b;
         }
         ++r_batches;
         if (nb > r_maxb) r_maxb = nb;
@@ -852,15 +950,58 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             if (sbusy || tinf) {  // engine.hpp:273: queued only; take every arrival up to the next event
                 ai = bk == EK_NONE ? N : find_tail(arr, N, ai, bt);
                 na = ai < N ? arr[ai] : 0.0;
+                if (tmode != TM_DIRECT) {
+                    if (tmode == TM_OUT && ai > P.tasks[w].next) {  // the stop arrival came while busy
+                        seg_err = stopped = true;
+                        seg_why = 1;
+                        break;
+                    }
+                    if (spec && ai < N && ai >= P.tasks[w].xend) {
+                        stopped = true;
+                        break;
+                    }
+                }
                 continue;
+            }
+            if (tmode != TM_DIRECT) {  // a fresh-equivalent state (see SegTask)?
+                const bool idle = qhead == ai && !has_store && !has_job && !l_on && d2h_busy <= na;
+                const uint64_t nx = P.tasks[w].next;
+                if (tmode == TM_OUT) {
+                    if (ai == nx) {
+                        seg_err = !idle;
+                        if (!idle) seg_why = 2;
+                        stopped = true;
+                        break;
+                    }
+                } else {
+                    if (idle && (ai < nx ? nhead : ntail) < kSegPts) {
+                        const uint64_t gen_tot = warp_sum_u64(a_gen);
+                        if (lane == 0) {
+                            SegPoint& sp = ai < nx ? P.spec[w].head[nhead] : P.spec[w].tail[ntail];
+                            sp.idx = ai;
+                            sp.samples = gen_tot;
+                            sp.batches = r_batches;
+                            sp.jobs = jc;
+                            sp.nlog[0] = nl0;
+                            sp.nlog[1] = nl1;
+                            sp.nlog[2] = nl2;
+                        }
+                        if (ai < nx) ++nhead;
+                        else ++ntail;
+                    }
+                    if (ntail == kSegPts || (ai >= P.tasks[w].xend && P.tasks[w].xend < N)) {
+                        stopped = true;
+                        break;
+                    }
+                }
             }
             now = na;
             ++ai;
             na = ai < N ? arr[ai] : 0.0;
             if (has_job && waiting) {  // interrupt_training_wait(true), engine.hpp:622-631
                 const double waited = now - wait_since;
-                r_wait += waited;
-                tbusy += waited;
+                add_wait(waited);
+                add_busy(waited);
                 waiting = false;
                 ++r_pre;
                 ++plan_gen;
@@ -896,7 +1037,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             want_serve = true;
         } else if (bk == EK_TRAIN) {
             tinf = false;
-            tbusy += t_dur;
+            add_busy(t_dur);
             if (t_fwd) {  // engine.hpp:693-722
                 const uint64_t bytes = cur_tok * m.act_bytes_per_token_per_layer;
                 if (stream && S.rec[cursor] == 0) ++r_freed;
@@ -954,8 +1095,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             ++r_loads;
             if (has_job && waiting && phase == PH_BWD && cursor == a && !sbusy && qhead == ai) {
                 const double waited = now - wait_since;
-                r_wait += waited;
-                tbusy += waited;
+                add_wait(waited);
+                add_busy(waited);
                 waiting = false;
                 schedule_backward();
             }
@@ -987,10 +1128,36 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         acc[2] = a2;
         for (int s = 16; s > 0; s >>= 1) flags |= __shfl_xor_sync(kFullMask, flags, s);
     }
-    if (breach && lane == 0) atomicOr(P.err, 2);
+    if (spec) {
+        if (lane == 0) {
+            SegSpec& sp = P.spec[w];
+            sp.nhead = nhead;
+            sp.ntail = ntail;
+            sp.err = breach || seg_err;
+            sp.end.idx = stopped || breach ? ~0ull : N;
+            sp.end.samples = g_gen;
+            sp.end.batches = r_batches;
+            sp.end.jobs = jc;
+            sp.end.nlog[0] = nl0;
+            sp.end.nlog[1] = nl1;
+            sp.end.nlog[2] = nl2;
+        }
+        return;
+    }
+    if (tmode == TM_OUT) {  // a breach is re-run on the whole trace (its report stops there)
+        const uint64_t* ex = P.tasks[w].expect;
+        if (!breach && !seg_err && (r_batches != ex[0] || jc != ex[1] || nl0 != ex[2] || nl1 != ex[3] || nl2 != ex[4])) {
+            seg_err = true;
+            seg_why = 3;
+        }
+        if (breach && lane == 0) atomicOr(P.err, 8);
+        if (seg_err && lane == 0) atomicOr(P.err, 16);
+    } else if (breach && lane == 0) {
+        atomicOr(P.err, 2);
+    }
     if (__any_sync(kFullMask, unsorted) && lane == 0) atomicOr(P.err, 4);
-    if (P.job_cnt && lane == 0) P.job_cnt[d] = jc;  // every device (0 unless SeparateCluster): sort segments
-    if (lane == 0 && P.summary) {
+    if (tmode == TM_DIRECT && P.job_cnt && lane == 0) P.job_cnt[d] = jc;  // every device (0 unless SeparateCluster)
+    if (lane == 0 && (P.summary || tmode == TM_OUT)) {
         colo_colocated_summary r;
         r.generated_tokens = g_gen;
         r.trained_tokens = r_trained;
@@ -1019,7 +1186,16 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         r.tpt_sum[1] = acc[1];
         r.tpt_sum[2] = acc[2];
         r.flags = flags;
-        P.summary[d] = r;
+        if (tmode == TM_OUT) {
+            P.segout[w].s = r;
+            P.segout[w].jobs = jc;
+            P.segout[w].err = seg_why;
+            P.segout[w].nlog[0] = nl0;
+            P.segout[w].nlog[1] = nl1;
+            P.segout[w].nlog[2] = nl2;
+        } else {
+            P.summary[d] = r;
+        }
     }
 }
 
@@ -1105,6 +1281,220 @@ __global__ void __launch_bounds__(128) k_co_validate(const __grid_constant__ CoP
     if (__any_sync(kFullMask, bad) && lane == 0) atomicOr(P.err, 1);
 }
 
+// ---- exact sequential f64 folds of the segments' addend logs ------------------
+// S_{i+1} = fl(S_i + a_i), a_i >= 0, in log order, without a sequential pass
+// over every addend.  While S stays in one binade [2^e, 2^(e+1)) the grid is
+// u = 2^(e-52), S is a multiple of u, and fl(S + a) = S + RN_u(a) unless
+// S + a is exactly halfway between two grid points (ties-to-even then depends
+// on S's last bit).  So per chunk of kFoldCh addends and per candidate binade
+// e, k_fold_cand sums the integers RN_u(a)/u (a tie, a negative / NaN addend
+// or a term >= 2^53 marks the candidate unusable), and k_fold_walk advances S
+// over whole chunks as long as it provably stays in its binade; a chunk where
+// S crosses into the next binade (a few per log), a tie, or S = 0 is folded
+// addend by addend.  The logs are zero-padded to whole chunks (S + 0 = S).
+constexpr int kFoldCh = 2048;
+constexpr int kFoldE0 = -30;  // candidate binades e = kFoldE0 .. kFoldE0 + 63
+constexpr uint64_t kFoldBad = ~0ull;
+
+struct SegDev {  // a segmented device: its OUT tasks and its three log ranges
+    uint32_t dev, t0, t1, pad;
+    uint64_t lbase[3], lcnt[3];  // lcnt padded to kFoldCh
+};
+
+__global__ void __launch_bounds__(128) k_fold_cand(const double* __restrict__ log, uint64_t nchunks,
+                                                   uint64_t* __restrict__ cand) {
+    const uint64_t c = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (c >= nchunks) return;
+    const double sc0 = ldexp(1.0, 52 - (kFoldE0 + static_cast<int>(lane)));
+    const double sc1 = ldexp(1.0, 52 - (kFoldE0 + 32 + static_cast<int>(lane)));
+    uint64_t acc0 = 0, acc1 = 0;
+    bool bad0 = false, bad1 = false;
+    const double* p = log + c * kFoldCh;
+    auto term = [](double x, double sc, uint64_t& acc, bool& bad) {
+        if (!(x >= 0.0)) {
+            bad = true;
+            return;
+        }
+        const double xs = x * sc;  // exact (power-of-two scaling, no overflow in range)
+        if (xs >= 9007199254740992.0) {
+            bad = true;
+            return;
+        }
+        const double fl = floor(xs), fr = xs - fl;  // both exact below 2^53
+        if (fr == 0.5) bad = true;
+        acc += static_cast<uint64_t>(fl) + (fr > 0.5 ? 1u : 0u);
+    };
+    for (int i = 0; i < kFoldCh; i += 32) {
+        const double v = p[i + lane];
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) {
+            const double x = __shfl_sync(kFullMask, v, t);
+            term(x, sc0, acc0, bad0);
+            term(x, sc1, acc1, bad1);
+        }
+    }
+    cand[c * 64 + lane] = bad0 ? kFoldBad : acc0;
+    cand[c * 64 + 32 + lane] = bad1 ? kFoldBad : acc1;
+}
+
+// one warp per (segmented device, log): S over its chunks (see above)
+__global__ void __launch_bounds__(32) k_fold_walk(const SegDev* __restrict__ devs, const double* const* logs,
+                                                  const uint64_t* const* cands, double* __restrict__ out) {
+    __shared__ alignas(16) double buf[128];
+    const uint32_t r = blockIdx.x, lane = threadIdx.x;
+    const SegDev& sd = devs[r / 3];
+    const int k = static_cast<int>(r % 3);
+    const double* lg = logs[k];
+    const uint64_t* cd = cands[k];
+    const uint64_t c0 = sd.lbase[k] / kFoldCh, c1 = c0 + sd.lcnt[k] / kFoldCh;
+    double S = 0.0;
+    uint64_t c = c0;
+    while (c < c1) {
+        int e = 0;
+        bool whole = false;
+        if (S > 0.0) {
+            e = ilogb(S);
+            whole = e >= kFoldE0 && e < kFoldE0 + 64;
+        }
+        uint32_t took = 0;
+        if (whole) {  // as many whole chunks as stay in S's binade
+            const uint32_t idx = static_cast<uint32_t>(e - kFoldE0);
+            const double u = ldexp(1.0, e - 52);
+            const uint64_t m = static_cast<uint64_t>(S / u);  // S's significand, in [2^52, 2^53)
+            const uint64_t room = (1ull << 53) - m;          // S + T*u < 2^(e+1)  <=>  T < room
+            const uint64_t cc = c + lane;
+            uint64_t t = cc < c1 ? cd[cc * 64 + idx] : kFoldBad;
+            bool ok = t != kFoldBad;
+            uint64_t pre = ok ? t : 0;  // inclusive prefix, saturating at 2^53
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint64_t y = __shfl_up_sync(kFullMask, pre, s);
+                const bool yo = __shfl_up_sync(kFullMask, ok, s);
+                if (lane >= static_cast<uint32_t>(s)) {
+                    pre = min(pre + y, static_cast<uint64_t>(1ull << 53));
+                    ok = ok && yo;
+                }
+            }
+            ok = ok && pre < room;
+            took = __popc(__ballot_sync(kFullMask, ok));  // leading lanes (ok is monotone)
+            if (took) {
+                const uint64_t T = __shfl_sync(kFullMask, pre, took - 1);
+                S = S + static_cast<double>(T) * u;  // exact: a multiple of u below 2^(e+1)
+                c += took;
+            }
+        }
+        if (!took) {  // addend by addend
+            const double* p = lg + c * kFoldCh;
+            for (int i = 0; i < kFoldCh; i += 128) {
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 4; ++q) buf[q * 32 + lane] = p[i + q * 32 + lane];
+                __syncwarp();
+                if (lane == 0) S = chain_fold(S, buf, 128);
+                S = __shfl_sync(kFullMask, S, 0);
+            }
+            ++c;
+        }
+    }
+    if (lane == 0) out[r] = S;
+}
+
+// one warp per segmented device: its OUT segments' partial reports -> the report
+__global__ void __launch_bounds__(32) k_seg_combine(const __grid_constant__ CoParams P, const SegDev* __restrict__ devs,
+                                                    const double* __restrict__ folds) {
+    const SegDev& sd = devs[blockIdx.x];
+    const uint32_t lane = threadIdx.x;
+    uint64_t gen = 0, trained = 0, peak = 0, ptab = 0, pre = 0, freed = 0, loads = 0, recomp = 0, dropped = 0, jobs = 0,
+             fb = 0, oom = 0, batches = 0, maxb = 0, offd = 0, adm = 0, slow = 0, slowq = 0, njobs = 0;
+    uint64_t acc[3] = {0, 0, 0};
+    uint64_t flags = 0;
+    double end = 0.0;
+    for (uint32_t t = sd.t0 + lane; t < sd.t1; t += 32) {
+        const colo_colocated_summary& s = P.segout[t].s;
+        gen += s.generated_tokens;
+        trained += s.trained_tokens;
+        peak = max(peak, s.peak_device_bytes);
+        ptab = max(ptab, s.peak_training_activation_bytes);
+        pre += s.preemptions;
+        freed += s.layers_freed;
+        loads += s.loads;
+        recomp += s.recomputes;
+        dropped += s.labels_dropped;
+        jobs += s.completed_jobs;
+        fb += s.map_fallbacks;
+        oom += s.oom_jobs;
+        batches += s.batches;
+        maxb = max(maxb, s.max_batch_size);
+        offd += s.offload_decisions;
+        adm += s.admissions;
+        slow += s.slow_tokens;
+        slowq += s.slow_queries;
+        end = dmax(end, s.end_time);
+        add3(acc, s.tpt_sum[0], s.tpt_sum[1], s.tpt_sum[2]);
+        flags |= s.flags;
+        njobs += P.segout[t].jobs;
+    }
+    gen = warp_sum_u64(gen);
+    trained = warp_sum_u64(trained);
+    peak = warp_max_u64(peak);
+    ptab = warp_max_u64(ptab);
+    pre = warp_sum_u64(pre);
+    freed = warp_sum_u64(freed);
+    loads = warp_sum_u64(loads);
+    recomp = warp_sum_u64(recomp);
+    dropped = warp_sum_u64(dropped);
+    jobs = warp_sum_u64(jobs);
+    fb = warp_sum_u64(fb);
+    oom = warp_sum_u64(oom);
+    batches = warp_sum_u64(batches);
+    maxb = warp_max_u64(maxb);
+    offd = warp_sum_u64(offd);
+    adm = warp_sum_u64(adm);
+    slow = warp_sum_u64(slow);
+    slowq = warp_sum_u64(slowq);
+    njobs = warp_sum_u64(njobs);
+    end = warp_max_f64(end);
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint64_t b0 = __shfl_xor_sync(kFullMask, acc[0], s), b1 = __shfl_xor_sync(kFullMask, acc[1], s),
+                       b2 = __shfl_xor_sync(kFullMask, acc[2], s);
+        add3(acc, b0, b1, b2);
+        flags |= __shfl_xor_sync(kFullMask, flags, s);
+    }
+    if (lane) return;
+    if (P.job_cnt) P.job_cnt[sd.dev] = njobs;
+    if (!P.summary) return;
+    colo_colocated_summary r;
+    r.generated_tokens = gen;
+    r.trained_tokens = trained;
+    r.training_busy_time = folds[blockIdx.x * 3 + 0];
+    r.peak_device_bytes = peak;
+    r.peak_training_activation_bytes = ptab;
+    r.preemptions = pre;
+    r.layers_freed = freed;
+    r.loads = loads;
+    r.recomputes = recomp;
+    r.copy_stall_seconds = folds[blockIdx.x * 3 + 1];
+    r.labels_dropped = dropped;
+    r.prefetch_wait_seconds = folds[blockIdx.x * 3 + 2];
+    r.completed_jobs = jobs;
+    r.map_fallbacks = fb;
+    r.oom_jobs = oom;
+    r.batches = batches;
+    r.max_batch_size = maxb;
+    r.offload_decisions = offd;
+    r.admissions = adm;
+    r.slow_tokens = slow;
+    r.slow_queries = slowq;
+    r.end_time = end;
+    r.status = COLO_OK;
+    r.tpt_sum[0] = acc[0];
+    r.tpt_sum[1] = acc[1];
+    r.tpt_sum[2] = acc[2];
+    r.flags = flags;
+    P.summary[sd.dev] = r;
+}
+
 size_t align256c(size_t x) { return (x + 255) & ~size_t(255); }
 
 colo_status grow_scratch(colo_ctx* ctx, size_t bytes) {
@@ -1115,6 +1505,320 @@ colo_status grow_scratch(colo_ctx* ctx, size_t bytes) {
     ctx->rscratch_bytes = 0;
     COLO_CK(ctx, cudaMalloc(&ctx->d_rscratch, bytes));
     ctx->rscratch_bytes = bytes;
+    return COLO_OK;
+}
+
+colo_status grow_buf(colo_ctx* ctx, void*& p, size_t& cap, size_t bytes) {
+    if (cap >= bytes) return COLO_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    COLO_CK(ctx, cudaMalloc(&p, bytes));
+    cap = bytes;
+    return COLO_OK;
+}
+
+colo_status launch_co(colo_ctx* ctx, const CoParams& Q, size_t nwarps, int& flag) {
+    COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
+    const uint32_t blocks = static_cast<uint32_t>((nwarps + kWarpsC - 1) / kWarpsC);
+    k_colocated<<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
+    COLO_CK(ctx, cudaGetLastError());
+    COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return COLO_OK;
+}
+
+// Every device's run: one warp per device, or -- when there are too few
+// devices to fill the GPU -- long devices in parallel segments (see SegTask):
+// speculate, resolve the entry arrivals here, replay the segments with their
+// outputs, fold the f64 sums, combine the partial reports.  A device whose
+// segments do not resolve (no common idle arrival, e.g. a server that never
+// drains) or whose replay breaches runs whole.  seg_len: 0 = automatic,
+// 0xffffffff = never, else the segment length in queries.
+colo_status run_devices(colo_ctx* ctx, CoParams P, const std::vector<uint64_t>& off,
+                        const std::vector<uint8_t>& smode, size_t n, uint32_t seg_len, int& flag) {
+    const size_t ndev = P.ndev;
+    flag = 0;
+    const size_t W = static_cast<size_t>(std::max(ctx->sm_count, 1)) * 8;  // resident warps
+    uint64_t L = 0;
+    if (seg_len == 0) {
+        if (ndev < W) L = std::max<uint64_t>(512, (n + 4 * W - 1) / (4 * W));
+    } else if (seg_len != 0xffffffffu) {
+        L = seg_len;
+    }
+    std::vector<uint32_t> sdevs;
+    for (size_t d = 0; L && d < ndev; ++d) {
+        const uint64_t nd = off[d + 1] - off[d];
+        if (seg_len == 0 ? nd >= 4 * L : nd > L) sdevs.push_back(static_cast<uint32_t>(d));
+    }
+    if (sdevs.empty()) return launch_co(ctx, P, ndev, flag);
+
+    // ---- speculate ----
+    const uint64_t ext = std::max<uint64_t>(L, 2048);
+    std::vector<SegTask> t1;
+    std::vector<size_t> sfirst(sdevs.size());
+    std::vector<char> isseg(ndev, 0);
+    bool seg_separate = false;
+    for (size_t i = 0; i < sdevs.size(); ++i) {
+        const uint32_t d = sdevs[i];
+        const uint64_t nd = off[d + 1] - off[d];
+        isseg[d] = 1;
+        seg_separate |= smode[d] == COLO_SIM_SEPARATE;
+        sfirst[i] = t1.size();
+        for (uint64_t s0 = 0; s0 < nd; s0 += L) {
+            SegTask t{};
+            t.dev = d;
+            t.mode = TM_SPEC;
+            t.start = s0;
+            t.next = std::min(nd, s0 + L);
+            t.xend = t.next < nd ? std::min(nd, t.next + ext) : nd;
+            t1.push_back(t);
+        }
+    }
+    const size_t nspec = t1.size();
+    for (size_t d = 0; d < ndev; ++d)
+        if (!isseg[d]) {
+            SegTask t{};
+            t.dev = static_cast<uint32_t>(d);
+            t.mode = TM_DIRECT;
+            t1.push_back(t);
+        }
+    const size_t nsd = sdevs.size();
+    const size_t maxt = nspec + ndev;
+    size_t b = 0;
+    const size_t o_task = b;
+    b += align256c(maxt * sizeof(SegTask));
+    const size_t o_spec = b;
+    b += align256c(nspec * sizeof(SegSpec));
+    const size_t o_out = b;
+    b += align256c(nspec * sizeof(SegOut));
+    const size_t o_sdv = b;
+    b += align256c(nsd * sizeof(SegDev));
+    const size_t o_fold = b;
+    b += align256c(nsd * 3 * sizeof(double));
+    const size_t o_ptr = b;
+    b += align256c(6 * sizeof(void*));
+    {
+        const colo_status st = grow_buf(ctx, ctx->d_seg, ctx->seg_bytes, b);
+        if (st != COLO_OK) return st;
+    }
+    auto* base = static_cast<uint8_t*>(ctx->d_seg);
+    auto* d_task = reinterpret_cast<SegTask*>(base + o_task);
+    auto* d_spec = reinterpret_cast<SegSpec*>(base + o_spec);
+    auto* d_out = reinterpret_cast<SegOut*>(base + o_out);
+    auto* d_sdv = reinterpret_cast<SegDev*>(base + o_sdv);
+    auto* d_fold = reinterpret_cast<double*>(base + o_fold);
+    auto* d_ptr = reinterpret_cast<void**>(base + o_ptr);
+    COLO_CK(ctx, cudaMemcpyAsync(d_task, t1.data(), t1.size() * sizeof(SegTask), cudaMemcpyHostToDevice, ctx->stream));
+    CoParams P1 = P;
+    P1.tasks = d_task;
+    P1.ntasks = static_cast<uint32_t>(t1.size());
+    P1.spec = d_spec;
+    int f1 = 0;
+    {
+        const colo_status st = launch_co(ctx, P1, t1.size(), f1);
+        if (st != COLO_OK) return st;
+    }
+    std::vector<SegSpec> sp(nspec);
+    COLO_CK(ctx, cudaMemcpyAsync(sp.data(), d_spec, nspec * sizeof(SegSpec), cudaMemcpyDeviceToHost, ctx->stream));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+
+    // ---- resolve: b_0 = 0, b_j = first arrival idle in tail(j-1) and head(j) ----
+    std::vector<SegTask> t2;
+    std::vector<SegDev> sdv;
+    std::vector<uint32_t> whole;
+    uint64_t LB[3] = {0, 0, 0};
+    for (size_t i = 0; i < nsd; ++i) {
+        const uint32_t d = sdevs[i];
+        const uint64_t nd = off[d + 1] - off[d];
+        const SegSpec* S = sp.data() + sfirst[i];
+        const size_t ns = static_cast<size_t>((nd + L - 1) / L);
+        std::vector<uint64_t> bj(ns, 0);
+        std::vector<SegPoint> ph(ns), pt(ns);
+        bool ok = !S[0].err && S[0].nhead > 0 && S[0].head[0].idx == 0;
+        if (ok) ph[0] = S[0].head[0];
+        size_t used = ns;  // segments that replay (the last one may run to the end of the trace)
+        for (size_t j = 1; ok && j < ns; ++j) {
+            const SegSpec &A = S[j - 1], &B = S[j];
+            if (A.end.idx == nd && !A.err) {
+                // segment j-1's own run reached the end of the trace: it is the truth up to there
+                used = j;
+                break;
+            }
+            if (B.err) {
+                ok = false;
+                break;
+            }
+            uint32_t ia = 0, ib = 0;
+            bool found = false;
+            while (ia < A.ntail && ib < B.nhead) {
+                if (A.tail[ia].idx == B.head[ib].idx) {
+                    found = true;
+                    break;
+                }
+                if (A.tail[ia].idx < B.head[ib].idx) ++ia;
+                else ++ib;
+            }
+            if (!found) {
+                ok = false;
+                break;
+            }
+            bj[j] = B.head[ib].idx;
+            pt[j - 1] = A.tail[ia];
+            ph[j] = B.head[ib];
+        }
+        if (ok) {
+            const SegPoint& E = S[used - 1].end;
+            if (E.idx != nd) ok = false;
+            else pt[used - 1] = E;
+        }
+        if (!ok) {
+            if (std::getenv("COLO_SEG_DEBUG")) {
+                size_t j = 0;
+                while (j < ns && !S[j].err) ++j;
+                std::fprintf(stderr, "seg dev %u: %zu segments, unresolved; first err seg %zu\n", d, ns, j);
+                for (size_t q = ns > 4 ? ns - 3 : 0; q < ns; ++q) {
+                    std::fprintf(stderr, "  seg %zu err %u nhead %u ntail %u end %llu head:", q, S[q].err, S[q].nhead,
+                                 S[q].ntail, static_cast<unsigned long long>(S[q].end.idx));
+                    for (uint32_t h = 0; h < std::min<uint32_t>(S[q].nhead, 8); ++h)
+                        std::fprintf(stderr, " %llu", static_cast<unsigned long long>(S[q].head[h].idx));
+                    std::fprintf(stderr, " tail:");
+                    for (uint32_t h = 0; h < std::min<uint32_t>(S[q].ntail, 8); ++h)
+                        std::fprintf(stderr, " %llu", static_cast<unsigned long long>(S[q].tail[h].idx));
+                    std::fprintf(stderr, "\n");
+                }
+            }
+            whole.push_back(d);
+            continue;
+        }
+        SegDev sd{};
+        sd.dev = d;
+        sd.t0 = static_cast<uint32_t>(t2.size());
+        uint64_t bb = 0, jb = 0, sb = 0, lb[3] = {LB[0], LB[1], LB[2]};
+        for (size_t j = 0; j < used; ++j) {
+            SegTask t{};
+            t.dev = d;
+            t.mode = TM_OUT;
+            t.start = bj[j];
+            t.next = j + 1 < used ? bj[j + 1] : nd;
+            t.batch_base = bb;
+            t.job_base = jb;
+            t.sample_base = sb;
+            t.expect[0] = pt[j].batches - ph[j].batches;
+            t.expect[1] = pt[j].jobs - ph[j].jobs;
+            for (int k = 0; k < 3; ++k) {
+                t.log_base[k] = lb[k];
+                t.expect[2 + k] = pt[j].nlog[k] - ph[j].nlog[k];
+                lb[k] += t.expect[2 + k];
+            }
+            bb += t.expect[0];
+            jb += t.expect[1];
+            sb += pt[j].samples - ph[j].samples;
+            t2.push_back(t);
+        }
+        sd.t1 = static_cast<uint32_t>(t2.size());
+        for (int k = 0; k < 3; ++k) {
+            sd.lbase[k] = LB[k];
+            sd.lcnt[k] = (lb[k] - LB[k] + kFoldCh - 1) / kFoldCh * kFoldCh;
+            LB[k] += sd.lcnt[k];
+        }
+        sdv.push_back(sd);
+    }
+    for (uint32_t d : whole) {
+        SegTask t{};
+        t.dev = d;
+        t.mode = TM_DIRECT;
+        t2.push_back(t);
+    }
+
+    // ---- replay the segments with outputs ----
+    const size_t nlog = LB[0] + LB[1] + LB[2], nch = nlog / kFoldCh;
+    {
+        const colo_status st =
+            grow_buf(ctx, ctx->d_seglog, ctx->seglog_bytes, std::max<size_t>(nlog * 8 + nch * 64 * 8, 256));
+        if (st != COLO_OK) return st;
+    }
+    auto* logs = static_cast<double*>(ctx->d_seglog);
+    auto* cands = reinterpret_cast<uint64_t*>(logs + nlog);
+    if (nlog) COLO_CK(ctx, cudaMemsetAsync(logs, 0, nlog * 8, ctx->stream));
+    const double* lp[3] = {logs, logs + LB[0], logs + LB[0] + LB[1]};
+    const uint64_t* cp[3] = {cands, cands + LB[0] / kFoldCh * 64, cands + (LB[0] + LB[1]) / kFoldCh * 64};
+    const void* ptrs[6] = {lp[0], lp[1], lp[2], cp[0], cp[1], cp[2]};
+    COLO_CK(ctx, cudaMemcpyAsync(d_ptr, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, ctx->stream));
+    if (!sdv.empty())
+        COLO_CK(ctx, cudaMemcpyAsync(d_sdv, sdv.data(), sdv.size() * sizeof(SegDev), cudaMemcpyHostToDevice, ctx->stream));
+    int f2 = 0;
+    CoParams P2 = P;
+    if (!t2.empty()) {
+        COLO_CK(ctx, cudaMemcpyAsync(d_task, t2.data(), t2.size() * sizeof(SegTask), cudaMemcpyHostToDevice, ctx->stream));
+        P2.tasks = d_task;
+        P2.ntasks = static_cast<uint32_t>(t2.size());
+        P2.segout = d_out;
+        for (int k = 0; k < 3; ++k) P2.log[k] = const_cast<double*>(lp[k]);
+        const colo_status st = launch_co(ctx, P2, t2.size(), f2);
+        if (st != COLO_OK) return st;
+    }
+    if (f2 & 16) {
+        if (std::getenv("COLO_SEG_DEBUG")) {
+            std::vector<SegOut> so(t2.size());
+            cudaMemcpy(so.data(), d_out, t2.size() * sizeof(SegOut), cudaMemcpyDeviceToHost);
+            int shown = 0;
+            for (size_t t = 0; t < t2.size() && shown < 6; ++t) {
+                if (t2[t].mode != TM_OUT || !so[t].err) continue;
+                ++shown;
+                const SegTask& k = t2[t];
+                std::fprintf(stderr,
+                             "out task %zu dev %u [%llu, %llu) err %llu: batches %llu/%llu jobs %llu/%llu log %llu/%llu "
+                             "%llu/%llu %llu/%llu\n",
+                             t, k.dev, (unsigned long long)k.start, (unsigned long long)k.next,
+                             (unsigned long long)so[t].err, (unsigned long long)so[t].s.batches,
+                             (unsigned long long)k.expect[0], (unsigned long long)so[t].jobs,
+                             (unsigned long long)k.expect[1], (unsigned long long)so[t].nlog[0],
+                             (unsigned long long)k.expect[2], (unsigned long long)so[t].nlog[1],
+                             (unsigned long long)k.expect[3], (unsigned long long)so[t].nlog[2],
+                             (unsigned long long)k.expect[4]);
+            }
+        }
+        return set_err(ctx, COLO_ECUDA, "colocated replay: a segment disagreed with its speculation (internal)");
+    }
+    if (!sdv.empty()) {
+        for (int k = 0; k < 3; ++k) {
+            const uint64_t c = LB[k] / kFoldCh;
+            if (c) k_fold_cand<<<static_cast<uint32_t>((c * 32 + 127) / 128), 128, 0, ctx->stream>>>(lp[k], c,
+                                                                                                   const_cast<uint64_t*>(cp[k]));
+        }
+        k_fold_walk<<<static_cast<uint32_t>(sdv.size() * 3), 32, 0, ctx->stream>>>(
+            d_sdv, reinterpret_cast<const double* const*>(d_ptr), reinterpret_cast<const uint64_t* const*>(d_ptr + 3),
+            d_fold);
+        k_seg_combine<<<static_cast<uint32_t>(sdv.size()), 32, 0, ctx->stream>>>(P2, d_sdv, d_fold);
+        COLO_CK(ctx, cudaGetLastError());
+    }
+    int f3 = 0;
+    if (f2 & 8) {  // a segment breached: those devices run whole (the report stops at the breach)
+        std::vector<SegOut> so(t2.size());
+        COLO_CK(ctx, cudaMemcpyAsync(so.data(), d_out, t2.size() * sizeof(SegOut), cudaMemcpyDeviceToHost, ctx->stream));
+        COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+        std::vector<SegTask> t3;
+        for (const SegDev& sd : sdv) {
+            bool br = false;
+            for (uint32_t t = sd.t0; t < sd.t1; ++t) br |= so[t].s.status == COLO_EBREACH;
+            if (br) {
+                SegTask t{};
+                t.dev = sd.dev;
+                t.mode = TM_DIRECT;
+                t3.push_back(t);
+            }
+        }
+        COLO_CK(ctx, cudaMemcpyAsync(d_task, t3.data(), t3.size() * sizeof(SegTask), cudaMemcpyHostToDevice, ctx->stream));
+        CoParams P3 = P;
+        P3.tasks = d_task;
+        P3.ntasks = static_cast<uint32_t>(t3.size());
+        const colo_status st = launch_co(ctx, P3, t3.size(), f3);
+        if (st != COLO_OK) return st;
+    }
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    flag = f1 | (f2 & ~8) | f3;
+    if (seg_separate) flag |= 4;  // enqueue order across segments is not checked: sort (stable, so exact)
     return COLO_OK;
 }
 
@@ -1237,11 +1941,10 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     if (flag)
         return set_err(ctx, COLO_EVALIDATION,
                        "trace rejected: unsorted arrivals, zero tokens, or a query that cannot fit the device alone");
-    const uint32_t blocks = static_cast<uint32_t>((ndev + kWarpsC - 1) / kWarpsC);
-    k_colocated<<<blocks, kWarpsC * 32, 0, ctx->stream>>>(P);
-    COLO_CK(ctx, cudaGetLastError());
-    COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    {
+        const colo_status st = run_devices(ctx, P, off, smode, n, opts->seg_len, flag);
+        if (st != COLO_OK) return st;
+    }
     if (any_separate && P.summary) {
         const double* jt = P.job_t;
         const uint32_t* jq = P.job_q;

@@ -29,6 +29,10 @@ struct colo_ctx {
     size_t satpool_bytes = 0;
     void* d_dtab = nullptr;         // serving replay: decode-latency tables (lazily grown)
     size_t dtab_bytes = 0;
+    void* d_seg = nullptr;          // colocated replay: segment tasks / idle lists / partial reports (lazily grown)
+    size_t seg_bytes = 0;
+    void* d_seglog = nullptr;       // colocated replay: the segments' f64 addend logs (lazily grown)
+    size_t seglog_bytes = 0;
     // serving replay: identity of the last full replay whose segment entry
     // states are still in d_rscratch (reuse_entries); any other d_rscratch
     // user clears rs_valid

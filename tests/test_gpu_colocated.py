@@ -86,7 +86,11 @@ def batches_of(raw, lo, nb):
     return b
 
 
-def test_golden_each_case(ctx, gold):
+SEG = [None, 16]  # automatic (these traces are short: one warp per device), and forced 16-query segments
+
+
+@pytest.mark.parametrize("seg", SEG)
+def test_golden_each_case(ctx, gold, seg):
     for name in gold["names"]:
         m, g, grid, cpa, to, a, p, o, ld, rep, sim = case(gold, name)
         ms = mapset(ctx, m, g, grid, cpa)
@@ -96,11 +100,12 @@ def test_golden_each_case(ctx, gold):
         sm = cs.SimMode.parse(sim)
         if rc == 3:
             with pytest.raises(cs.ColoBreachError) as ei:
-                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to, sim_mode=sm)
+                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to, sim_mode=sm,
+                                    seg_len=seg)
             assert cs.colocated_summaries(ei.value.result["summary"])[0]["status"] == 3, name
             continue
         r = cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=to, samples=True,
-                                batches=True, sim_mode=sm)
+                                batches=True, sim_mode=sm, seg_len=seg)
         s = cs.colocated_summaries(r["summary"])[0]
         assert s["status"] == 0
         assert not diff(s, rep), (name, diff(s, rep))
@@ -120,7 +125,8 @@ def cs_bit(name):
     return {"EVALUATED": 1 << 25, "ADMITTED": 1 << 26}[name]
 
 
-def test_golden_one_launch_many_devices(ctx, gold):
+@pytest.mark.parametrize("seg", SEG)
+def test_golden_one_launch_many_devices(ctx, gold, seg):
     """All timeout-60 non-breach fixture cases as devices of ONE launch, each
     with its own map set (profiles, grids, modes mixed), devices replicated so
     several warps share CTAs; every device's slice must equal its fixture."""
@@ -139,7 +145,7 @@ def test_golden_one_launch_many_devices(ctx, gold):
     dset = torch.tensor([d[1] for d in devs], dtype=torch.int16, device="cuda")
     dmode = torch.tensor([d[3] for d in devs], dtype=torch.uint8, device="cuda")
     r = cs.replay_colocated(ctx, sets, da, dp, do, doff, dset, label_delay=dld, samples=True, batches=True,
-                            sim_mode=dmode)
+                            sim_mode=dmode, seg_len=seg)
     S = cs.colocated_summaries(r["summary"])
     smp = r["samples"].cpu().numpy()
     so = r["sample_offsets"].cpu().numpy()
@@ -150,7 +156,8 @@ def test_golden_one_launch_many_devices(ctx, gold):
         assert np.array_equal(b["start"].view(np.uint64), gold[f"{n}_batches"][:, 0].view(np.uint64)), n
 
 
-def test_vs_oracle_random(ctx, orc):
+@pytest.mark.parametrize("seg", SEG)
+def test_vs_oracle_random(ctx, orc, seg):
     """Fresh traces (variable outputs, label delays, odd GPU profiles): the
     kernel equals the restatement on every field, sample, label and batch."""
     rng = np.random.default_rng(77)
@@ -178,10 +185,11 @@ def test_vs_oracle_random(ctx, orc):
         dset = torch.zeros(1, dtype=torch.int16, device="cuda")
         if ref["rc"] == 3:
             with pytest.raises(cs.ColoBreachError):
-                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=30.0, tau=0.05)
+                cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=30.0, tau=0.05,
+                                    seg_len=seg)
             continue
         r = cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, cache_timeout=30.0, tau=0.05,
-                                samples=True, batches=True)
+                                samples=True, batches=True, seg_len=seg)
         s = cs.colocated_summaries(r["summary"])[0]
         assert not diff(s, ref["report"]), (it, diff(s, ref["report"]))
         for f in ("batches", "max_batch_size", "offload_decisions", "admissions", "slow_tokens", "slow_queries"):
@@ -244,7 +252,8 @@ def test_colocated_stats_exact(ctx, gold, orc):
     assert tot["generated_tokens"] == len(u)
 
 
-def test_modes_vs_oracle_random(ctx, orc):
+@pytest.mark.parametrize("seg", SEG)
+def test_modes_vs_oracle_random(ctx, orc, seg):
     """ServingOnly and SeparateCluster devices (constant, varying and absent
     label delays: the sorted job-stream path) mixed with Colocated devices in
     one launch; every device equals the restatement."""
@@ -276,7 +285,7 @@ def test_modes_vs_oracle_random(ctx, orc):
         refs.append(ref)
     da, dp, do, dld, doff, off = upload(traces)
     r = cs.replay_colocated(ctx, sets, da, dp, do, doff, torch.tensor(dset, dtype=torch.int16, device="cuda"),
-                            label_delay=dld, tau=0.05, samples=True,
+                            label_delay=dld, tau=0.05, samples=True, batches=True, seg_len=seg,
                             sim_mode=torch.tensor(dmode, dtype=torch.uint8, device="cuda"))
     S = cs.colocated_summaries(r["summary"])
     smp = r["samples"].cpu().numpy()
@@ -286,4 +295,38 @@ def test_modes_vs_oracle_random(ctx, orc):
         assert not diff(S[i], ref["report"]), (i, dmode[i], diff(S[i], ref["report"]))
         assert np.array_equal(smp[so[i]:so[i + 1]].view(np.uint64), ref["samples"].view(np.uint64)), i
         assert np.array_equal(lab[off[i]:off[i + 1]], ref["labels"]), i
+        b = batches_of(r["batches"], int(off[i]), S[i]["batches"])
+        for k in ("start", "end", "first", "n"):
+            assert np.array_equal(b[k], ref["batches"][k]), (i, k)
     assert len(refs) >= 30 and {0, 1, 2} <= set(dmode)
+
+
+@pytest.mark.parametrize("qps,cpa", [(0.3, 1), (0.1, 0), (1.7, 1)])
+def test_segmented_long_trace(ctx, orc, qps, cpa):
+    """One long device (the C1 shape, 60k queries): the automatic segmented
+    replay (speculate / resolve / replay segments, exact folds of the three
+    f64 sums) equals the one-warp replay and the restatement on every report
+    field, sample, label and batch.  At 1.7 QPS the server never drains, no
+    segment resolves and the device runs whole."""
+    hv, hp = sharegpt_histogram()
+    m, g, grid = default_model(), default_gpu(), default_grid()
+    a, p, o, ld = orc.generate_trace(qps, 60000 / qps, ("histogram", hv, hp), 41, ("fixed", 0.01), with_labels=True)
+    ref = orc.replay_colocated(m, g, grid, cpa, a, p, o, ld, 60.0, tau=0.05)
+    ms = mapset(ctx, m, g, grid, cpa)
+    da, dp, do, dld, doff, off = upload([(a, p, o, ld)])
+    dset = torch.zeros(1, dtype=torch.int16, device="cuda")
+    outs = []
+    for seg in (None, 0, 1000):
+        r = cs.replay_colocated(ctx, [ms], da, dp, do, doff, dset, label_delay=dld, tau=0.05, samples=True,
+                                batches=True, seg_len=seg)
+        s = cs.colocated_summaries(r["summary"])[0]
+        assert not diff(s, ref["report"]), (seg, diff(s, ref["report"]))
+        for f in ("batches", "max_batch_size", "offload_decisions", "admissions", "slow_tokens", "slow_queries"):
+            assert s[f] == ref["report"][f], (seg, f)
+        assert np.array_equal(r["samples"].cpu().numpy().view(np.uint64), ref["samples"].view(np.uint64)), seg
+        assert np.array_equal(r["labels"].cpu().numpy(), ref["labels"]), seg
+        b = batches_of(r["batches"], 0, s["batches"])
+        for k in ("start", "end", "first", "n", "need_total", "max_incoming"):
+            assert np.array_equal(b[k], ref["batches"][k]), (seg, k)
+        outs.append(b["verdict"].copy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
