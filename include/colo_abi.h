@@ -436,6 +436,13 @@ uint64_t colo_trace_hash(const uint64_t* query_id, const double* arrival, const 
  * finalize / export_tpt_cdf, metrics.hpp:59-60, 280-288).  d_in and d_out may
  * not alias.  Synchronous. */
 colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size_t n);
+/* finalize (metrics.hpp:56-69) of n TPT samples on the device, bit-exact:
+ * out[0..2] nearest-rank p50/p90/p99 of the ascending sort, out[3] the mean as
+ * the reference computes it -- the strictly sequential sum of the sorted
+ * samples, divided by n (an exact parallel evaluation of that left fold;
+ * NaN for n = 0).  d_sorted (may be NULL) receives the sorted samples.
+ * Synchronous. */
+colo_status colo_finalize(colo_ctx* ctx, const double* d_samples, size_t n, double* d_sorted, double* out);
 /* n doubles formatted as nlohmann::json::dump() writes them (the reference's
  * report serializer, metrics.hpp:191-226), comma-separated, NUL-terminated
  * into out when cap exceeds the length.  Returns the length (without NUL). */

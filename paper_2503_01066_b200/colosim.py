@@ -893,6 +893,25 @@ def colocated_summaries(summary_bytes) -> list:
     return out
 
 
+def finalize(ctx: Context, samples, sorted_out=None) -> list:
+    """colo_finalize: finalize (metrics.hpp:56-69) of a device tensor of TPT
+    samples, bit-exact -- [p50, p90, p99, mean] with the mean the sequential
+    sum of the ascending-sorted samples / n (NaN when empty).  ``sorted_out``
+    (optional f64 device tensor of the same length) receives the sorted
+    samples."""
+    _need_cuda(samples, "samples", 8)
+    samples = samples.contiguous()
+    n = samples.numel()
+    if sorted_out is not None:
+        _need_cuda(sorted_out, "sorted_out", 8)
+        if sorted_out.numel() != n or not sorted_out.is_contiguous():
+            raise ColoInvalidArgument(_lib.COLO_EINVAL, "sorted_out must be a contiguous tensor of len(samples)")
+    out = (C.c_double * 4)()
+    check(lib().colo_finalize(ctx.h, _ptr(samples) if n else None, n,
+                              _ptr(sorted_out) if (sorted_out is not None and n) else None, out), ctx.h, "finalize")
+    return list(out)
+
+
 def colocated_stats(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                     label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
                     tau: float = math.inf, sim_mode=None, seg_len=None):

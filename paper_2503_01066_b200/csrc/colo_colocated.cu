@@ -2010,6 +2010,56 @@ colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size
     return COLO_OK;
 }
 
+colo_status colo_finalize(colo_ctx* ctx, const double* d_samples, size_t n, double* d_sorted, double* out) {
+    if (!ctx || !out || (n && !d_samples) || (d_sorted && d_sorted == d_samples)) return COLO_EINVAL;
+    for (int i = 0; i < 4; ++i) out[i] = std::nan("");
+    if (n == 0) return COLO_OK;
+    if (n >= (1ull << 31)) return set_err(ctx, COLO_EINVAL, "colo_finalize: at most 2^31-1 samples");
+    COLO_CK(ctx, cudaSetDevice(ctx->device));
+    // sorted values zero-padded to whole fold chunks (S + 0 = S), the fold's
+    // chunk candidates, one SegDev range, the pointer table and the result
+    const size_t nch = (n + kFoldCh - 1) / kFoldCh, npad = nch * kFoldCh;
+    size_t tb = 0;
+    COLO_CK(ctx, cub::DeviceRadixSort::SortKeys(nullptr, tb, d_samples, static_cast<double*>(nullptr),
+                                                static_cast<int>(n), 0, 64, ctx->stream));
+    const size_t o_srt = 0, o_cand = align256c(npad * 8), o_sd = o_cand + align256c(nch * 64 * 8),
+                 o_ptr = o_sd + align256c(sizeof(SegDev)), o_res = o_ptr + 256, o_tmp = o_res + 256;
+    {
+        const colo_status st = grow_buf(ctx, ctx->d_seglog, ctx->seglog_bytes, o_tmp + tb + 256);
+        if (st != COLO_OK) return st;
+    }
+    auto* base = static_cast<uint8_t*>(ctx->d_seglog);
+    auto* srt = reinterpret_cast<double*>(base + o_srt);
+    auto* cand = reinterpret_cast<uint64_t*>(base + o_cand);
+    COLO_CK(ctx, cub::DeviceRadixSort::SortKeys(base + o_tmp, tb, d_samples, srt, static_cast<int>(n), 0, 64,
+                                                ctx->stream));
+    if (npad > n) COLO_CK(ctx, cudaMemsetAsync(srt + n, 0, (npad - n) * 8, ctx->stream));
+    SegDev sd{};
+    sd.lcnt[0] = npad;
+    const void* ptrs[6] = {srt, srt, srt, cand, cand, cand};
+    COLO_CK(ctx, cudaMemcpyAsync(base + o_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, ctx->stream));
+    COLO_CK(ctx, cudaMemcpyAsync(base + o_ptr, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, ctx->stream));
+    k_fold_cand<<<static_cast<uint32_t>((nch * 32 + 127) / 128), 128, 0, ctx->stream>>>(srt, nch, cand);
+    k_fold_walk<<<1, 32, 0, ctx->stream>>>(reinterpret_cast<const SegDev*>(base + o_sd),
+                                          reinterpret_cast<const double* const*>(base + o_ptr),
+                                          reinterpret_cast<const uint64_t* const*>(base + o_ptr + 3 * sizeof(void*)),
+                                          reinterpret_cast<double*>(base + o_res));
+    COLO_CK(ctx, cudaGetLastError());
+    double sum = 0.0, q[3];
+    const double qs[3] = {0.50, 0.90, 0.99};
+    COLO_CK(ctx, cudaMemcpyAsync(&sum, base + o_res, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    for (int i = 0; i < 3; ++i)  // nearest_rank (metrics.hpp:48-53)
+        COLO_CK(ctx, cudaMemcpyAsync(&q[i], srt + colo_nearest_rank_index(qs[i], n) - 1, 8, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    if (d_sorted) COLO_CK(ctx, cudaMemcpyAsync(d_sorted, srt, n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    out[0] = q[0];
+    out[1] = q[1];
+    out[2] = q[2];
+    out[3] = sum / static_cast<double>(n);  // metrics.hpp:63-65
+    return COLO_OK;
+}
+
 colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, size_t nsets, const double* d_arrival,
                                  const uint32_t* d_prompt, const uint32_t* d_output, size_t n,
                                  const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev,

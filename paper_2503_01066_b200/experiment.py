@@ -307,7 +307,10 @@ def finalize_report(r: dict) -> dict:
     x = r["tpt_samples"]
     for k in ("tpt_p50", "tpt_p90", "tpt_p99", "tpt_mean"):
         r[k] = None
-    if len(x):
+    fin = r.pop("_finalized", None)
+    if len(x) and fin is not None:  # computed on the device by colo_finalize (same bits)
+        r["tpt_p50"], r["tpt_p90"], r["tpt_p99"], r["tpt_mean"] = fin
+    elif len(x):
         srt = s if s is not None else np.sort(x)
         n = len(srt)
 
@@ -366,14 +369,15 @@ def run_simulations(ctx: cs.Context, runs: Sequence[Run], sort_on_gpu: bool = Tr
         so = res["sample_offsets"].cpu().numpy()
         smp_dev = res["samples"]
         srt_dev = None
+        fin = {}
         if sort_on_gpu and smp_dev.numel():
             srt_dev = torch.empty_like(smp_dev)
-            # per run: sort its own sample range on the device (colo_sort_f64)
+            # per run: finalize its own sample range on the device (colo_finalize: sort,
+            # nearest ranks, the sequential sum of the sorted samples)
             for k in range(len(batch)):
                 lo_, hi_ = int(so[k]), int(so[k + 1])
                 if hi_ > lo_:
-                    cs.check(lib().colo_sort_f64(ctx.h, C.c_void_p(smp_dev.data_ptr() + 8 * lo_),
-                                                 C.c_void_p(srt_dev.data_ptr() + 8 * lo_), hi_ - lo_), ctx.h, "sort")
+                    fin[k] = cs.finalize(ctx, smp_dev[lo_:hi_], sorted_out=srt_dev[lo_:hi_])
         smp = smp_dev.cpu().numpy()
         srt = srt_dev.cpu().numpy() if srt_dev is not None else None
         for k, i in enumerate(batch):
@@ -383,6 +387,8 @@ def run_simulations(ctx: cs.Context, runs: Sequence[Run], sort_on_gpu: bool = Tr
             rep["tpt_samples"] = smp[so[k]:so[k + 1]].copy()
             if srt is not None:
                 rep["_sorted_for_cdf"] = srt[so[k]:so[k + 1]]
+            if k in fin:
+                rep["_finalized"] = fin[k]
             rep["trace_hash"] = run.trace.content_hash()
             rep["mode_tag"] = f"{_sm_str(run.mode)}/{_tm_str(run.training)}"
             out[i] = finalize_report(rep)
