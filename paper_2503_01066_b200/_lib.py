@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcolo_b200.so")
+LIB_PATH = os.environ.get("COLO_B200_LIB") or os.path.join(HERE, "libcolo_b200.so")  # override: build variants
 
 COLO_OK, COLO_EINVAL, COLO_EVALIDATION, COLO_EBREACH, COLO_ECUDA = range(5)
 STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "EVALIDATION", 3: "EBREACH", 4: "ECUDA"}

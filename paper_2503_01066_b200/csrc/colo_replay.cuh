@@ -68,6 +68,15 @@ __device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, dou
     }
 }
 
+// a -= fixed(s * mult) (mod 2^192; the lane partials are summed mod 2^192 and
+// the total is non-negative)
+__device__ __forceinline__ void acc_fixed_sub(uint64_t (&a)[3], uint32_t& flags, double s, uint32_t mult) {
+    uint64_t t[3] = {0, 0, 0};
+    acc_fixed(t, flags, s, mult);
+    const uint64_t c0 = t[0] == 0, c1 = c0 & (t[1] == 0);
+    add3(a, ~t[0] + 1, ~t[1] + c0, ~t[2] + c1);
+}
+
 // First index >= from whose arrival is > T (or N): every arrival at or before
 // T has been popped by the time the batch starts (engine.hpp:146-147,184-187).
 // Arrivals are sorted, so the warp gallops with 32 probes per step (stride

@@ -45,6 +45,11 @@ namespace {
 constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
+#ifndef COLO_REPLAY_BLOCKS
+#define COLO_REPLAY_BLOCKS 4
+#endif
+constexpr int kReplayBlocks = COLO_REPLAY_BLOCKS;  // resident CTAs per SM the replay pass is compiled for
+constexpr int kTileBytes = kWarps * 32 * 33 * 8;   // k_replay_full's dynamic shared memory
 constexpr unsigned FULL = 0xffffffffu;
 
 struct DevProfile {
@@ -122,6 +127,7 @@ struct ReplayParams {
     uint64_t* sat_seg_start;  // [pseg] first recorded batch (pass 2)
     double* sat_dk;
     uint32_t sat_on;
+    uint32_t singles;  // idle starts 32 at a time (run_batches); COLO_SINGLES=0 turns it off
     unsigned long long* dbg;  // COLO_REPLAY_TIMING: [0] fast-path batches, [1] other batches of the resolve pass
     // decode-step latency table per profile: dtab[pi][x] = gamma + delta * x for
     // every context x < dtab_n (cost_model.hpp:28-35 with batch 1, the same f64
@@ -148,7 +154,7 @@ struct Acc {  // per-warp outputs of RUN_FULL (every lane holds its own partials
 template <int MODE>
 __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, double& T, uint64_t stop,
                             uint64_t seg_start, SpecOut* sp, bool& synced, Acc& A, uint2* sPO, double* sPD,
-                            double* sDK) {
+                            double* sDK, double* sT) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t pi = P.dev_prof[d];
     const colo_model& m = P.prof[pi].m;
@@ -166,6 +172,143 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
         uint64_t tail;
         const double ah = arr[head];
+        if (ah > T && P.singles) {
+            // ---- idle starts, up to 32 at a time -------------------------------
+            // An idle start is a batch of one query that starts at its arrival
+            // (T = arr[q]), so its whole timeline depends on q alone.  Lane l
+            // takes query head+l.  It is the next batch iff every lane before
+            // it is and arr[head+l] > T_end(l-1); the exact-arithmetic decode
+            // time S = o*gamma + delta*(o*p + o(o-1)/2) bounds T_end to within
+            // o rounding steps, so lanes whose arrival clears the bound by that
+            // margin are certain, and the block stops before the first lane
+            // that is not (the sequential loop below takes it).  The batches'
+            // step chains then run one per lane in 32-step windows through a
+            // shared-memory tile, and each batch's samples are post-processed
+            // with lanes = steps, exactly as the per-batch path does.
+            const uint64_t q = head + lane;
+            const bool inr = q < stop && q < N;
+            const uint32_t pq = inr ? pp[q] : 0u, oq = inr ? po[q] : 0u;
+            const double aq = inr ? arr[q] : 0.0;
+            const double tq = static_cast<double>(pq), od = static_cast<double>(oq);
+            const double gam = m.decode_coef_const, del = m.decode_coef_context;
+            // prefill of one member: 0.0 + (lin*t + (quad*t)*t) (cost_model.hpp:18-25)
+            const double t_pre = (aq + 0.0) + (0.0 + (m.prefill_coef_linear * tq + m.prefill_coef_quad * tq * tq));
+            const double S = od * gam + del * (od * tq + 0.5 * od * (od - 1.0));
+            const double est = t_pre + S;
+            const double hi_end = est + (8.0 * od * fabs(est) * 0x1p-52 + 1e-9 * S);
+            const double prev_hi = __shfl_up_sync(FULL, hi_end, 1);
+            const bool fits = inr && (lane == 0 || aq > prev_hi);
+            const uint32_t bad = __ballot_sync(FULL, !fits);
+            const uint32_t nv = bad ? static_cast<uint32_t>(__ffs(bad) - 1) : 32u;  // lanes [0, nv): batches
+            if (MODE == RUN_RESOLVE) {  // stop at the first idle start the speculative run also had
+                const uint32_t rel = static_cast<uint32_t>(q - seg_start);
+                bool hit = false;
+                for (uint32_t i = 0; i < nreg; ++i) hit |= sp->regen[i] == rel;
+                const uint32_t hb = __ballot_sync(FULL, hit && lane < nv);
+                if (hb) {
+                    head += __ffs(hb) - 1;
+                    synced = true;
+                    return;
+                }
+            }
+            if (MODE == RUN_SPEC) {
+                if (lane < nv && ridx + lane < kRegen) sp->regen[ridx + lane] = static_cast<uint32_t>(q - seg_start);
+                ridx += nv;
+            }
+            const bool v = lane < nv;
+            const uint32_t ov = v ? oq : 0u;
+            double now = t_pre, kd = 0.0;
+            if (MODE != RUN_FULL) {
+                for (uint32_t k = 0; k < ov; ++k, kd += 1.0) now = now + (0.0 + (gam + del * (tq + kd)));
+            } else {
+                uint32_t kmax = ov;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) kmax = max(kmax, __shfl_xor_sync(FULL, kmax, s));
+                uint32_t ex = ov;  // sample slots: the batches' samples in batch order
+#pragma unroll
+                for (int s = 1; s < 32; s <<= 1) {
+                    const uint32_t y = __shfl_up_sync(FULL, ex, s);
+                    if (lane >= static_cast<uint32_t>(s)) ex += y;
+                }
+                const uint64_t spos = A.sample_pos + ex - ov;
+                A.sample_pos += __shfl_sync(FULL, ex, 31);
+                // exact TPT sum by telescoping when every step time lies in [t_pre, 2 t_pre]
+                // (each sample T_k - T_{k-1} is then exact, Sterbenz)
+                const bool tl = v && t_pre >= 0x1p-44 && hi_end <= 2.0 * t_pre;
+                if (tl) acc_fixed_sub(A.acc, A.flags, t_pre, 1u);
+                const uint32_t tlm = __ballot_sync(FULL, tl);
+                uint32_t slowm = 0;
+                double* row = sT + lane * 33;
+                for (uint32_t k0 = 0; k0 < kmax; k0 += 32) {
+                    row[0] = now;  // T_{k0-1}
+#pragma unroll 8
+                    for (uint32_t i = 0; i < 32; ++i) {
+                        if (k0 + i < ov) {
+                            now = now + (0.0 + (gam + del * (tq + kd)));
+                            kd += 1.0;
+                        }
+                        row[1 + i] = now;
+                    }
+                    __syncwarp();
+                    for (uint32_t b = 0; b < nv; ++b) {  // batch b's window, lanes = steps
+                        const uint32_t ob = __shfl_sync(FULL, ov, b);
+                        if (k0 >= ob) continue;
+                        const uint32_t k = k0 + lane;
+                        const bool live = k < ob;
+                        const double s = sT[b * 33 + 1 + lane] - sT[b * 33 + lane];
+                        const bool slow = live && s > P.tau;
+                        if (__ballot_sync(FULL, slow)) slowm |= 1u << b;
+                        A.slow_tok += slow;
+                        if (want_hist) {
+                            const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+                            const uint64_t hb = bits >> P.filter_shift;
+                            const uint32_t nf = P.nfilters;
+                            const bool any = live && (hb == P.prefix[0] || (nf > 1 && hb == P.prefix[1]) ||
+                                                      (nf > 2 && hb == P.prefix[2]));
+                            if (__any_sync(FULL, any))
+                                for (uint32_t f = 0; f < nf; ++f)
+                                    hist_add(P.hist,
+                                             f * COLO_HIST_BINS +
+                                                 static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
+                                             1u, live && hb == P.prefix[f]);
+                        }
+                        if (live && !((tlm >> b) & 1u)) acc_fixed(A.acc, A.flags, s, 1u);
+                        const uint64_t sb = __shfl_sync(FULL, spos, b);
+                        if (live && P.samples) P.samples[sb + k] = s;
+                    }
+                    __syncwarp();
+                }
+                if (tl) acc_fixed(A.acc, A.flags, now, 1u);
+                const uint64_t need = v ? serving_memory(m, static_cast<uint64_t>(pq) + oq, 1) : 0ull;
+                if (v) {
+                    const bool slowq = (slowm >> lane) & 1u;  // a lone query's tokens are every step
+                    A.gen += ov;
+                    A.slow_q += slowq;
+                    if (P.labels) P.labels[lo + q] = slowq ? 1 : 0;
+                    if (P.bstage) {
+                        colo_batch b;
+                        b.start = aq + 0.0;
+                        b.end = now;
+                        b.first = static_cast<uint32_t>(q);
+                        b.n = 1;
+                        b.need_total = need;
+                        const uint64_t inc = static_cast<uint64_t>(pq) + oq;
+                        b.max_incoming = inc < 0xffffffffull ? static_cast<uint32_t>(inc) : 0xffffffffu;
+                        b.verdict = 0;
+                        P.bstage[lo + q] = b;
+                        P.bflag[lo + q] = 1;
+                    }
+                }
+                A.max_need = max(A.max_need, warp_max_u64(need));
+                A.maxb = max(A.maxb, static_cast<uint64_t>(1));
+                A.nbatch += nv;
+            }
+            T = __shfl_sync(FULL, now, nv - 1);
+            head += nv;
+            tail_ptr = head;
+            __syncwarp();
+            continue;
+        }
         if (ah > T) {  // idle: the first popped arrival starts a batch alone
             if (MODE == RUN_SPEC) {
                 if (lane == 0 && ridx < kRegen) sp->regen[ridx] = static_cast<uint32_t>(head - seg_start);
@@ -367,6 +510,21 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         }
         const double start = T + 0.0;  // prefill_start = now_ + stall, stall = 0
         double now = start + dur;      // PrefillDone time = every member's last_token_time
+        // Exact TPT sum by telescoping: when every step time of the batch lies
+        // in [now, 2 now], each sample T_k - T_{k-1} is exact (Sterbenz), so
+        // sum_k alive_k * s_k = sum_j T_{o_j - 1} - n * now: one fixed-point
+        // add per member instead of one per sample.  span bounds the batch's
+        // decode time from above (n members, <= maxo steps of at most
+        // n * (gamma + delta * (max_incoming + maxo)) each).
+        bool tele = false;
+        if (MODE == RUN_FULL) {
+            const double span = static_cast<double>(maxo) *
+                                (static_cast<double>(nb) * (m.decode_coef_const +
+                                                            m.decode_coef_context * static_cast<double>(max_inc + maxo))) *
+                                1.001;
+            tele = now >= 0x1p-44 && span <= now && m.decode_coef_const >= 0.0 && m.decode_coef_context >= 0.0;
+            if (tele && lane == 0) acc_fixed_sub(A.acc, A.flags, now, static_cast<uint32_t>(nb));
+        }
 
         // ---- decode steps (engine.hpp:358-387) ---------------------------------
         // Lane l owns steps k0+l, k0+32+l, k0+64+l, k0+96+l: four independent
@@ -439,6 +597,12 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 const uint32_t i = 32 * r + lane;
                 if (i < cnt) sv[r] = sDK[i] - (i ? sDK[i - 1] : now);
             }
+            if (MODE == RUN_FULL && tele) {  // members whose last step is in this window: + T_{o_j - 1}
+                for (uint64_t j = lane; j < nb; j += 32) {
+                    const uint32_t last = member(j).y - 1;
+                    if (last >= k0 && last < k0 + cnt) acc_fixed(A.acc, A.flags, sDK[last - k0], 1u);
+                }
+            }
             now = sDK[cnt - 1];
             __syncwarp();
 #pragma unroll
@@ -457,11 +621,16 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 if (slow) A.slow_tok += alv;
                 if (want_hist) {  // warp-aggregated: lanes with the same bin add once
                     const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
-                    for (uint32_t f = 0; f < P.nfilters; ++f)
-                        hist_add(P.hist, f * COLO_HIST_BINS + static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
-                                 alv, live && (bits >> P.filter_shift) == P.prefix[f]);
+                    const uint64_t hb = bits >> P.filter_shift;
+                    const uint32_t nf = P.nfilters;
+                    const bool any = live && (hb == P.prefix[0] || (nf > 1 && hb == P.prefix[1]) ||
+                                              (nf > 2 && hb == P.prefix[2]));
+                    if (__any_sync(FULL, any))  // most samples of a narrowing pass match no filter
+                        for (uint32_t f = 0; f < nf; ++f)
+                            hist_add(P.hist, f * COLO_HIST_BINS + static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
+                                     alv, live && hb == P.prefix[f]);
                 }
-                if (live) {
+                if (live && !tele) {
                     acc_fixed(A.acc, A.flags, s, alv);
                 }
                 if (P.samples) {
@@ -782,7 +951,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant
     double T = -INFINITY;
     bool synced;
     Acc A;
-    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, spo[warp], spd[warp], sdk[warp]);
+    run_batches<RUN_SPEC>(P, sg.dev, head, T, sg.end, sg.start, &P.spec[w], synced, A, spo[warp], spd[warp], sdk[warp],
+                          nullptr);
     if ((threadIdx.x & 31) == 0) {
         P.spec[w].exit_head = head;
         P.spec[w].exit_T = T;
@@ -807,7 +977,7 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
         if (head >= sg.end) continue;  // an earlier batch already covers this segment
         bool synced;
         run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp], spd[warp],
-                                 sdk[warp]);
+                                 sdk[warp], nullptr);
         if (synced) {
             head = P.spec[k].exit_head;
             T = P.spec[k].exit_T;
@@ -815,10 +985,11 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
+    extern __shared__ double stile[];  // idle-start blocks: one row of 33 step times per batch, per warp
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
@@ -835,7 +1006,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_replay_full(const __grid_consta
     }
     bool synced;
     if (head < sg.end)
-        run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp], spd[warp], sdk[warp]);
+        run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp], spd[warp], sdk[warp],
+                              stile + warp * (32 * 33));
     const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
     const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
 #pragma unroll
@@ -1157,6 +1329,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     if (opts->d_samples && !opts->d_sample_offsets) return set_err(ctx, COLO_EINVAL, "samples need d_sample_offsets");
     if (opts->d_hist && (opts->nfilters == 0 || opts->nfilters > 3)) return set_err(ctx, COLO_EINVAL, "nfilters 1..3");
     ReplayParams P{};
+    {
+        const char* e = std::getenv("COLO_SINGLES");
+        P.singles = (e && e[0] == '0') ? 0u : 1u;
+    }
     for (size_t i = 0; i < nprofiles; ++i) {
         const colo_status st = colo_validate_profile_pair(&models[i], &gpus[i]);
         if (st != COLO_OK) return set_err(ctx, st, "profile pair rejected (profiles.hpp:129-134)");
@@ -1261,13 +1437,14 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     P.maxctx = reinterpret_cast<unsigned long long*>(ctx->d_counters) + 2;
     COLO_CK(ctx, cudaMemsetAsync(P.maxctx, 0, 8, ctx->stream));
     const uint32_t seg_blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
+    COLO_CK(ctx, cudaFuncSetAttribute(k_replay_full, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
     const uint32_t dev_blocks = static_cast<uint32_t>((ndev + kWarps - 1) / kWarps);
     if (ns && reuse) {  // histogram passes 2-3: the entry states of the previous full replay
         if (P.samples) {
             k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
-        k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
     } else if (ns) {
         k_validate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         int flag = 0;
@@ -1320,7 +1497,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         }
         k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[2], ctx->stream);
-        k_replay_full<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+        k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
         if (timing) {
             cudaEventRecord(ev[3], ctx->stream);
             cudaEventSynchronize(ev[3]);
