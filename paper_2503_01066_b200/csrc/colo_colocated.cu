@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             // absolute-time chain now_k = now_{k-1} + d_k (sequential, one lane),
             // the durations are overwritten by the absolute times
             const uint32_t cnt = min(128u, maxo - k0);
-            if (lane == 0) chain_fold_store(tnow, S.dk, cnt);
+            if (!chain_fast_store(tnow, S.dk, cnt) && lane == 0) chain_fold_store(tnow, S.dk, cnt);
             __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll

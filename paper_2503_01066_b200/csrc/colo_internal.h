@@ -33,6 +33,8 @@ struct colo_ctx {
     size_t seg_bytes = 0;
     void* d_seglog = nullptr;       // colocated replay: the segments' f64 addend logs (lazily grown)
     size_t seglog_bytes = 0;
+    void* d_tmp = nullptr;          // small library temp storage (cub scans; lazily grown)
+    size_t tmp_bytes = 0;
     // serving replay: identity of the last full replay whose segment entry
     // states are still in d_rscratch (reuse_entries); any other d_rscratch
     // user clears rs_valid

@@ -68,6 +68,86 @@ __device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, dou
     }
 }
 
+// ---- the absolute-time chain without the chain ----------------------------------
+// now_k = now_{k-1} + d_k (f64, in order) for K <= 128 durations held 4 per
+// lane (d[r] is step 32r + lane).  While now stays in the binade
+// [2^e, 2^(e+1)) of now_0 the grid is u = 2^(e-52), now is a multiple of u and
+// fl(now + d) = now + RN_u(d) unless now + d is a tie; so with the integers
+// r_k = RN_u(d_k) / u, now_k = now_0 + u * (r_0 + ... + r_k) exactly, and the
+// whole chain is a warp scan.  Returns false (warp-uniform) when a step is a
+// tie, a duration is negative / not finite / too small to scale exactly, or
+// the chain would reach the next binade: the caller folds sequentially.
+__device__ __forceinline__ bool chain_rk(double t0, const double (&d)[4], uint32_t K, uint64_t (&rk)[4], double& u,
+                                         uint64_t& room) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (!(t0 > 0.0) || t0 > 0x1p200 || t0 < 0x1p-200) return false;
+    const int e = ilogb(t0);
+    const double sc = ldexp(1.0, 52 - e);
+    u = ldexp(1.0, e - 52);
+    room = (1ull << 53) - static_cast<uint64_t>(t0 * sc);  // now_K < 2^(e+1)  <=>  sum r < room
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t i = 32 * r + lane;
+        const double x = i < K ? d[r] : 0.0;
+        const double xs = x * sc;
+        bad |= !(x >= 0.0) || (x != 0.0 && x < 0x1p-800) || !(xs < 9007199254740992.0);
+        const double fl = floor(xs), fr = xs - fl;
+        bad |= fr == 0.5;
+        rk[r] = bad ? 0ull : static_cast<uint64_t>(fl) + (fr > 0.5 ? 1u : 0u);
+    }
+    return !__any_sync(kFullMask, bad);
+}
+
+// now_{K-1} (the batch's end) or false
+__device__ __forceinline__ bool chain_fast_end(double t0, const double (&d)[4], uint32_t K, double& t_end) {
+    uint64_t rk[4];
+    double u;
+    uint64_t room;
+    if (!chain_rk(t0, d, K, rk, u, room)) return false;
+    uint64_t s = rk[0] + rk[1] + rk[2] + rk[3];  // each < 2^53: no wrap below 2^55
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullMask, s, o);
+    if (s >= room) return false;
+    t_end = t0 + static_cast<double>(s) * u;  // exact: a multiple of u below 2^(e+1)
+    return true;
+}
+
+// every now_k, k < K, stored over the durations in d (shared memory, step i at d[i])
+__device__ __forceinline__ bool chain_fast_store(double t0, double* d, uint32_t K) {
+    const uint32_t lane = threadIdx.x & 31;
+    double x[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t i = 32 * r + lane;
+        x[r] = i < K ? d[i] : 0.0;
+    }
+    uint64_t rk[4];
+    double u;
+    uint64_t room;
+    if (!chain_rk(t0, x, K, rk, u, room)) return false;
+    uint64_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {  // inclusive prefix in step order
+        uint64_t v = rk[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(kFullMask, v, o);
+            if (lane >= static_cast<uint32_t>(o)) v += y;
+        }
+        v += carry;
+        carry = __shfl_sync(kFullMask, v, 31);
+        rk[r] = v;
+    }
+    if (carry >= room) return false;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t i = 32 * r + lane;
+        if (i < K) d[i] = t0 + static_cast<double>(rk[r]) * u;
+    }
+    return true;
+}
+
 // a -= fixed(s * mult) (mod 2^192; the lane partials are summed mod 2^192 and
 // the total is non-negative)
 __device__ __forceinline__ void acc_fixed_sub(uint64_t (&a)[3], uint32_t& flags, double s, uint32_t mult) {

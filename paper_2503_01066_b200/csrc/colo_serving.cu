@@ -393,7 +393,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                             }
                         }
                         double now = (T + 0.0) + pre;
-                        if (K <= 128) {
+                        double fast_end;
+                        if (K <= 128 && chain_fast_end(now, cur, K, fast_end)) {
+                            now = fast_end;
+                        } else if (K <= 128) {
 #pragma unroll
                             for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = cur[r];
                             __syncwarp();
@@ -589,7 +592,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             // absolute-time chain now_k = now_{k-1} + d_k, sequential on one
             // lane; the durations are overwritten by the absolute times
             const uint32_t cnt = min(128u, maxo - k0);
-            if (lane == 0) chain_fold_store(now, sDK, cnt);
+            if (!chain_fast_store(now, sDK, cnt) && lane == 0) chain_fold_store(now, sDK, cnt);
             __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -1215,10 +1218,13 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
     // segment step counts -> exclusive bases (in place) and the pool size
     size_t tb = 0;
     COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
-    COLO_CK(ctx, cudaMalloc(&sb.tmp, tb + 16));
+    {
+        const colo_status gs = grow_buf(ctx, &ctx->d_tmp, &ctx->tmp_bytes, tb + 16);
+        if (gs != COLO_OK) return gs;
+    }
     uint64_t last_in = 0, last_base = 0;
     COLO_CK(ctx, cudaMemcpyAsync(&last_in, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
-    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(sb.tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
+    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
     COLO_CK(ctx, cudaMemcpyAsync(&last_base, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
     COLO_CK(ctx, cudaStreamSynchronize(st));
     const uint64_t np = last_base + last_in;
