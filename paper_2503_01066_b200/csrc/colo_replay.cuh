@@ -77,26 +77,48 @@ __device__ __forceinline__ void acc_fixed(uint64_t (&a)[3], uint32_t& flags, dou
 // whole chain is a warp scan.  Returns false (warp-uniform) when a step is a
 // tie, a duration is negative / not finite / too small to scale exactly, or
 // the chain would reach the next binade: the caller folds sequentially.
+// binade e of a positive normal double (t in [2^e, 2^(e+1))) and 2^k, from the bits
+__device__ __forceinline__ int binade_of(double t) {
+    return static_cast<int>((static_cast<uint64_t>(__double_as_longlong(t)) >> 52) & 0x7ff) - 1023;
+}
+__device__ __forceinline__ double pow2i(int k) {  // k in [-1022, 1023]
+    return __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(k + 1023) << 52));
+}
+// RN_u(x) / u for u = 1/sc (a power of two): false on a tie, a negative / NaN
+// x, or a result >= 2^53 (x*sc is exact: callers keep sc in [2^-60, 2^260]
+// and x either 0 or >= 2^-700)
+__device__ __forceinline__ bool rn_units(double x, double sc, uint64_t& r) {
+    const double xs = x * sc;
+    if (!(xs < 9007199254740992.0) || !(x >= 0.0) || (x != 0.0 && x < 0x1p-700)) return false;
+    const uint64_t fl = __double2ull_rd(xs);
+    const double fr = xs - static_cast<double>(fl);  // exact below 2^53
+    r = fl + (fr > 0.5 ? 1u : 0u);
+    return fr != 0.5;
+}
 __device__ __forceinline__ bool chain_rk(double t0, const double (&d)[4], uint32_t K, uint64_t (&rk)[4], double& u,
                                          uint64_t& room) {
     const uint32_t lane = threadIdx.x & 31;
-    if (!(t0 > 0.0) || t0 > 0x1p200 || t0 < 0x1p-200) return false;
-    const int e = ilogb(t0);
-    const double sc = ldexp(1.0, 52 - e);
-    u = ldexp(1.0, e - 52);
+    if (!(t0 >= 0x1p-200) || !(t0 <= 0x1p200)) return false;
+    const int e = binade_of(t0);
+    const double sc = pow2i(52 - e);
+    u = pow2i(e - 52);
     room = (1ull << 53) - static_cast<uint64_t>(t0 * sc);  // now_K < 2^(e+1)  <=>  sum r < room
-    bool bad = false;
+    bool ok = true;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         const uint32_t i = 32 * r + lane;
-        const double x = i < K ? d[r] : 0.0;
-        const double xs = x * sc;
-        bad |= !(x >= 0.0) || (x != 0.0 && x < 0x1p-800) || !(xs < 9007199254740992.0);
-        const double fl = floor(xs), fr = xs - fl;
-        bad |= fr == 0.5;
-        rk[r] = bad ? 0ull : static_cast<uint64_t>(fl) + (fr > 0.5 ? 1u : 0u);
+        rk[r] = 0;
+        if (i < K) ok &= rn_units(d[r], sc, rk[r]);
     }
-    return !__any_sync(kFullMask, bad);
+    return __all_sync(kFullMask, ok);
+}
+
+// warp sum of values < 2^57 (three exact 32-bit reductions of 19-bit chunks)
+__device__ __forceinline__ uint64_t warp_sum_small(uint64_t v) {
+    const uint32_t c0 = __reduce_add_sync(kFullMask, static_cast<uint32_t>(v & 0x7ffff));
+    const uint32_t c1 = __reduce_add_sync(kFullMask, static_cast<uint32_t>((v >> 19) & 0x7ffff));
+    const uint32_t c2 = __reduce_add_sync(kFullMask, static_cast<uint32_t>(v >> 38));
+    return static_cast<uint64_t>(c0) + (static_cast<uint64_t>(c1) << 19) + (static_cast<uint64_t>(c2) << 38);
 }
 
 // now_{K-1} (the batch's end) or false
@@ -105,9 +127,7 @@ __device__ __forceinline__ bool chain_fast_end(double t0, const double (&d)[4], 
     double u;
     uint64_t room;
     if (!chain_rk(t0, d, K, rk, u, room)) return false;
-    uint64_t s = rk[0] + rk[1] + rk[2] + rk[3];  // each < 2^53: no wrap below 2^55
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFullMask, s, o);
+    const uint64_t s = warp_sum_small(rk[0] + rk[1] + rk[2] + rk[3]);  // lane sums < 2^55
     if (s >= room) return false;
     t_end = t0 + static_cast<double>(s) * u;  // exact: a multiple of u below 2^(e+1)
     return true;
