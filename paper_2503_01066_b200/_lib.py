@@ -253,7 +253,10 @@ def lib() -> C.CDLL:
         "colo_load_trace_jsonl": (C.c_int64, [C.c_char_p, vp, vp, vp, vp, vp, sz, C.c_char_p, sz]),
         "colo_load_histogram_jsonl": (C.c_int64, [C.c_char_p, vp, vp, sz, C.c_char_p, sz]),
     }
+    variant = bool(os.environ.get("COLO_B200_LIB"))  # an older build variant may lack newer entry points
     for name, (res, args) in sig.items():
+        if variant and not hasattr(L, name):
+            continue
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args

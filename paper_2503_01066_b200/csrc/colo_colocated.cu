@@ -180,21 +180,17 @@ __device__ __forceinline__ double warp_max_f64(double v) {
     return v;
 }
 
+// SEG = false: warp w is device w over its whole trace (no segment code at all);
+// SEG = true: warp w runs P.tasks[w] (whole-trace, speculative or output segment)
+template <bool SEG>
 __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constant__ CoParams P) {
     __shared__ WarpSmem SM[kWarpsC];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t w = blockIdx.x * kWarpsC + wib;
-    uint32_t d = w;
-    int tmode = TM_DIRECT;
-    uint64_t q0 = 0;
-    if (P.tasks) {
-        if (w >= P.ntasks) return;
-        d = P.tasks[w].dev;
-        tmode = static_cast<int>(P.tasks[w].mode);
-        q0 = P.tasks[w].start;
-    } else if (d >= P.ndev) {
-        return;
-    }
+    if (SEG ? w >= P.ntasks : w >= P.ndev) return;
+    const uint32_t d = SEG ? P.tasks[w].dev : w;
+    const int tmode = SEG ? static_cast<int>(P.tasks[w].mode) : static_cast<int>(TM_DIRECT);
+    const uint64_t q0 = SEG ? P.tasks[w].start : 0;
     const bool spec = tmode == TM_SPEC;
     WarpSmem& S = SM[wib];
     const uint32_t pi = P.dev_set[d];
@@ -794,7 +790,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             // absolute-time chain now_k = now_{k-1} + d_k (sequential, one lane),
             // the durations are overwritten by the absolute times
             const uint32_t cnt = min(128u, maxo - k0);
-            if (!chain_fast_store(tnow, S.dk, cnt) && lane == 0) chain_fold_store(tnow, S.dk, cnt);
+            if (lane == 0) chain_fold_store(tnow, S.dk, cnt);  // (a warp scan is slower here: other warps hide this)
             __syncwarp();
             double sv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -1521,7 +1517,8 @@ colo_status grow_buf(colo_ctx* ctx, void*& p, size_t& cap, size_t bytes) {
 colo_status launch_co(colo_ctx* ctx, const CoParams& Q, size_t nwarps, int& flag) {
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
     const uint32_t blocks = static_cast<uint32_t>((nwarps + kWarpsC - 1) / kWarpsC);
-    k_colocated<<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
+    if (Q.tasks) k_colocated<true><<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
+    else k_colocated<false><<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
