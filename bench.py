@@ -255,10 +255,12 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        l0 = ctx.launches()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
+        launches = ctx.launches() - l0
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -315,7 +317,7 @@ def run_ours(args, world, rank, local):
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
                         "d2h_bytes_per_step": 4 * n * world, "steps": e2e_steps,
                         "api": "colo_features_decide_host (pinned host buffers, wall clock)"},
-                "gpu_launches": args.steps, "clocks": clk.report(), "counters": cnt}
+                "gpu_launches": launches, "clocks": clk.report(), "counters": cnt}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline_leg(hp.numpy().view(np.uint32), ho.numpy().view(np.uint32), offs_h)
@@ -533,10 +535,12 @@ def run_colo(args, world, rank, local):
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        l0 = ctx.launches()
         ev0.record()
         for _ in range(args.steps):
             r = step()
         ev1.record()
+        launches = ctx.launches() - l0
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -561,7 +565,7 @@ def run_colo(args, world, rank, local):
                 "totals": dict(zip(keys, [int(x) for x in tot.cpu().tolist()])),
                 "roofline": {"bound": "latency (sequential per-device event loop)", "achieved": None,
                              "peak": None, "unit": "GB/s", "frac": None, "traffic": None},
-                "gpu_launches": 2 * args.steps, "clocks": clk.report(), "c1": c1}
+                "gpu_launches": launches, "clocks": clk.report(), "c1": c1}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 k = min(D, max(threads, 8))
@@ -639,10 +643,12 @@ def run_c4(args, world, rank, local):
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        l0 = ctx.launches()
         ev0.record()
         for _ in range(args.steps):
             st = step()
         ev1.record()
+        launches = ctx.launches() - l0
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -665,7 +671,7 @@ def run_c4(args, world, rank, local):
                 "counters": dict(zip(cs.COUNTER_NAMES, [int(x) for x in counters.cpu().tolist()])),
                 "roofline": {"bound": "latency (sequential f64 time folds per device)", "achieved": None, "peak": None,
                              "unit": "GB/s", "frac": None, "traffic": None},
-                "gpu_launches": None, "clocks": clk.report()}
+                "gpu_launches": launches, "clocks": clk.report()}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -712,10 +718,12 @@ def run_c3(args, world, rank, local):
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        l0 = ctx.launches()
         ev0.record()
         for _ in range(args.steps):
             r = step()
         ev1.record()
+        launches = ctx.launches() - l0
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -746,7 +754,7 @@ def run_c3(args, world, rank, local):
                 "labels": {"tokens": gen, "slow_tokens": slow_tok, "slow_queries": slow_q, "batches": nb},
                 "roofline": {"bound": "latency (sequential f64 time fold per device)", "achieved": achieved,
                              "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
-                "gpu_launches": 5 * args.steps, "clocks": clk.report()}
+                "gpu_launches": launches, "clocks": clk.report()}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

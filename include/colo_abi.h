@@ -176,6 +176,9 @@ colo_status colo_sync(colo_ctx* ctx);
 colo_status colo_ctx_release_scratch(colo_ctx* ctx);
 const char* colo_last_error(const colo_ctx* ctx);
 int colo_ctx_sm_count(const colo_ctx* ctx);
+/* Kernels this context has launched so far (the library's own kernels; the
+ * sorts and scans it takes from CUB are not counted). */
+uint64_t colo_ctx_launches(const colo_ctx* ctx);
 int colo_abi_version(void);
 
 /* Device memory helpers for C/C++ callers without another allocator. */

@@ -220,6 +220,10 @@ class Context:
     def sm_count(self) -> int:
         return lib().colo_ctx_sm_count(self.h)
 
+    def launches(self) -> int:
+        """Kernels this context launched so far (colo_ctx_launches)."""
+        return int(lib().colo_ctx_launches(self.h))
+
     def sync(self) -> None:
         check(lib().colo_sync(self.h), self.h)
 

@@ -1517,6 +1517,7 @@ colo_status grow_buf(colo_ctx* ctx, void*& p, size_t& cap, size_t bytes) {
 colo_status launch_co(colo_ctx* ctx, const CoParams& Q, size_t nwarps, int& flag) {
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
     const uint32_t blocks = static_cast<uint32_t>((nwarps + kWarpsC - 1) / kWarpsC);
+    COLO_LAUNCHED(ctx);
     if (Q.tasks) k_colocated<true><<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
     else k_colocated<false><<<blocks, kWarpsC * 32, 0, ctx->stream>>>(Q);
     COLO_CK(ctx, cudaGetLastError());
@@ -1781,12 +1782,15 @@ colo_status run_devices(colo_ctx* ctx, CoParams P, const std::vector<uint64_t>& 
     if (!sdv.empty()) {
         for (int k = 0; k < 3; ++k) {
             const uint64_t c = LB[k] / kFoldCh;
+            if (c) COLO_LAUNCHED(ctx);
             if (c) k_fold_cand<<<static_cast<uint32_t>((c * 32 + 127) / 128), 128, 0, ctx->stream>>>(lp[k], c,
                                                                                                    const_cast<uint64_t*>(cp[k]));
         }
+        COLO_LAUNCHED(ctx);
         k_fold_walk<<<static_cast<uint32_t>(sdv.size() * 3), 32, 0, ctx->stream>>>(
             d_sdv, reinterpret_cast<const double* const*>(d_ptr), reinterpret_cast<const uint64_t* const*>(d_ptr + 3),
             d_fold);
+        COLO_LAUNCHED(ctx);
         k_seg_combine<<<static_cast<uint32_t>(sdv.size()), 32, 0, ctx->stream>>>(P2, d_sdv, d_fold);
         COLO_CK(ctx, cudaGetLastError());
     }
@@ -1931,6 +1935,7 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     }
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
     const uint32_t vblocks = static_cast<uint32_t>((ndev + 3) / 4);
+    COLO_LAUNCHED(ctx);
     k_co_validate<<<vblocks, 128, 0, ctx->stream>>>(P);
     int flag = 0;
     COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1984,6 +1989,7 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
             jt = reinterpret_cast<const double*>(base + o_jt2);
             jq = reinterpret_cast<const uint32_t*>(base + o_jq2);
         }
+        COLO_LAUNCHED(ctx);
         k_trainer_fold<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P, jt, jq);
         COLO_CK(ctx, cudaGetLastError());
         COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -2036,7 +2042,9 @@ colo_status colo_finalize(colo_ctx* ctx, const double* d_samples, size_t n, doub
     const void* ptrs[6] = {srt, srt, srt, cand, cand, cand};
     COLO_CK(ctx, cudaMemcpyAsync(base + o_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, ctx->stream));
     COLO_CK(ctx, cudaMemcpyAsync(base + o_ptr, ptrs, sizeof ptrs, cudaMemcpyHostToDevice, ctx->stream));
+    COLO_LAUNCHED(ctx);
     k_fold_cand<<<static_cast<uint32_t>((nch * 32 + 127) / 128), 128, 0, ctx->stream>>>(srt, nch, cand);
+    COLO_LAUNCHED(ctx);
     k_fold_walk<<<1, 32, 0, ctx->stream>>>(reinterpret_cast<const SegDev*>(base + o_sd),
                                           reinterpret_cast<const double* const*>(base + o_ptr),
                                           reinterpret_cast<const uint64_t* const*>(base + o_ptr + 3 * sizeof(void*)),

@@ -540,6 +540,7 @@ colo_status launch_fused(colo_ctx* ctx, cudaStream_t stream, const colo_mapset* 
     const uint64_t need_blocks = (n + kChunk * (kThreads / 32) - 1) / (kChunk * (kThreads / 32));
     if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(std::max<uint64_t>(need_blocks, 1));
     void* args[] = {&P};
+    COLO_LAUNCHED(ctx);
     COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, smem, stream));
     return COLO_OK;
 }
@@ -581,6 +582,7 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
         const uint64_t ntiles = (n + kTile - 1) / kTile;
         if (static_cast<uint64_t>(blocks) > ntiles) blocks = static_cast<int>(ntiles);
         void* args[] = {&P};
+        COLO_LAUNCHED(ctx);
         COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, stream));
         return COLO_OK;
     }
@@ -593,6 +595,7 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
     const uint64_t need_blocks = (n + kThreads - 1) / kThreads;
     if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     void* args[] = {&P};
+    COLO_LAUNCHED(ctx);
     COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, stream));
     return COLO_OK;
 }
@@ -634,6 +637,7 @@ colo_status colo_decide_exact(colo_ctx* ctx, const colo_model* m, const colo_gpu
     const uint64_t need_blocks = (n + kThreads - 1) / kThreads;
     if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
     void* args[] = {&P};
+    COLO_LAUNCHED(ctx);
     COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, 0, ctx->stream));
     return COLO_OK;
 }

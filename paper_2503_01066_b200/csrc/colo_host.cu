@@ -235,6 +235,8 @@ const char* colo_last_error(const colo_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 int colo_ctx_sm_count(const colo_ctx* ctx) { return ctx ? ctx->sm_count : 0; }
 
+uint64_t colo_ctx_launches(const colo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
 colo_status colo_dev_alloc(colo_ctx* ctx, size_t bytes, void** d_ptr) {
     if (!ctx || !d_ptr) return COLO_EINVAL;
     COLO_CK(ctx, cudaSetDevice(ctx->device));

@@ -40,7 +40,10 @@ struct colo_ctx {
     // user clears rs_valid
     uint64_t rs_sig[10] = {};
     bool rs_valid = false;
+    uint64_t launches = 0;          // kernels this context launched (colo_ctx_launches)
 };
+
+#define COLO_LAUNCHED(ctx) (++(ctx)->launches)
 
 struct colo_mapset {
     int device = 0;

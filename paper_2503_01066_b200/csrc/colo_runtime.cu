@@ -181,13 +181,16 @@ colo_status colo_mapset_build(colo_ctx* ctx, const colo_model* m, const colo_gpu
     }
     uint64_t budget = g->capacity_bytes - g->runtime_reserve_bytes - m->weights_bytes;
     uint32_t cpa = mode == COLO_CPA;
+    COLO_LAUNCHED(ctx);
     k_build_offload<<<static_cast<uint32_t>((noff + 255) / 256), 256, 0, ctx->stream>>>(
         *m, budget, cpa, grid->cached_step, grid->incoming_step, grid->batch_step, ms->I, ms->B,
         static_cast<uint32_t>(noff), ms->d_off);
+    COLO_LAUNCHED(ctx);
     k_build_hedge<<<static_cast<uint32_t>((nhed + 255) / 256), 256, 0, ctx->stream>>>(
         *m, *g, cpa, hedge_step, assumed, ms->F, static_cast<uint32_t>(nhed), ms->d_hed);
     if (ms->fast) {
         MapView mv = make_view(ms);
+        COLO_LAUNCHED(ctx);
         k_build_tab<<<static_cast<uint32_t>((ntab + 255) / 256), 256, 0, ctx->stream>>>(mv, ms->d_tab, ms->d_str);
     }
     e = cudaGetLastError();
@@ -226,6 +229,7 @@ colo_status colo_mapset_from_cells(colo_ctx* ctx, const colo_model* m, const col
     if (ms->fast) {
         MapView mv = make_view(ms);
         uint64_t ntab = static_cast<uint64_t>(ms->C + 1) * (ms->I + 1);
+        COLO_LAUNCHED(ctx);
         k_build_tab<<<static_cast<uint32_t>((ntab + 255) / 256), 256, 0, ctx->stream>>>(mv, ms->d_tab, ms->d_str);
     }
     COLO_CK(ctx, cudaGetLastError());
@@ -272,6 +276,7 @@ colo_status colo_features(colo_ctx* ctx, const colo_model* m, colo_mode mode, co
     if (!ctx || !m || (n && (!d_prompt || !d_output))) return COLO_EINVAL;
     if (n == 0) return COLO_OK;
     int blocks = std::max<int>(1, static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 8ull)));
+    COLO_LAUNCHED(ctx);
     k_features<<<blocks, 256, 0, ctx->stream>>>(*m, mode == COLO_CPA, d_prompt, d_output, n, d_need, d_charged,
                                                 d_prefill);
     COLO_CK(ctx, cudaGetLastError());
@@ -301,6 +306,7 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
     P.prompt = d_prompt;
     P.output = d_output;
     uint32_t blocks = static_cast<uint32_t>((ndev * 32 + 127) / 128);
+    COLO_LAUNCHED(ctx);
     k_synth<<<blocks, 128, 0, ctx->stream>>>(P);
     COLO_CK(ctx, cudaGetLastError());
     return COLO_OK;

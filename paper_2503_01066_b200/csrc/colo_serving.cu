@@ -1174,6 +1174,7 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
     {
         unsigned long long* cnt = reinterpret_cast<unsigned long long*>(ctx->d_counters);
         COLO_CK(ctx, cudaMemsetAsync(cnt, 0, 8, st));
+        COLO_LAUNCHED(ctx);
         k_count_saturated<<<(P.nsegs + 255) / 256, 256, 0, st>>>(P.spec, P.nsegs, cnt);
         unsigned long long nsat = 0;
         COLO_CK(ctx, cudaMemcpyAsync(&nsat, cnt, 8, cudaMemcpyDeviceToHost, st));
@@ -1212,8 +1213,10 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
     COLO_CK(ctx, cudaMemsetAsync(P.sat_end, 0, n * 4, st));
     const uint32_t blocks = static_cast<uint32_t>((ns + kWarps - 1) / kWarps);
     P.sat_pass = 1;
+    COLO_LAUNCHED(ctx);
     k_sat_partition<<<blocks, kWarps * 32, 0, st>>>(P);
     P.sat_pass = 2;
+    COLO_LAUNCHED(ctx);
     k_sat_partition<<<blocks, kWarps * 32, 0, st>>>(P);
     // segment step counts -> exclusive bases (in place) and the pool size
     size_t tb = 0;
@@ -1239,6 +1242,7 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         if (g != COLO_OK) return g;
     }
     P.sat_dk = static_cast<double*>(ctx->d_satpool);
+    COLO_LAUNCHED(ctx);
     k_sat_durations<<<blocks, kWarps * 32, 0, st>>>(P);
     COLO_CK(ctx, cudaGetLastError());
     P.sat_on = 1;
@@ -1447,11 +1451,15 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     const uint32_t dev_blocks = static_cast<uint32_t>((ndev + kWarps - 1) / kWarps);
     if (ns && reuse) {  // histogram passes 2-3: the entry states of the previous full replay
         if (P.samples) {
+            COLO_LAUNCHED(ctx);
             k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+            COLO_LAUNCHED(ctx);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
+        COLO_LAUNCHED(ctx);
         k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
     } else if (ns) {
+        COLO_LAUNCHED(ctx);
         k_validate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         int flag = 0;
         COLO_CK(ctx, cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1476,6 +1484,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
                 for (size_t i = 0; i < nprofiles; ++i) {
                     double* t = reinterpret_cast<double*>(static_cast<uint8_t*>(ctx->d_dtab) +
                                                           i * ((tn * 8 + 255) & ~size_t(255)));
+                    COLO_LAUNCHED(ctx);
                     k_fill_dtab<<<256, 256, 0, ctx->stream>>>(t, tn, models[i].decode_coef_const,
                                                               models[i].decode_coef_context);
                     P.dtab[i] = t;
@@ -1484,7 +1493,9 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             }
         }
         if (P.samples) {
+            COLO_LAUNCHED(ctx);
             k_seg_sums<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+            COLO_LAUNCHED(ctx);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
         const bool timing = std::getenv("COLO_REPLAY_TIMING") != nullptr;  // per-pass device times to stderr
@@ -1492,6 +1503,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (timing)
             for (auto& e : ev) cudaEventCreate(&e);
         if (timing) cudaEventRecord(ev[0], ctx->stream);
+        COLO_LAUNCHED(ctx);
         k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
         SatBuffers sat;  // all-queued batch records for the resolve pass's fast path
         const colo_status sst = sat_prepare(ctx, P, off, sat, ctx->stream);
@@ -1501,8 +1513,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             P.dbg = reinterpret_cast<unsigned long long*>(ctx->d_counters);
             cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream);
         }
+        COLO_LAUNCHED(ctx);
         k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[2], ctx->stream);
+        COLO_LAUNCHED(ctx);
         k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
         if (timing) {
             cudaEventRecord(ev[3], ctx->stream);
@@ -1519,8 +1533,14 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             for (auto& e : ev) cudaEventDestroy(e);
         }
     }
-    if (P.summary) k_finalize<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
-    if (want_batches && ns) k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    if (P.summary) {
+        COLO_LAUNCHED(ctx);
+        k_finalize<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    }
+    if (want_batches && ns) {
+        COLO_LAUNCHED(ctx);
+        k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    }
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(ctx->rs_sig, sig, sizeof sig);

@@ -100,6 +100,7 @@ colo_status colo_synth_tuples(colo_ctx* ctx, uint64_t seed, size_t n, uint32_t n
     P.n = n;
     P.out = reinterpret_cast<uint4*>(d_out);
     const int blocks = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 16ull));
+    COLO_LAUNCHED(ctx);
     k_synth_tuples<<<blocks, 256, 0, ctx->stream>>>(P);
     COLO_CK(ctx, cudaGetLastError());
     return COLO_OK;
@@ -110,6 +111,7 @@ colo_status colo_compare_verdicts(colo_ctx* ctx, const uint32_t* d_map, const ui
     if (!ctx || !d_counts || (n && (!d_map || !d_exact))) return COLO_EINVAL;
     if (n == 0) return COLO_OK;
     const int blocks = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->sm_count * 8ull));
+    COLO_LAUNCHED(ctx);
     k_compare<<<blocks, 256, 0, ctx->stream>>>(d_map, d_exact, n, num_layers, d_counts);
     COLO_CK(ctx, cudaGetLastError());
     return COLO_OK;
