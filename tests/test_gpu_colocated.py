@@ -330,3 +330,29 @@ def test_segmented_long_trace(ctx, orc, qps, cpa):
             assert np.array_equal(b[k], ref["batches"][k]), (seg, k)
         outs.append(b["verdict"].copy())
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+def test_segmented_stats_and_modes(ctx, orc):
+    """colo_colocated_stats over two long devices (Colocated CPA at 0.3 QPS,
+    SeparateCluster with varying label delays): forced segments, automatic and
+    one warp per device give the same percentiles, exact sums and totals."""
+    hv, hp = sharegpt_histogram()
+    m, g, grid = default_model(), default_gpu(), default_grid()
+    tr = []
+    for seed, qps, spec in ((3, 0.3, ("fixed", 0.01)), (4, 0.2, ("uniform", 0.0, 30.0))):
+        a, p, o, ld = orc.generate_trace(qps, 20000 / qps, ("histogram", hv, hp), seed, spec, with_labels=True)
+        tr.append((a, p, o, ld))
+    da, dp, do, dld, doff, off = upload(tr)
+    sets = [mapset(ctx, m, g, grid, 1)]
+    dset = torch.zeros(2, dtype=torch.int16, device="cuda")
+    dmode = torch.tensor([int(cs.SimMode.COLOCATED), int(cs.SimMode.SEPARATE_CLUSTER)], dtype=torch.uint8, device="cuda")
+    outs = [cs.colocated_stats(ctx, sets, da, dp, do, doff, dset, label_delay=dld, tau=0.05, sim_mode=dmode, seg_len=s)
+            for s in (0, None, 700)]
+    for pc, tot in outs[1:]:
+        assert np.array_equal(np.array(pc).view(np.uint64), np.array(outs[0][0]).view(np.uint64))
+        assert tot == outs[0][1]
+    for i, (a, p, o, ld) in enumerate(tr):
+        ref = orc.replay_colocated(m, g, grid, 1, a, p, o, ld, 60.0, tau=0.05, sim_mode=["colocated", "baseline"][i])
+        r = cs.replay_colocated(ctx, sets, da, dp, do, doff, dset, label_delay=dld, tau=0.05, sim_mode=dmode, seg_len=700)
+        s = cs.colocated_summaries(r["summary"])[i]
+        assert not diff(s, ref["report"]), (i, diff(s, ref["report"]))
