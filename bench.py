@@ -467,6 +467,43 @@ def reference_colocated(dev_traces, threads):
     return n, time.perf_counter() - t0
 
 
+def reference_serving(dev_traces, threads, with_stats=False):
+    """The reference's own Simulation::run (SimMode::ServingOnly) through
+    oracle/_ref, one device per task on all host threads; with_stats also
+    keeps the TPT samples and runs finalize (sort, nearest ranks, mean) as
+    run_simulation does.  dev_traces: list of (model, gpu, arrival, prompt,
+    output)."""
+    from oracle.oracle import OracleLib, default_grid
+
+    ref = OracleLib("ref")
+    grid = default_grid()
+
+    def one(t):
+        m, g, a, p, o = t
+        ref.replay_colocated(m, g, grid, 1, a, p, o, np.full(len(a), 0.01), 60.0, tau=0.05,
+                             want_samples=with_stats, want_batches=False, sim_mode="serving-only")
+        return len(a)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        n = sum(ex.map(one, dev_traces))
+    return n, time.perf_counter() - t0
+
+
+def reference_sample(arrival, prompt, output, offs, devs, per, models):
+    """Host copies of the first `per` queries of the first `devs` devices."""
+    from oracle.oracle import default_gpu
+
+    offs_h = offs.cpu().numpy()
+    out = []
+    for d in range(min(devs, len(offs_h) - 1)):
+        lo = int(offs_h[d])
+        hi = min(int(offs_h[d + 1]), lo + per)
+        out.append((models[d % len(models)], default_gpu(), arrival[lo:hi].cpu().numpy(),
+                    prompt[lo:hi].cpu().numpy().view(np.uint32), output[lo:hi].cpu().numpy().view(np.uint32)))
+    return out
+
+
 def run_colo(args, world, rank, local):
     """Colocated replay (the full admission loop).
     (1) C1 (BASELINE.json configs[0]): the 1M-query single-device trace at
@@ -672,6 +709,21 @@ def run_c4(args, world, rank, local):
                 "roofline": {"bound": "latency (sequential f64 time folds per device)", "achieved": None, "peak": None,
                              "unit": "GB/s", "frac": None, "traffic": None},
                 "gpu_launches": launches, "clocks": clk.report()}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle.oracle import default_model, phi14b_model
+
+                threads = os.cpu_count() or 1
+                tr = reference_sample(arrival, prompt, output, offs, 16, 100_000, [default_model(), phi14b_model()])
+                nq, ts = reference_serving(tr, threads, with_stats=True)
+                line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "sample": f"first 100k queries of 16 of the rank's devices ({nq} queries), "
+                                                  f"Simulation::run ServingOnly + finalize via oracle/_ref, "
+                                                  f"{threads} host threads, {ts:.1f} s (the decision lookups "
+                                                  "are not included)"}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -755,6 +807,20 @@ def run_c3(args, world, rank, local):
                 "roofline": {"bound": "latency (sequential f64 time fold per device)", "achieved": achieved,
                              "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
                 "gpu_launches": launches, "clocks": clk.report()}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle.oracle import default_model, phi14b_model
+
+                threads = os.cpu_count() or 1
+                tr = reference_sample(arrival, prompt, output, offs, 16, 250_000, [default_model(), phi14b_model()])
+                nq, ts = reference_serving(tr, threads)
+                line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "sample": f"first 250k queries of 16 of the C3 devices ({nq} queries), "
+                                                  f"Simulation::run ServingOnly via oracle/_ref, {threads} host "
+                                                  f"threads, {ts:.1f} s"}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
