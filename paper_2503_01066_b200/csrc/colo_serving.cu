@@ -172,7 +172,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
         uint64_t tail;
         const double ah = arr[head];
-        if (ah > T && P.singles) {
+        if (ah > T && P.singles && m.decode_coef_const >= 0.0 && m.decode_coef_context >= 0.0) {
             // ---- idle starts, up to 32 at a time -------------------------------
             // An idle start is a batch of one query that starts at its arrival
             // (T = arr[q]), so its whole timeline depends on q alone.  Lane l
