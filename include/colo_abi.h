@@ -299,7 +299,11 @@ typedef struct colo_replay_opts {
                                          speculation and resolution and reuse its segment entry states
                                          (histogram passes 2-3 of the exact-stats protocol).  Falls back
                                          to a full replay when the context cannot prove that. */
-    uint32_t pad;
+    uint32_t stats_mode;              /* sparse exact-stats passes: 1 = also record, per batch, its start
+                                         and the range of its samples' top-21-bit bins (the first histogram
+                                         pass); 2 (with reuse_entries, after a mode-1 call on the same
+                                         trace) = replay only the batches whose range covers a filter bin
+                                         (the narrowing passes; same histograms).  0 = off. */
 } colo_replay_opts;
 
 /* Serving-only replay of every device's trace.  Each device is cut into

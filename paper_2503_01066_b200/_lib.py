@@ -91,7 +91,7 @@ class ReplayOpts(C.Structure):
         ("segment_len", C.c_uint32),
         ("filter_prefix", C.c_uint64 * 3),
         ("reuse_entries", C.c_uint32),
-        ("pad", C.c_uint32),
+        ("stats_mode", C.c_uint32),
     ]
 
 

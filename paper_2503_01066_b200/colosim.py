@@ -18,6 +18,7 @@ import ctypes as C
 import dataclasses
 import enum
 import math
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import List, Optional, Sequence, Tuple
@@ -609,7 +610,7 @@ def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfi
                    dev_offsets, dev_profile, tau: float = math.inf, sets: Optional[Sequence[MapSet]] = None,
                    samples: bool = False, labels: bool = True, batches: bool = False, summary: bool = True,
                    hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), segment_len: int = 0,
-                   reuse_entries: bool = False):
+                   reuse_entries: bool = False, stats_mode: int = 0):
     """Serving-only replay of every device (engine.hpp:140-387, SimMode::ServingOnly).
     Returns a dict of device tensors: samples (f64, reference order),
     labels (u8 per query), batches (raw bytes, BATCH_DTYPE), summary (DeviceSummary bytes)."""
@@ -627,6 +628,7 @@ def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfi
     opts.tau = tau
     opts.segment_len = segment_len
     opts.reuse_entries = 1 if reuse_entries else 0
+    opts.stats_mode = int(stats_mode)  # 1: record per-batch sample-bin ranges; 2: sparse narrowing pass
     keep = []
     if sets is not None:
         arr = _sets_array(sets)
@@ -693,6 +695,7 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
     dist = torch.distributed if (torch.distributed.is_available() and torch.distributed.is_initialized()) else None
     dev = prompt.device
     hist = torch.zeros(len(quantiles) * HIST_BINS, dtype=torch.int64, device=dev)
+    sparse = os.environ.get("COLO_SPARSE_STATS", "1") != "0"
 
     def run_pass(hist_shift, filter_shift, prefixes):
         h = hist[: len(prefixes) * HIST_BINS]
@@ -700,7 +703,8 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
         first = filter_shift == 63
         r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
                            summary=first, hist=h, hist_shift=hist_shift, filter_shift=filter_shift,
-                           filter_prefix=tuple(prefixes), reuse_entries=not first)
+                           filter_prefix=tuple(prefixes), reuse_entries=not first,
+                           stats_mode=(1 if first else 2) if sparse else 0)
         if not first:
             return h, None
         S = summaries_to_numpy(r["summary"])

@@ -189,6 +189,7 @@ void colo_ctx_destroy(colo_ctx* ctx) {
     if (ctx->d_seg) cudaFree(ctx->d_seg);
     if (ctx->d_seglog) cudaFree(ctx->d_seglog);
     if (ctx->d_tmp) cudaFree(ctx->d_tmp);
+    if (ctx->d_bmeta) cudaFree(ctx->d_bmeta);
     if (ctx->d_dtab) cudaFree(ctx->d_dtab);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
@@ -212,8 +213,10 @@ colo_status colo_ctx_release_scratch(colo_ctx* ctx) {
     drop(ctx->d_seg, ctx->seg_bytes);
     drop(ctx->d_seglog, ctx->seglog_bytes);
     drop(ctx->d_tmp, ctx->tmp_bytes);
+    drop(ctx->d_bmeta, ctx->bmeta_bytes);
     drop(ctx->d_dtab, ctx->dtab_bytes);
     ctx->rs_valid = false;
+    ctx->bmeta_valid = false;
     return COLO_OK;
 }
 

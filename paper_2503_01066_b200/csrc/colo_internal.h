@@ -35,6 +35,9 @@ struct colo_ctx {
     size_t seglog_bytes = 0;
     void* d_tmp = nullptr;          // small library temp storage (cub scans; lazily grown)
     size_t tmp_bytes = 0;
+    void* d_bmeta = nullptr;        // serving stats: per-query batch start + sample-bin range (lazily grown)
+    size_t bmeta_bytes = 0;
+    bool bmeta_valid = false;       // d_bmeta holds the batch records of the replay rs_sig describes
     // serving replay: identity of the last full replay whose segment entry
     // states are still in d_rscratch (reuse_entries); any other d_rscratch
     // user clears rs_valid

@@ -128,6 +128,14 @@ struct ReplayParams {
     double* sat_dk;
     uint32_t sat_on;
     uint32_t singles;  // idle starts 32 at a time (run_batches); COLO_SINGLES=0 turns it off
+    // Sparse stats passes (serving_stats): the first pass records, at each
+    // batch's first query, its start time and the range of its samples' top
+    // 21-bit bins (bmeta_bins: valid<<63 | idle<<62 | max<<21 | min); the
+    // narrowing passes then replay only batches whose range covers a filter bin
+    double* bmeta_start;
+    uint64_t* bmeta_bins;
+    const double* sparse_start;  // the same records, read by k_sparse_hist
+    const uint64_t* sparse_bins;
     unsigned long long* dbg;  // COLO_REPLAY_TIMING: [0] fast-path batches, [1] other batches of the resolve pass
     // decode-step latency table per profile: dtab[pi][x] = gamma + delta * x for
     // every context x < dtab_n (cost_model.hpp:28-35 with batch 1, the same f64
@@ -171,6 +179,8 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
     while (head < stop && head < N) {
         // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
         uint64_t tail;
+        bool idle_b = false;
+        uint32_t bmin = 0xffffffffu, bmax = 0;  // bins (bits >> 42) of this batch's samples
         const double ah = arr[head];
         if (ah > T && P.singles && m.decode_coef_const >= 0.0 && m.decode_coef_context >= 0.0) {
             // ---- idle starts, up to 32 at a time -------------------------------
@@ -256,6 +266,20 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         const uint32_t k = k0 + lane;
                         const bool live = k < ob;
                         const double s = sT[b * 33 + 1 + lane] - sT[b * 33 + lane];
+                        if (P.bmeta_bins) {
+                            const uint32_t bn = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(s)) >> 42);
+                            const bool in = live && !(s < 0.0);
+                            uint32_t lo_b = in ? bn : 0xffffffffu, hi_b = in ? bn : 0u;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                lo_b = min(lo_b, __shfl_xor_sync(FULL, lo_b, o));
+                                hi_b = max(hi_b, __shfl_xor_sync(FULL, hi_b, o));
+                            }
+                            if (lane == b) {
+                                bmin = min(bmin, lo_b);
+                                bmax = max(bmax, hi_b);
+                            }
+                        }
                         const bool slow = live && s > P.tau;
                         if (__ballot_sync(FULL, slow)) slowm |= 1u << b;
                         A.slow_tok += slow;
@@ -280,6 +304,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 }
                 if (tl) acc_fixed(A.acc, A.flags, now, 1u);
                 const uint64_t need = v ? serving_memory(m, static_cast<uint64_t>(pq) + oq, 1) : 0ull;
+                if (v && P.bmeta_bins) {
+                    P.bmeta_start[lo + q] = aq + 0.0;
+                    P.bmeta_bins[lo + q] = (1ull << 63) | (1ull << 62) | (static_cast<uint64_t>(bmax) << 21) | bmin;
+                }
                 if (v) {
                     const bool slowq = (slowm >> lane) & 1u;  // a lone query's tokens are every step
                     A.gen += ov;
@@ -325,6 +353,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             T = ah;
             tail = head + 1;
             tail_ptr = head + 1;
+            idle_b = true;
         } else {  // queued: every arrival with time <= T has been popped
             if (MODE == RUN_RESOLVE && P.sat_on) {
                 // Saturated fast path: a record at head whose last member has
@@ -617,6 +646,11 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             if (MODE == RUN_FULL) {
                 const uint32_t alv = alive[r];
                 const bool live = k < maxo;
+                if (P.bmeta_bins && live && !(s < 0.0)) {  // (negative samples never match a filter)
+                    const uint32_t bn = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(s)) >> 42);
+                    bmin = min(bmin, bn);
+                    bmax = max(bmax, bn);
+                }
                 const bool slow = live && s > P.tau;
                 const uint32_t sb = __ballot_sync(FULL, slow);
                 if (sb && first_slow == 0xffffffffu) first_slow = kr0 + __ffs(sb) - 1;
@@ -658,6 +692,18 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 const bool slowq = member(j).y > first_slow;
                 A.slow_q += slowq;
                 if (P.labels) P.labels[lo + head + j] = slowq ? 1 : 0;
+            }
+            if (P.bmeta_bins) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    bmin = min(bmin, __shfl_xor_sync(FULL, bmin, o));
+                    bmax = max(bmax, __shfl_xor_sync(FULL, bmax, o));
+                }
+                if (lane == 0) {
+                    P.bmeta_start[lo + head] = start;
+                    P.bmeta_bins[lo + head] = (1ull << 63) | (idle_b ? 1ull << 62 : 0ull) |
+                                              (static_cast<uint64_t>(bmax) << 21) | bmin;
+                }
             }
             if (lane == 0 && P.bstage) {
                 colo_batch b;
@@ -1033,6 +1079,46 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
         q.acc[2] = A.acc[2];
         q.flags = fl;
         q.t_end = T;
+    }
+}
+
+// Narrowing stats passes over the batches of the first pass whose sample-bin
+// range covers a filter bin: each is replayed alone from its recorded start
+// (an idle start forms the same one-query batch from T = -inf; a queued batch
+// starts at the previous end, T = start).  One warp per replay segment.
+__global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_sparse_hist(const __grid_constant__ ReplayParams P) {
+    __shared__ uint2 spo[kWarps][kStage];
+    __shared__ double spd[kWarps][kStage];
+    __shared__ __align__(16) double sdk[kWarps][128];
+    extern __shared__ double stile[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const uint64_t lo = P.dev_off[sg.dev];
+    const uint32_t sh = 42 - P.filter_shift;  // filter prefix -> its top-21-bit bin
+    uint32_t fb[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f) fb[f] = f < static_cast<int>(P.nfilters) ? static_cast<uint32_t>(P.prefix[f] >> sh) : 0xffffffffu;
+    Acc A;
+    for (uint64_t j0 = sg.start; j0 < sg.end; j0 += 32) {
+        const uint64_t q = j0 + lane;
+        const uint64_t bb = q < sg.end ? P.sparse_bins[lo + q] : 0ull;
+        const uint32_t mn = static_cast<uint32_t>(bb & 0x1fffff), mx = static_cast<uint32_t>((bb >> 21) & 0x1fffff);
+        bool hit = false;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) hit |= mn <= fb[f] && fb[f] <= mx;
+        uint32_t hits = __ballot_sync(FULL, (bb >> 63) && hit);
+        while (hits) {
+            const uint32_t l = __ffs(hits) - 1;
+            hits &= hits - 1;
+            const uint64_t b2 = __shfl_sync(FULL, bb, l);
+            uint64_t head = j0 + l;
+            double T = (b2 >> 62) & 1ull ? -INFINITY : P.sparse_start[lo + head];
+            bool synced;
+            run_batches<RUN_FULL>(P, sg.dev, head, T, j0 + l + 1, sg.start, nullptr, synced, A, spo[warp], spd[warp],
+                                  sdk[warp], stile + warp * (32 * 33));
+        }
     }
 }
 
@@ -1443,6 +1529,18 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     P.filter_shift = opts->filter_shift;
     for (int f = 0; f < 3; ++f) P.prefix[f] = opts->filter_prefix[f];
     P.err = ctx->d_flag;
+    if (opts->stats_mode == 1 && n) {  // first stats pass: record every batch's start and sample-bin range
+        ctx->bmeta_valid = false;
+        size_t freeb = 0, totb = 0;
+        bool room = ctx->bmeta_bytes >= n * 16;
+        if (!room && cudaMemGetInfo(&freeb, &totb) == cudaSuccess)
+            room = n * 16 + (8ull << 30) < freeb + ctx->bmeta_bytes;
+        if (room && grow_buf(ctx, &ctx->d_bmeta, &ctx->bmeta_bytes, n * 16) == COLO_OK) {
+            P.bmeta_start = static_cast<double*>(ctx->d_bmeta);
+            P.bmeta_bins = reinterpret_cast<uint64_t*>(static_cast<double*>(ctx->d_bmeta) + n);
+            COLO_CK(ctx, cudaMemsetAsync(P.bmeta_bins, 0, n * 8, ctx->stream));
+        }
+    }
     COLO_CK(ctx, cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream));
     P.maxctx = reinterpret_cast<unsigned long long*>(ctx->d_counters) + 2;
     COLO_CK(ctx, cudaMemsetAsync(P.maxctx, 0, 8, ctx->stream));
@@ -1456,8 +1554,16 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             COLO_LAUNCHED(ctx);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
-        COLO_LAUNCHED(ctx);
-        k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+        if (opts->stats_mode == 2 && ctx->bmeta_valid && P.hist) {  // narrowing pass: only batches that can hit a filter bin
+            P.sparse_start = static_cast<const double*>(ctx->d_bmeta);
+            P.sparse_bins = reinterpret_cast<const uint64_t*>(static_cast<const double*>(ctx->d_bmeta) + n);
+            COLO_CK(ctx, cudaFuncSetAttribute(k_sparse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+            COLO_LAUNCHED(ctx);
+            k_sparse_hist<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+        } else {
+            COLO_LAUNCHED(ctx);
+            k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+        }
     } else if (ns) {
         COLO_LAUNCHED(ctx);
         k_validate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
@@ -1545,6 +1651,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(ctx->rs_sig, sig, sizeof sig);
     ctx->rs_valid = true;
+    if (!reuse) ctx->bmeta_valid = P.bmeta_bins != nullptr;  // records of exactly this replay
     return COLO_OK;
 }
 
@@ -1572,8 +1679,11 @@ static colo_status serving_stats_impl(colo_ctx* ctx, void* comm, const colo_mode
     uint64_t ntot = 0;
     *totals = colo_device_summary{};
     for (int i = 0; i < 4; ++i) pctl[i] = std::nan("");
+    const char* sparse_env = std::getenv("COLO_SPARSE_STATS");
+    const bool sparse = !(sparse_env && sparse_env[0] == '0');
     for (int pass = 0; pass < 3 && st == COLO_OK; ++pass) {
         colo_replay_opts o{};
+        o.stats_mode = sparse ? (pass == 0 ? 1u : 2u) : 0u;
         o.tau = tau;
         o.d_hist = d_hist;
         o.d_summary = pass == 0 ? d_sum : nullptr;
@@ -1593,8 +1703,24 @@ static colo_status serving_stats_impl(colo_ctx* ctx, void* comm, const colo_mode
             st = cuda_err(ctx, e, "cudaMemset(hist)");
             break;
         }
+        const bool timing = std::getenv("COLO_REPLAY_TIMING") != nullptr;
+        cudaEvent_t pe[2];
+        if (timing) {
+            cudaEventCreate(&pe[0]);
+            cudaEventCreate(&pe[1]);
+            cudaEventRecord(pe[0], ctx->stream);
+        }
         st = colo_replay_serving(ctx, models, gpus, nprofiles, d_arrival, d_prompt, d_output, n, d_dev_offsets,
                                  d_dev_profile, ndev, &o);
+        if (timing) {
+            cudaEventRecord(pe[1], ctx->stream);
+            cudaEventSynchronize(pe[1]);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pe[0], pe[1]);
+            std::fprintf(stderr, "colo stats pass %d (mode %u): %.3f ms\n", pass, o.stats_mode, ms);
+            cudaEventDestroy(pe[0]);
+            cudaEventDestroy(pe[1]);
+        }
         if (st != COLO_OK) break;
         if (comm) {  // every rank holds its own device shard: sum the histograms
             st = colo_stats_allreduce(ctx, comm, d_hist, static_cast<size_t>(o.nfilters) * COLO_HIST_BINS);

@@ -385,6 +385,31 @@ def test_serving_stats_exact(ctx, orc):
     assert tot.generated_tokens == len(ref["samples"])
 
 
+def test_serving_stats_sparse_passes(ctx, orc, monkeypatch):
+    """Sparse narrowing passes (only batches whose first-pass sample-bin range
+    covers a filter bin are replayed) give the same percentiles, counters and
+    exact sums as full passes, in Python and through the C-ABI, and both equal
+    finalize over the union of the reference's samples."""
+    hv, hp = sharegpt_histogram()
+    tr = [orc.generate_trace(q, 3000.0, ("histogram", hv, hp), 20 + i) for i, q in enumerate((0.05, 0.3, 1.1, 2.5))]
+    a = np.concatenate([t[0] for t in tr])
+    p = np.concatenate([t[1] for t in tr])
+    o = np.concatenate([t[2] for t in tr])
+    off = np.concatenate([[0], np.cumsum([len(t[0]) for t in tr])]).astype(np.int64)
+    smp = np.concatenate([orc.replay_serving(default_model(), OG, *t)["samples"] for t in tr])
+    want = orc.finalize(smp)
+    args = (ctx, [(cs.ModelProfile(), G)], torch.from_numpy(a).cuda(), i32(p), i32(o), torch.from_numpy(off).cuda(),
+            torch.zeros(len(tr), dtype=torch.int16).cuda())
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("COLO_SPARSE_STATS", mode)
+        st = cs.serving_stats(*args, tau=0.05)
+        pc, tot = cs.serving_stats_c(*args, tau=0.05)
+        assert (st["p50"], st["p90"], st["p99"]) == tuple(want[:3]) == tuple(pc[:3]), mode
+        got[mode] = (st, tuple(pc), tot.generated_tokens, tot.slow_tokens, list(tot.tpt_sum))
+    assert got["1"] == got["0"]
+
+
 def test_mapset_save_load_roundtrip(ctx, tmp_path):  # maps.hpp:118-191, 284-332 through device map sets
     for m, mode in ((cs.ModelProfile(), cs.TrainingMode.CPA), (cs.ModelProfile.phi14b_like(), cs.TrainingMode.CPT)):
         ms = cs.MapSet.build(ctx, m, G, mode=mode)
