@@ -266,20 +266,6 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         const uint32_t k = k0 + lane;
                         const bool live = k < ob;
                         const double s = sT[b * 33 + 1 + lane] - sT[b * 33 + lane];
-                        if (P.bmeta_bins) {
-                            const uint32_t bn = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(s)) >> 42);
-                            const bool in = live && !(s < 0.0);
-                            uint32_t lo_b = in ? bn : 0xffffffffu, hi_b = in ? bn : 0u;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) {
-                                lo_b = min(lo_b, __shfl_xor_sync(FULL, lo_b, o));
-                                hi_b = max(hi_b, __shfl_xor_sync(FULL, hi_b, o));
-                            }
-                            if (lane == b) {
-                                bmin = min(bmin, lo_b);
-                                bmax = max(bmax, hi_b);
-                            }
-                        }
                         const bool slow = live && s > P.tau;
                         if (__ballot_sync(FULL, slow)) slowm |= 1u << b;
                         A.slow_tok += slow;
@@ -305,8 +291,16 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 if (tl) acc_fixed(A.acc, A.flags, now, 1u);
                 const uint64_t need = v ? serving_memory(m, static_cast<uint64_t>(pq) + oq, 1) : 0ull;
                 if (v && P.bmeta_bins) {
+                    // a conservative bin range without looking at the samples: d_k grows with k
+                    // (delta >= 0) and each sample is d_k within one rounding of the time (<= ulp(T_end))
+                    const double d_first = 0.0 + (gam + del * tq);
+                    const double d_last = 0.0 + (gam + del * (tq + static_cast<double>(oq - 1)));
+                    const double ue = fabs(now) * 0x1p-51 + 0x1p-1000;
+                    const double slo = d_first - ue - d_first * 0x1p-40, shi = d_last + ue + d_last * 0x1p-40;
+                    const uint32_t blo = slo > 0.0 ? static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(slo)) >> 42) : 0u;
+                    const uint32_t bhi = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(shi)) >> 42);
                     P.bmeta_start[lo + q] = aq + 0.0;
-                    P.bmeta_bins[lo + q] = (1ull << 63) | (1ull << 62) | (static_cast<uint64_t>(bmax) << 21) | bmin;
+                    P.bmeta_bins[lo + q] = (1ull << 63) | (1ull << 62) | (static_cast<uint64_t>(bhi) << 21) | blo;
                 }
                 if (v) {
                     const bool slowq = (slowm >> lane) & 1u;  // a lone query's tokens are every step
