@@ -207,25 +207,21 @@ __device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, ui
 }
 
 // hist[key] += cnt for every lane with act; lanes of the warp that share a key
-// add once (match + reduce), so consecutive decode steps of a batch, whose
-// TPT samples usually fall in one bin, cost one atomic.  Call from all lanes.
+// add once, so consecutive decode steps of a batch, whose TPT samples fall in
+// one or a few bins, cost one atomic per distinct bin: the warp takes the
+// distinct keys one at a time (the lowest active lane's key, a ballot of its
+// peers, one warp-wide REDUX of their counts).  Call from all lanes.
 __device__ __forceinline__ void hist_add(uint64_t* hist, uint32_t key, uint32_t cnt, bool act) {
-    const unsigned am = __ballot_sync(kFullMask, act);
-    if (!am) return;
-    const int first = __ffs(am) - 1;
-    const uint32_t k0 = __shfl_sync(kFullMask, key, first);
-    if (__all_sync(kFullMask, !act || key == k0)) {  // the common case: one bin for the whole warp
-        const unsigned total = __reduce_add_sync(kFullMask, act ? cnt : 0u);
-        if ((threadIdx.x & 31) == static_cast<unsigned>(first))
+    unsigned rem = __ballot_sync(kFullMask, act);
+    while (rem) {
+        const int ld = __ffs(rem) - 1;
+        const uint32_t k0 = __shfl_sync(kFullMask, key, ld);
+        const bool mine = act && key == k0;
+        const unsigned total = __reduce_add_sync(kFullMask, mine ? cnt : 0u);
+        if ((threadIdx.x & 31) == static_cast<unsigned>(ld))
             atomicAdd(reinterpret_cast<unsigned long long*>(&hist[k0]), static_cast<unsigned long long>(total));
-        return;
+        rem &= ~__ballot_sync(kFullMask, mine);
     }
-    if (!act) return;
-    const unsigned peers = __match_any_sync(am, key);
-    unsigned total = 0;  // sum over the peers by shuffles within the active mask
-    for (unsigned b = peers; b; b &= b - 1) total += __shfl_sync(peers, cnt, __ffs(b) - 1);
-    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(peers) - 1))
-        atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(total));
 }
 
 // Sequential f64 fold t = (((t + d0) + d1) + ...) over K durations staged in
