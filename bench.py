@@ -205,9 +205,21 @@ def run_reference(args, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": config(args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "cpu": cpu_model(),
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline_leg(prompt_h, output_h, offs_h):
@@ -215,7 +227,9 @@ def cpu_baseline_leg(prompt_h, output_h, offs_h):
     devices = list(range(DEVICES))
     reference_decide(prompt_h, output_h, offs_h, devices[:1], threads)  # warm
     n, t = reference_decide(prompt_h, output_h, offs_h, devices, threads)
-    return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference",
+    n1, t1 = reference_decide(prompt_h, output_h, offs_h, devices[:4], 1)  # the reference is single-threaded
+    return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference", "cpu": cpu_model(),
+            "single_thread": {"value": n1 / t1, "cores": 1, "sample": f"4 devices ({n1} queries), {t1:.2f} s"},
             "sample": f"the same GPU-generated C2 arrays, all 64 devices ({n} queries), {threads} host threads, "
                       f"oracle/_ref (reference headers compiled unchanged), {t:.2f} s"}
 
@@ -616,6 +630,7 @@ def run_colo(args, world, rank, local):
                     tr.append((mm, default_gpu(), cpa, a_h[lo:hi], p_h[lo:hi], o_h[lo:hi]))
                 nq, ts = reference_colocated(tr, threads)
                 line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "cpu": cpu_model(),
                                         "sample": f"{k} of the fleet's devices ({nq} queries), Simulation::run "
                                                   f"Colocated via oracle/_ref, {threads} host threads, {ts:.1f} s"}
             except Exception as e:
@@ -717,6 +732,7 @@ def run_c4(args, world, rank, local):
                 tr = reference_sample(arrival, prompt, output, offs, 16, 100_000, [default_model(), phi14b_model()])
                 nq, ts = reference_serving(tr, threads, with_stats=True)
                 line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "cpu": cpu_model(),
                                         "sample": f"first 100k queries of 16 of the rank's devices ({nq} queries), "
                                                   f"Simulation::run ServingOnly + finalize via oracle/_ref, "
                                                   f"{threads} host threads, {ts:.1f} s (the decision lookups "
@@ -815,6 +831,7 @@ def run_c3(args, world, rank, local):
                 tr = reference_sample(arrival, prompt, output, offs, 16, 250_000, [default_model(), phi14b_model()])
                 nq, ts = reference_serving(tr, threads)
                 line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                        "cpu": cpu_model(),
                                         "sample": f"first 250k queries of 16 of the C3 devices ({nq} queries), "
                                                   f"Simulation::run ServingOnly via oracle/_ref, {threads} host "
                                                   f"threads, {ts:.1f} s"}
