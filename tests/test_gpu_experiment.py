@@ -18,3 +18,34 @@ def test_harness_outputs_match_reference_cli_gpu(tmp_path):
 
 def test_cli_profile_matches_reference_cli(tmp_path):
     run_cli_profile(str(tmp_path))
+
+
+def test_cli_run_long_trace_segmented(tmp_path):
+    """`run` on a trace long enough for the colocated replay to split the
+    device into parallel segments (qps 0.3 for 20000 s, about 6000 queries):
+    report.csv / report.jsonl / tpt_cdf.csv byte-identical to the reference
+    CLI's (oracle/_ref/colosim, run live on the same config), in all three
+    modes."""
+    import os
+    import subprocess
+
+    from experiment_check import CLI
+
+    ref_bin = os.path.join(os.path.dirname(CLI), "..", "..", "oracle", "_ref", "colosim")
+    if not os.path.exists(ref_bin):
+        pytest.skip("oracle/_ref/colosim not built")
+    cfg = open(os.path.join(CLI, "small.config")).read()
+    cfg = cfg.replace("trace.qps = 0.12", "trace.qps = 0.3").replace("trace.duration = 900", "trace.duration = 20000")
+    cfg = cfg.replace("histogram:lengths.jsonl", "histogram:" + os.path.join(CLI, "lengths.jsonl"))
+    cp = tmp_path / "long.config"
+    cp.write_text(cfg)
+    eng = ex.GpuEngine(cs.Context(0))
+    for mode in ("", "baseline", "serving-only"):
+        dr, dg = tmp_path / f"ref{mode}", tmp_path / f"gpu{mode}"
+        args = [ref_bin, "run", "--config", str(cp), "--out", str(dr)] + (["--mode", mode] if mode else [])
+        subprocess.run(args, check=True, capture_output=True)
+        ex.cmd_run(eng, str(cp), str(dg), mode_override=mode)
+        names = sorted(os.listdir(dr))
+        assert names == sorted(os.listdir(dg)), (mode, names)
+        for nm in names:
+            assert (dr / nm).read_bytes() == (dg / nm).read_bytes(), (mode, nm)
