@@ -71,3 +71,15 @@ def test_finalize_empty_and_replay_samples(ctx):
     want, _ = ref_finalize(x.cpu().numpy())
     got = cs.finalize(ctx, x)
     assert np.array_equal(np.array(got).view(np.uint64), np.array(want).view(np.uint64))
+
+
+def test_finalize_contract_and_launch_counter(ctx):
+    x = torch.rand(5000, dtype=torch.float64, device="cuda")
+    with pytest.raises(cs.ColoInvalidArgument):
+        cs.finalize(ctx, x, sorted_out=torch.empty(10, dtype=torch.float64, device="cuda"))
+    # the library's own launch counter moves with every launch this context makes
+    l0 = ctx.launches()
+    cs.finalize(ctx, x)
+    assert ctx.launches() == l0 + 2  # k_fold_cand + k_fold_walk (the sort is CUB's)
+    st = cs.lib().colo_finalize(ctx.h, cs._ptr(x), 5000, cs._ptr(x), (cs.C.c_double * 4)())  # d_sorted aliases the input
+    assert st == 1  # COLO_EINVAL
