@@ -745,11 +745,21 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         auto member_pd = [&](uint64_t j) -> double { return staged ? S.pd[j] : static_cast<double>(pp[head + j]); };
         // prefill: left fold in batch order (engine.hpp:321-325); member 0 may be recording
         double dur = 0.0;
-        for (uint64_t j = 0; j < nb; ++j) {
-            const double t = member_pd(j);
-            double base = 1.0 * (m.prefill_coef_linear * t + m.prefill_coef_quad * t * t);
-            if (j == 0 && rec) base = base * m.record_prefill_multiplier;
-            dur += base;
+        if (staged) {
+#pragma unroll 4
+            for (uint64_t j = 0; j < nb; ++j) {
+                const double t = S.pd[j];
+                double base = 1.0 * (m.prefill_coef_linear * t + m.prefill_coef_quad * t * t);
+                if (j == 0 && rec) base = base * m.record_prefill_multiplier;
+                dur += base;
+            }
+        } else {
+            for (uint64_t j = 0; j < nb; ++j) {
+                const double t = member_pd(j);
+                double base = 1.0 * (m.prefill_coef_linear * t + m.prefill_coef_quad * t * t);
+                if (j == 0 && rec) base = base * m.record_prefill_multiplier;
+                dur += base;
+            }
         }
         const double start = now + stall;
         ++seq;  // PrefillDone
@@ -773,14 +783,29 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             double kd[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
-            for (uint64_t j = 0; j < nb; ++j) {
-                const uint32_t oj = staged ? S.po[j].y : po[head + j];
-                const double pj = member_pd(j);
+            if (staged) {  // members from shared memory, unrolled so loads overlap the accumulate chains
+#pragma unroll 4
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint32_t oj = S.po[j].y;
+                    const double pj = S.pd[j];
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    if (kb + 32 * r < oj) {
-                        dk[r] += gam + del * (pj + kd[r]);
-                        ++alive[r];
+                    for (int r = 0; r < 4; ++r) {
+                        if (kb + 32 * r < oj) {
+                            dk[r] += gam + del * (pj + kd[r]);
+                            ++alive[r];
+                        }
+                    }
+                }
+            } else {
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint32_t oj = po[head + j];
+                    const double pj = static_cast<double>(pp[head + j]);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (kb + 32 * r < oj) {
+                            dk[r] += gam + del * (pj + kd[r]);
+                            ++alive[r];
+                        }
                     }
                 }
             }
