@@ -348,6 +348,10 @@ def run_ours(args, world, rank, local):
 C3_DEVICES, C3_PER_DEVICE = 128, 7_812_500
 
 
+TUPLE_DTYPE_NP = np.dtype([("cached", "<u4"), ("incoming", "<u4"), ("charged", "<u4"), ("batch", "<u2"),
+                           ("pending", "u1"), ("dev_layers", "u1")])
+
+
 def run_c5(args, world, rank, local):
     """C5 (BASELINE.json configs[4]): grid steps {500,250,100,50} x profiles
     {llama8b, phi14b} x modes {CPT, CPA}; per point the batched quantised map
@@ -406,6 +410,33 @@ def run_c5(args, world, rank, local):
                 "config": {"workload": f"C5: 16 sweep points x {total} questions (steps 500/250/100/50 x llama8b/phi14b x CPT/CPA)",
                            "parallelism": f"dp{world}"},
                 "exact_value": n_done / t_exact, "points": rows}
+        if world == 1 and not args.no_cpu_baseline:
+            try:  # the reference's composed lookup and exact decision on 16M of the same questions, all threads
+                from oracle.oracle import OracleLib, Grid, default_gpu, default_model
+
+                ref = OracleLib("ref")
+                threads = os.cpu_count() or 1
+                om = default_model()
+                tup = cs.synth_tuples(ctx, 16_000_000, om.num_layers, 1).cpu().numpy().view(TUPLE_DTYPE_NP).reshape(-1)
+                parts = np.array_split(tup, threads)
+                grid = Grid(500, 500, 5, 8000, 8000, 50)
+                t0 = time.perf_counter()
+                with ThreadPoolExecutor(threads) as ex:
+                    list(ex.map(lambda t: ref.decide(om, default_gpu(), grid, 1, t), parts))
+                tmap = time.perf_counter() - t0
+                t0 = time.perf_counter()
+                with ThreadPoolExecutor(threads) as ex:
+                    list(ex.map(lambda t: ref.decide_exact(om, default_gpu(), 1, t), parts))
+                tex = time.perf_counter() - t0
+                line["cpu_baseline"] = {"value": len(tup) / tmap, "unit": "decisions/s", "cores": threads,
+                                        "kind": "reference", "cpu": cpu_model(), "exact_value": len(tup) / tex,
+                                        "sample": f"16M of the step-500 llama8b CPA questions, OffloadingMap/HedgingMap "
+                                                  f"lookups composed as apply_offload_decision ({tmap:.2f} s) and "
+                                                  f"offload_cell_decision + direct hedge ({tex:.2f} s), oracle/_ref, "
+                                                  f"{threads} host threads"}
+            except Exception as e:
+                line["cpu_baseline"] = {"value": None, "unit": "decisions/s", "cores": 0, "kind": "reference",
+                                        "sample": f"unavailable: {e}"}
         print(json.dumps(line), flush=True)
     ctx.close()
 
