@@ -124,7 +124,7 @@ struct DecideParams {
 
 template <bool SMEM, bool COUNT>
 __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ DecideParams P) {
-    extern __shared__ __align__(16) uint8_t sm[];
+    extern __shared__ __align__(128) uint8_t sm[];  // (one alignment for the TU's dynamic shared memory)
     const MapView mv = P.mv;  // by value: the fields live in registers / uniform registers
     const uint8_t* off = mv.off;
     const uint8_t* hed = mv.hed;

@@ -16,8 +16,6 @@ using namespace colo;
 
 namespace {
 
-constexpr int kThreads = 256;
-
 // ---------------------------------------------------------------- map build
 // build_offloading_map, maps.hpp:233-252: one thread per cell, cell (ci,ii,bi)
 // evaluated at (ci*sc, (ii+1)*si, (bi+1)*sb), row-major.
