@@ -433,6 +433,21 @@ colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, 
                                  const uint64_t* d_dev_offsets, const uint16_t* d_dev_set, size_t ndev,
                                  const colo_colocated_opts* opts, double* pctl, colo_colocated_summary* totals);
 
+/* The event log of one device's Simulation::run (tools/colosim.cpp --emit-events;
+ * LoggedEvent::to_json, engine.hpp:109-129, 241-244) in SimMode::ServingOnly or
+ * Colocated: the run on the GPU records every logged event, which are put in
+ * dispatch order ((time, sequence), engine.hpp:184-187) and formatted as the
+ * reference formats them.  d_label_delay may be NULL (default_label_delay for
+ * every query; < 0 = never); d_query_id may be NULL (ids 0..n-1).  Returns the
+ * length of the JSON-lines text, kept in the context (colo_events_text), or
+ * -status (EBREACH: the run breached, as the reference throws). */
+int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mode, double cache_timeout,
+                              const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output,
+                              const double* d_label_delay, double default_label_delay, const uint64_t* d_query_id,
+                              size_t n, double tau);
+/* Copies the last event log (NUL-terminated) when cap exceeds its length; returns the length. */
+int64_t colo_events_text(colo_ctx* ctx, char* out, size_t cap);
+
 /* ------------------------------------------------------------ report helpers */
 /* Trace::content_hash (workload.hpp:140-161): FNV-1a over (query_id, arrival
  * bits, prompt, output, label_delay bits -- -1.0 for nullopt) per record.

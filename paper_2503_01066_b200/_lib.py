@@ -178,7 +178,7 @@ EXPORTS = [
     "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
     "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats", "colo_trace_hash",
     "colo_sort_f64", "colo_json_doubles", "colo_ctx_release_scratch", "colo_stats_allreduce",
-    "colo_serving_stats_nccl", "colo_finalize", "colo_ctx_launches",
+    "colo_serving_stats_nccl", "colo_finalize", "colo_ctx_launches", "colo_colocated_events", "colo_events_text",
 ]
 
 
@@ -240,6 +240,8 @@ def lib() -> C.CDLL:
         "colo_sort_f64": (i32, [vp, vp, vp, sz]),
         "colo_finalize": (i32, [vp, vp, sz, vp, vp]),
         "colo_ctx_launches": (u64, [vp]),
+        "colo_colocated_events": (C.c_int64, [vp, vp, i32, dbl, vp, vp, vp, vp, dbl, vp, sz, dbl]),
+        "colo_events_text": (C.c_int64, [vp, C.c_char_p, sz]),
         "colo_json_doubles": (C.c_int64, [vp, sz, C.c_char_p, sz]),
         "colo_replay_colocated": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts)]),
         "colo_colocated_stats": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts), vp,

@@ -920,6 +920,28 @@ def finalize(ctx: Context, samples, sorted_out=None) -> list:
     return list(out)
 
 
+def colocated_events(ctx: Context, mapset: MapSet, arrival, prompt, output, label_delay=None,
+                     default_label_delay: float = 0.01, query_id=None, cache_timeout: float = 60.0,
+                     sim_mode=None, tau: float = math.inf) -> str:
+    """colo_colocated_events: the event log of one device's Simulation::run
+    (tools/colosim.cpp --emit-events) in ServingOnly or Colocated mode, as the
+    reference's JSON lines (LoggedEvent::to_json, engine.hpp:109-129).
+    Device tensors: arrival f64, prompt/output int32, label_delay f64
+    (optional), query_id int64 (optional)."""
+    _need_cuda(arrival, "arrival", 8)
+    _need_cuda(prompt, "prompt", 4)
+    _need_cuda(output, "output", 4)
+    n = prompt.shape[0]
+    mode = int(SimMode.COLOCATED if sim_mode is None else sim_mode)
+    ln = lib().colo_colocated_events(ctx.h, mapset.h, mode, cache_timeout, _ptr(arrival), _ptr(prompt), _ptr(output),
+                                     _ptr(label_delay), default_label_delay, _ptr(query_id), n, tau)
+    if ln < 0:
+        check(-ln, ctx.h, "colocated_events")
+    buf = C.create_string_buffer(int(ln) + 1)
+    lib().colo_events_text(ctx.h, buf, int(ln) + 1)
+    return buf.raw[: int(ln)].decode()
+
+
 def colocated_stats(ctx: Context, sets: Sequence[MapSet], arrival, prompt, output, dev_offsets, dev_set,
                     label_delay=None, default_label_delay: float = 0.01, cache_timeout: float = 60.0,
                     tau: float = math.inf, sim_mode=None, seg_len=None):

@@ -122,6 +122,21 @@ struct SegOut {
     uint64_t nlog[3];
 };
 
+// Event log (tools/colosim.cpp --emit-events, engine.hpp:109-129, 241-244):
+// the kernel appends one record per logged event; the dispatch order is the
+// (time, sequence) order of the handled events, so the host sorts records by
+// (t, seq, sub) -- sub orders several records logged inside one handler --
+// and a store-teardown marker drops CopyDone records of torn-down stores
+// (engine.hpp:798-805).  Kinds follow EventKind (engine.hpp:78-90).
+enum { EV_ARRIVAL = 0, EV_PREFILL, EV_STEP, EV_QDONE, EV_LABEL, EV_TIMEOUT, EV_RESUME, EV_BWD, EV_FWD, EV_LOAD,
+       EV_COPY, EV_TEARDOWN = 100 };
+struct EvRec {
+    double t, start, dur;
+    uint64_t key;  // seq << 16 | sub
+    int64_t a, b;
+    uint32_t kind, gen;
+};
+
 struct CoParams {
     CoProfile prof[kMaxSets];
     MapView sets[kMaxSets];
@@ -150,6 +165,11 @@ struct CoParams {
     // segmented runs (NULL tasks: warp w = device w, whole trace)
     const SegTask* tasks;
     uint32_t ntasks;
+    EvRec* evlog;      // event log (LOG instantiation): records, their count and capacity
+    unsigned long long* evcnt;
+    uint64_t evcap;
+    const uint64_t* qid;  // query ids (device-local index -> id) for the log
+    double* lstart;       // LOG: [device][kLayerCap] start times of the current prefetch plan's loads
     SegSpec* spec;     // [task] (SPEC)
     SegOut* segout;    // [task] (OUT)
     double* log[3];    // addends of training_busy_time, copy_stall_seconds, prefetch_wait_seconds (OUT)
@@ -182,7 +202,7 @@ __device__ __forceinline__ double warp_max_f64(double v) {
 
 // SEG = false: warp w is device w over its whole trace (no segment code at all);
 // SEG = true: warp w runs P.tasks[w] (whole-trace, speculative or output segment)
-template <bool SEG>
+template <bool SEG, bool LOG = false>
 __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constant__ CoParams P) {
     __shared__ WarpSmem SM[kWarpsC];
     const uint32_t wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -231,6 +251,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     bool sbusy = false;
     double s_t = 0.0;
     uint64_t s_seq = 0, bfirst = 0, bn = 0, bneed = 0;
+    uint32_t s_nlast = 0;  // LOG: members that finish at the batch's last step
     // slot
     bool has_store = false, qcompleted = false, stream = false;
     uint64_t src = 0, prompt_kv = 0, kv_held = 0, cached_tokens = 0, gen = 0, store_gen = 0, plan_gen = 0;
@@ -240,7 +261,11 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     uint64_t jp = 0, jo = 0, pass0 = 0, pass1 = 0, pass2 = 0, npasses = 0, pass_index = 0, cursor = 0;
     int64_t kv_charged = -1;
     double wait_since = 0.0, plb = 0.0, tbusy = 0.0;  // plb = per_layer_backward(job) (engine.hpp:614-618)
-    double t_t = 0.0, t_dur = 0.0;
+    double t_t = 0.0, t_dur = 0.0, t_st = 0.0;  // t_st: when the in-flight layer was scheduled (LOG)
+    uint32_t t_pb = 0;                          // ... and its pass index (ForwardLayerDone b)
+    double h_t = 0.0;  // LOG: the handled event's time and sequence, and the next sub-position in it
+    uint64_t h_seq = 0;
+    uint32_t h_sub = 0;
     uint64_t t_seq = 0;
     bool t_fwd = false;
     uint32_t t_a = 0;
@@ -310,6 +335,27 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         if (tmode == TM_OUT && lane == 0 && nl2 < P.tasks[w].expect[4]) P.log[2][P.tasks[w].log_base[2] + nl2] = x;
         ++nl2;
     };
+    // LOG: append one record from this lane (callers pick the lane)
+    auto emit_from = [&](bool me, uint32_t kind, double t, uint64_t sq, uint32_t sub, int64_t a, int64_t b, double st,
+                         double du, uint32_t g) {
+        if (!LOG || !me) return;
+        const unsigned long long i = atomicAdd(P.evcnt, 1ull);
+        if (i < P.evcap) {
+            EvRec r;
+            r.t = t;
+            r.start = st;
+            r.dur = du;
+            r.key = (sq << 16) | sub;
+            r.a = a;
+            r.b = b;
+            r.kind = kind;
+            r.gen = g;
+            P.evlog[i] = r;
+        }
+    };
+    auto emit = [&](uint32_t kind, double t, uint64_t sq, uint32_t sub, int64_t a, int64_t b, double st, double du,
+                    uint32_t g) { emit_from(lane == 0, kind, t, sq, sub, a, b, st, du, g); };
+    auto qid_of = [&](uint64_t j) -> int64_t { return static_cast<int64_t>(P.qid ? P.qid[lo + j] : j); };
     auto pass_tok = [&](uint64_t i) -> uint64_t { return i == 0 ? pass0 : (i == 1 ? pass1 : pass2); };
     uint64_t cur_tok = 0;  // passes[pass_index] of the running forward pass (set by begin_pass)
     auto fwd_layer = [&](uint64_t t) -> double {  // cost_model.hpp:39-41
@@ -370,6 +416,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     };
     auto teardown = [&]() {  // engine.hpp:468-479
         if (!has_store) return;
+        emit(EV_TEARDOWN, h_t, h_seq, 0xff00u, 0, 0, 0.0, 0.0, static_cast<uint32_t>(gen));
         uint64_t s = 0;
         for (uint32_t l = lane; l < L; l += 32)
             if (S.flg[l] & LF_DEV) {
@@ -403,6 +450,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         d2h_busy = start + cp_val;
         if (lane == (l & 31)) S.lcd[l] = d2h_busy;
         set_layer(l, f, r);
+        emit(EV_COPY, d2h_busy, seq, 0, l, static_cast<int64_t>(bytes), t, d2h_busy - t, static_cast<uint32_t>(gen));
         ++seq;
     };
     // engine.hpp:563-610
@@ -464,6 +512,8 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         tinf = true;
         t_fwd = true;
         t_a = static_cast<uint32_t>(cursor);
+        t_st = now;
+        t_pb = static_cast<uint32_t>(pass_index);
         t_t = now + t_dur;
         t_seq = seq++;
     };
@@ -494,6 +544,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         tinf = true;
         t_fwd = false;
         t_a = static_cast<uint32_t>(cursor);
+        t_st = now;
         t_t = now + t_dur;
         t_seq = seq++;
     };
@@ -513,16 +564,21 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 dur = static_cast<double>(r) / static_cast<double>(pf.h2d);
             }
             const uint32_t bal = __ballot_sync(kFullMask, el);
-            double mine = 0.0;
+            double mine = 0.0, mine0 = 0.0;
             for (uint32_t b = bal; b; b &= b - 1) {  // channel += dur, descending layer order
                 const int j = __ffs(b) - 1;
+                const double before = channel;
                 channel += __shfl_sync(kFullMask, dur, j);
-                if (lane == static_cast<uint32_t>(j)) mine = channel;
+                if (lane == static_cast<uint32_t>(j)) {
+                    mine0 = before;
+                    mine = channel;
+                }
             }
             if (el) {
                 const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
                 S.llayer[pos] = static_cast<uint16_t>(l);
                 S.ldone[pos] = mine;
+                if (LOG) P.lstart[static_cast<uint64_t>(d) * kLayerCap + pos] = mine0;  // LoadDone start
             }
             cnt += __popc(bal);
         }
@@ -536,6 +592,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
     };
     auto try_start_training = [&]() {  // engine.hpp:633-660
         if (!has_job || sbusy || qhead != ai || tinf) return;
+        if (phase != PH_WAIT) emit(EV_RESUME, h_t, h_seq, h_sub++, qid_of(src), 0, h_t, 0.0, 0u);
         switch (phase) {
             case PH_WAIT: return;
             case PH_READY:
@@ -762,6 +819,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             }
         }
         const double start = now + stall;
+        const uint64_t pf_seq = seq;
         ++seq;  // PrefillDone
         if (rec) {  // engine.hpp:332-350
             const uint64_t per_layer = static_cast<uint64_t>(pp[head]) * m.act_bytes_per_token_per_layer;
@@ -772,6 +830,13 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 record(l, per_layer, seg_ready);
             }
             training_peak();
+        }
+        const uint64_t step_seq0 = seq;  // DecodeStepDone k takes step_seq0 + k (see the header)
+        emit(EV_PREFILL, start + dur, pf_seq, 0, static_cast<int64_t>(nb), 0, start, dur, 0u);
+        if (LOG) {  // QueryDone records: each member at its last step, in batch order among that step's finishers
+            uint32_t nl = 0;
+            for (uint64_t j = lane; j < nb; j += 32) nl += (staged ? S.po[j].y : po[head + j]) == maxo;
+            s_nlast = static_cast<uint32_t>(warp_sum_u64(nl));
         }
         double tnow = start + dur;  // PrefillDone time: every member's last_token_time
         // decode steps (engine.hpp:358-387), four 32-step windows per pass
@@ -822,6 +887,22 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             for (int r = 0; r < 4; ++r) {  // sample = now - last_token_time
                 const uint32_t i = 32 * r + lane;
                 if (i < cnt) sv[r] = S.dk[i] - (i ? S.dk[i - 1] : tnow);
+            }
+            if (LOG) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t i = 32 * r + lane;
+                    emit_from(i < cnt, EV_STEP, i < cnt ? S.dk[i] : 0.0, step_seq0 + k0 + i, 0, 0, 0,
+                              i < cnt ? (i ? S.dk[i - 1] : tnow) : 0.0, dk[r], 0u);
+                }
+                for (uint64_t j = lane; j < nb; j += 32) {
+                    const uint32_t oj = staged ? S.po[j].y : po[head + j];
+                    if (oj - 1 < k0 || oj - 1 >= k0 + cnt) continue;
+                    uint32_t rank = 0;
+                    for (uint64_t jj = 0; jj < j; ++jj) rank += (staged ? S.po[jj].y : po[head + jj]) == oj;
+                    const double tf = S.dk[oj - 1 - k0];
+                    emit_from(true, EV_QDONE, tf, step_seq0 + oj - 1, 1 + rank, qid_of(head + j), 0, tf, 0.0, 0u);
+                }
             }
             tnow = S.dk[cnt - 1];
             if (separate) {
@@ -1016,6 +1097,9 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                     }
                 }
             }
+            h_t = na;  // LOG: this arrival's handler (its QueryArrival record comes from k_log_arrivals)
+            h_seq = ai;
+            h_sub = 1;
             now = na;
             ++ai;
             na = ai < N ? arr[ai] : 0.0;
@@ -1031,7 +1115,11 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         } else {
         if (bk == EK_NONE) break;
         now = bt;
+        h_t = bt;  // LOG: the handled event; sub 0 is its own record
+        h_seq = bs;
+        h_sub = 1;
         if (bk == EK_SERVE) {  // the batch's last DecodeStepDone (engine.hpp:367-408)
+            h_sub = 1 + s_nlast;  // after the QueryDone records of the last step
             uint64_t release = bneed;
             if (has_store && !qcompleted && src >= bfirst && src < bfirst + bn) {
                 qcompleted = true;
@@ -1050,6 +1138,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                         l_t = now + ldl;
                         l_seq = seq++;
                         l_gen = gen;
+                        emit(EV_LABEL, l_t, l_seq, 0, static_cast<int64_t>(gen), qid_of(src), l_t, 0.0, 0u);
                     }
                 }
             }
@@ -1059,6 +1148,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         } else if (bk == EK_TRAIN) {
             tinf = false;
             add_busy(t_dur);
+            emit(t_fwd ? EV_FWD : EV_BWD, t_t, t_seq, 0, t_a, t_fwd ? static_cast<int64_t>(t_pb) : 0, t_st, t_dur, 0u);
             if (t_fwd) {  // engine.hpp:693-722
                 const uint64_t bytes = cur_tok * m.act_bytes_per_token_per_layer;
                 if (stream && S.rec[cursor] == 0) ++r_freed;
@@ -1104,11 +1194,16 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
         } else if (bk == EK_TIMEOUT) {  // engine.hpp:498-505
             to_on = false;
             if (has_store && gen == to_gen && has_job && phase == PH_WAIT) {
+                emit(EV_TIMEOUT, bt, bs, 0, static_cast<int64_t>(to_gen), 0, bt, 0.0, 0u);
                 ++r_dropped;
                 teardown();
             }
         } else {  // EK_LOAD, engine.hpp:781-797
             const uint32_t a = S.llayer[ld_cur];
+            if (LOG) {
+                const double ls = P.lstart[static_cast<uint64_t>(d) * kLayerCap + ld_cur];
+                emit(EV_LOAD, bt, bs, 0, a, 0, ls, bt - ls, 0u);
+            }
             ++ld_cur;
             const uint64_t r = S.rec[a];
             if (!led_alloc(r)) breach = true;
@@ -1514,6 +1609,24 @@ __global__ void __launch_bounds__(32) k_seg_combine(const __grid_constant__ CoPa
     r.tpt_sum[2] = acc[2];
     r.flags = flags;
     P.summary[sd.dev] = r;
+}
+
+// QueryArrival records (engine.hpp:270-276): state-independent, one per query
+__global__ void k_log_arrivals(const double* __restrict__ arr, const uint64_t* __restrict__ qid, uint64_t n,
+                               EvRec* __restrict__ out) {
+    for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < n;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        EvRec r;
+        r.t = arr[q];
+        r.start = arr[q];
+        r.dur = 0.0;
+        r.key = q << 16;
+        r.a = static_cast<int64_t>(qid ? qid[q] : q);
+        r.b = 0;
+        r.kind = EV_ARRIVAL;
+        r.gen = 0;
+        out[q] = r;
+    }
 }
 
 size_t align256c(size_t x) { return (x + 255) & ~size_t(255); }
@@ -2021,6 +2134,142 @@ colo_status colo_replay_colocated(colo_ctx* ctx, const colo_mapset* const* sets,
     }
     if (flag & 2) return set_err(ctx, COLO_EBREACH, "colocated replay: invariant breach on at least one device");
     return COLO_OK;
+}
+
+int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mode, double cache_timeout,
+                              const double* d_arrival, const uint32_t* d_prompt, const uint32_t* d_output,
+                              const double* d_label_delay, double default_label_delay, const uint64_t* d_query_id,
+                              size_t n, double tau) {
+    if (!ctx || !set || (n && (!d_arrival || !d_prompt || !d_output))) return -COLO_EINVAL;
+    if (sim_mode != COLO_SIM_SERVING_ONLY && sim_mode != COLO_SIM_COLOCATED)
+        return -set_err(ctx, COLO_EINVAL, "event log: ServingOnly and Colocated runs only");
+    if (n >= (1ull << 40)) return -set_err(ctx, COLO_EINVAL, "event log: trace too long");
+    ctx->evtext.clear();
+    {
+        const colo_status st = colo_validate_profile_pair(&set->m, &set->g);
+        if (st != COLO_OK) return -set_err(ctx, st, "profile pair rejected (profiles.hpp:129-134)");
+    }
+    if (set->hash != colo_profile_hash(&set->m, &set->g))
+        return -set_err(ctx, COLO_EVALIDATION, "sim config: map profile hash does not match the profiles");
+    if (set->m.num_layers > kMaxLayers) return -set_err(ctx, COLO_EINVAL, "num_layers > 253");
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return -cuda_err(ctx, cudaGetLastError(), "cudaSetDevice");
+    CoParams P{};
+    CoProfile& pf = P.prof[0];
+    pf.m = set->m;
+    pf.cap = set->g.capacity_bytes;
+    pf.budget = set->g.capacity_bytes - set->g.runtime_reserve_bytes - set->m.weights_bytes;
+    pf.fixed = set->m.weights_bytes + set->g.runtime_reserve_bytes;
+    pf.h2d = set->g.h2d_bandwidth;
+    pf.d2h = set->g.d2h_bandwidth;
+    pf.cpa = set->mode == COLO_CPA ? 1u : 0u;
+    pf.L = static_cast<uint32_t>(set->m.num_layers);
+    P.sets[0] = make_view(set);
+    // device scratch: offsets, set index, mode, lstart, then the records
+    size_t cap = n * 8 + 65536;  // records (grown and re-run when the run logs more)
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        const size_t o_off = 0, o_set = 64, o_mode = 128, o_ls = 256, o_ev = o_ls + align256c(kLayerCap * 8);
+        const size_t bytes = o_ev + (n + cap) * sizeof(EvRec);
+        {
+            const colo_status st = grow_buf(ctx, ctx->d_seglog, ctx->seglog_bytes, bytes);
+            if (st != COLO_OK) return -st;
+        }
+        auto* base = static_cast<uint8_t*>(ctx->d_seglog);
+        const uint64_t off[2] = {0, n};
+        const uint16_t dset = 0;
+        const uint8_t md = static_cast<uint8_t>(sim_mode);
+        if (cudaMemcpyAsync(base + o_off, off, 16, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaMemcpyAsync(base + o_set, &dset, 2, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaMemcpyAsync(base + o_mode, &md, 1, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+            return -cuda_err(ctx, cudaGetLastError(), "event log setup");
+        P.arr = d_arrival;
+        P.p = d_prompt;
+        P.o = d_output;
+        P.ld = d_label_delay;
+        P.ld_default = default_label_delay;
+        P.dev_off = reinterpret_cast<const uint64_t*>(base + o_off);
+        P.dev_set = reinterpret_cast<const uint16_t*>(base + o_set);
+        P.sim_mode = base + o_mode;
+        P.ndev = 1;
+        P.timeout = cache_timeout;
+        P.tau = tau;
+        P.err = ctx->d_flag;
+        P.qid = d_query_id;
+        P.lstart = reinterpret_cast<double*>(base + o_ls);
+        P.evlog = reinterpret_cast<EvRec*>(base + o_ev);
+        P.evcap = n + cap;
+        P.evcnt = reinterpret_cast<unsigned long long*>(ctx->d_counters);
+        const unsigned long long start_cnt = n;  // the arrival records come first
+        if (cudaMemcpyAsync(P.evcnt, &start_cnt, 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->stream) != cudaSuccess)
+            return -cuda_err(ctx, cudaGetLastError(), "event log setup");
+        COLO_LAUNCHED(ctx);
+        k_co_validate<<<1, 128, 0, ctx->stream>>>(P);
+        int flag = 0;
+        cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -cuda_err(ctx, cudaGetLastError(), "validate");
+        if (flag)
+            return -set_err(ctx, COLO_EVALIDATION,
+                            "trace rejected: unsorted arrivals, zero tokens, or a query that cannot fit the device alone");
+        if (n) {
+            COLO_LAUNCHED(ctx);
+            k_log_arrivals<<<static_cast<uint32_t>(std::min<uint64_t>((n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
+                d_arrival, d_query_id, n, P.evlog);
+        }
+        COLO_LAUNCHED(ctx);
+        k_colocated<false, true><<<1, kWarpsC * 32, 0, ctx->stream>>>(P);
+        unsigned long long cnt = 0;
+        cudaMemcpyAsync(&cnt, P.evcnt, 8, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -cuda_err(ctx, cudaGetLastError(), "event log");
+        if (flag & 2) return -set_err(ctx, COLO_EBREACH, "event log: the run breached an invariant (no log)");
+        if (cnt > n + cap) {  // more records than room: grow and run again
+            cap = static_cast<size_t>(cnt) * 5 / 4 + 65536;
+            continue;
+        }
+        std::vector<EvRec> ev(cnt);
+        if (cnt && cudaMemcpy(ev.data(), P.evlog, cnt * sizeof(EvRec), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return -cuda_err(ctx, cudaGetLastError(), "event log D2H");
+        // dispatch order: (time, sequence, position inside the handler); times are >= 0 here
+        std::stable_sort(ev.begin(), ev.end(), [](const EvRec& x, const EvRec& y) {
+            return x.t < y.t || (x.t == y.t && x.key < y.key);
+        });
+        std::vector<uint32_t> dead;  // torn-down store generations: their later CopyDone events are no-ops
+        std::string out;
+        out.reserve(ev.size() * 120);
+        static const char* const kNames[] = {"QueryArrival", "PrefillDone", "DecodeStepDone", "QueryDone",
+                                             "LabelArrival", "CacheTimeout", "TrainingResume", "BackwardLayerDone",
+                                             "ForwardLayerDone", "LoadDone", "CopyDone"};
+        static const char kLane[] = {'-', 's', 's', '-', '-', '-', '-', 't', 't', 'x', 'x'};
+        unsigned long long lseq = 0;
+        char buf[320];
+        for (const EvRec& r : ev) {
+            if (r.kind == EV_TEARDOWN) {
+                dead.push_back(r.gen);
+                continue;
+            }
+            if (r.kind == EV_COPY && std::find(dead.begin(), dead.end(), r.gen) != dead.end()) continue;
+            if (r.kind > EV_COPY) continue;
+            const int k = std::snprintf(buf, sizeof buf,
+                                        "{\"t\":%.9f,\"seq\":%llu,\"kind\":\"%s\",\"a\":%lld,\"b\":%lld,"
+                                        "\"start\":%.9f,\"dur\":%.9f,\"lane\":\"%c\"}\n",
+                                        r.t, lseq++, kNames[r.kind], static_cast<long long>(r.a),
+                                        static_cast<long long>(r.b), r.start, r.dur, kLane[r.kind]);
+            out.append(buf, static_cast<size_t>(k));
+        }
+        ctx->evtext.swap(out);
+        return static_cast<int64_t>(ctx->evtext.size());
+    }
+    return -set_err(ctx, COLO_EINVAL, "event log: could not size the record buffer");
+}
+
+int64_t colo_events_text(colo_ctx* ctx, char* out, size_t cap) {
+    if (!ctx) return -COLO_EINVAL;
+    const size_t len = ctx->evtext.size();
+    if (out && cap > len) {
+        std::memcpy(out, ctx->evtext.data(), len);
+        out[len] = '\0';
+    }
+    return static_cast<int64_t>(len);
 }
 
 colo_status colo_sort_f64(colo_ctx* ctx, const double* d_in, double* d_out, size_t n) {

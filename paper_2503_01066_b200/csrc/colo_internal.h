@@ -16,6 +16,7 @@ struct colo_ctx {
     cudaStream_t stream = nullptr;  // current stream (own or caller's)
     cudaStream_t aux = nullptr;     // second stream for the host-buffer pipelines
     std::string err;
+    std::string evtext;             // the last colo_colocated_events log (JSON lines)
     int* d_flag = nullptr;          // device error flag (replay validation)
     // host-pipeline scratch (lazily grown)
     void* d_pipe = nullptr;

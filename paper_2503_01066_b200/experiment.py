@@ -416,6 +416,19 @@ class GpuEngine:
     def run(self, runs: Sequence[Run], sort_on_gpu: bool = True) -> List[dict]:
         return run_simulations(self.ctx, runs, sort_on_gpu)
 
+    def events(self, run: Run) -> str:
+        """The run's event log (colo_colocated_events)."""
+        import torch
+
+        t = run.trace
+        T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dt)).cuda()
+        return cs.colocated_events(self.ctx, run.maps, T(t.arrival, np.float64),
+                                   T(np.asarray(t.prompt, np.uint32).view(np.int32), np.int32),
+                                   T(np.asarray(t.output, np.uint32).view(np.int32), np.int32),
+                                   label_delay=T(t.label_delay, np.float64),
+                                   query_id=T(np.asarray(t.query_id, np.uint64).view(np.int64), np.int64),
+                                   cache_timeout=run.cache_timeout, sim_mode=run.mode)
+
 
 def _engine(e):
     return e if hasattr(e, "run") else GpuEngine(e)
@@ -617,9 +630,7 @@ def load_config(engine, path, offload_map_path="", hedge_map_path=""):
 
 def cmd_run(engine, config_path, out_dir, trace_path="", offload_map_path="", hedge_map_path="", seed_override=-1,
             mode_override="", emit_events=False, force=False) -> dict:
-    """tools/colosim.cpp:97-131 (the event log is not produced by this build)."""
-    if emit_events:
-        raise ColoValidationError(_lib.COLO_EVALIDATION, "--emit-events: the GPU engine keeps no event log")
+    """tools/colosim.cpp:97-131 (--emit-events: ServingOnly and Colocated runs)."""
     eng = _engine(engine)
     ec, maps = load_config(eng, config_path, offload_map_path, hedge_map_path)
     if mode_override:
@@ -630,11 +641,17 @@ def cmd_run(engine, config_path, out_dir, trace_path="", offload_map_path="", he
     if trace_path:
         ec.trace_spec.file = _resolve(trace_path)
     trace = ec.trace_spec.realize()
-    rep = eng.run([Run(ec.model, ec.gpu, ec.mode, ec.training, maps, trace, ec.cache_timeout)])[0]
+    run = Run(ec.model, ec.gpu, ec.mode, ec.training, maps, trace, ec.cache_timeout)
+    if emit_events and (not hasattr(eng, "events") or ec.mode == cs.SimMode.SEPARATE_CLUSTER):
+        raise ColoValidationError(_lib.COLO_EVALIDATION, "--emit-events: ServingOnly and Colocated runs only")
+    rep = eng.run([run])[0]
     os.makedirs(out_dir, exist_ok=True)
     export_csv(rep, _out_file(out_dir, "report.csv", force))
     export_jsonl(rep, _out_file(out_dir, "report.jsonl", force))
     export_tpt_cdf(rep, _out_file(out_dir, "tpt_cdf.csv", force))
+    if emit_events:  # tools/colosim.cpp:121
+        with open(_out_file(out_dir, "events.jsonl", force), "w", newline="") as f:
+            f.write(eng.events(run))
     return rep
 
 

@@ -49,3 +49,39 @@ def test_cli_run_long_trace_segmented(tmp_path):
         assert names == sorted(os.listdir(dg)), (mode, names)
         for nm in names:
             assert (dr / nm).read_bytes() == (dg / nm).read_bytes(), (mode, nm)
+
+
+@pytest.mark.parametrize("variant", ["small", "timeout5", "cap48_d2h2", "cpa_label0", "cpt_label0"])
+def test_cli_emit_events_matches_reference(tmp_path, variant):
+    """`run --emit-events`: events.jsonl byte-identical to the reference CLI's
+    (LoggedEvent::to_json in dispatch order) for Colocated and ServingOnly runs,
+    including cache timeouts, prefetch loads, training resumes and zero label
+    delays."""
+    import os
+    import subprocess
+
+    from experiment_check import CLI
+
+    ref_bin = os.path.join(os.path.dirname(CLI), "..", "..", "oracle", "_ref", "colosim")
+    if not os.path.exists(ref_bin):
+        pytest.skip("oracle/_ref/colosim not built")
+    cfg = open(os.path.join(CLI, "small.config")).read()
+    cfg = cfg.replace("histogram:lengths.jsonl", "histogram:" + os.path.join(CLI, "lengths.jsonl"))
+    cfg = {"small": cfg,
+           "timeout5": cfg.replace("sim.cache_timeout = 60", "sim.cache_timeout = 5"),
+           "cap48_d2h2": cfg.replace("gpu.capacity_bytes = 85899345920", "gpu.capacity_bytes = 51539607552")
+                            .replace("gpu.d2h_bandwidth = 24000000000", "gpu.d2h_bandwidth = 2000000000")
+                            .replace("gpu.h2d_bandwidth = 24000000000", "gpu.h2d_bandwidth = 4000000000"),
+           "cpa_label0": cfg.replace("trace.label_delay = uniform:0,30", "trace.label_delay = fixed:0"),
+           "cpt_label0": cfg.replace("sim.training = cpa", "sim.training = cpt")
+                            .replace("trace.label_delay = uniform:0,30", "trace.label_delay = fixed:0")}[variant]
+    cp = tmp_path / "v.config"
+    cp.write_text(cfg)
+    eng = ex.GpuEngine(cs.Context(0))
+    for mode in ("", "serving-only"):
+        dr, dg = tmp_path / f"ref{mode}", tmp_path / f"gpu{mode}"
+        subprocess.run([ref_bin, "run", "--config", str(cp), "--out", str(dr), "--emit-events"] +
+                       (["--mode", mode] if mode else []), check=True, capture_output=True)
+        ex.cmd_run(eng, str(cp), str(dg), mode_override=mode, emit_events=True)
+        for nm in ("events.jsonl", "report.csv", "report.jsonl", "tpt_cdf.csv"):
+            assert (dr / nm).read_bytes() == (dg / nm).read_bytes(), (variant, mode, nm)
