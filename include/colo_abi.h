@@ -434,8 +434,7 @@ colo_status colo_colocated_stats(colo_ctx* ctx, const colo_mapset* const* sets, 
                                  const colo_colocated_opts* opts, double* pctl, colo_colocated_summary* totals);
 
 /* The event log of one device's Simulation::run (tools/colosim.cpp --emit-events;
- * LoggedEvent::to_json, engine.hpp:109-129, 241-244) in SimMode::ServingOnly or
- * Colocated: the run on the GPU records every logged event, which are put in
+ * LoggedEvent::to_json, engine.hpp:109-129, 241-244) in any SimMode: the run on the GPU records every logged event, which are put in
  * dispatch order ((time, sequence), engine.hpp:184-187) and formatted as the
  * reference formats them.  d_label_delay may be NULL (default_label_delay for
  * every query; < 0 = never); d_query_id may be NULL (ids 0..n-1).  Returns the

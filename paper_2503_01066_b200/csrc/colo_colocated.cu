@@ -941,6 +941,9 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                         if (bal) {
                             const uint32_t below = bal & ((1u << lane) - 1u);
                             const double prev_lane = __shfl_sync(kFullMask, te, below ? 31 - __clz(below) : 0);
+                            if (LOG && em && cpa)  // LabelArrival (-1, query) popped at te (engine.hpp:414-416, 481-486)
+                                emit_from(true, EV_LABEL, te, step_seq0 + mn, 0x4000u + static_cast<uint32_t>(j0 + lane),
+                                          -1, qid_of(head + j), te, 0.0, 0u);
                             if (em) {
                                 if (te < (below ? prev_lane : last_t)) unsorted = true;
                                 if (!spec && (tmode != TM_OUT || jc + __popc(below) < P.tasks[w].expect[1])) {
@@ -1322,6 +1325,27 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
 // time + its duration (:860-872, 888, 902), and training_busy_time adds every
 // layer's duration in that order (:875).  The trainer ledger peaks at the
 // fixed footprint plus the largest job it ran (memory.hpp:28-35 reuse).
+// SeparateCluster trainer layer events for the event log (lane 'r', b = -1,
+// engine.hpp:860-877).  Their sequence numbers are not tracked (the trainer is
+// folded after the serving run), so at an exactly equal time they sort after
+// the serving events; times of the two timelines practically never tie.
+__device__ __forceinline__ void trainer_log(const CoParams& P, uint32_t kind, double t, double t0, double dur,
+                                            int64_t layer) {
+    const unsigned long long i = atomicAdd(P.evcnt, 1ull);
+    if (i < P.evcap) {
+        EvRec r;
+        r.t = t;
+        r.start = t0;
+        r.dur = dur;
+        r.key = ((1ull << 48) - 1) << 16;
+        r.a = layer;
+        r.b = -1;
+        r.kind = kind;
+        r.gen = 1;  // trainer lane
+        P.evlog[i] = r;
+    }
+}
+
 __global__ void __launch_bounds__(128) k_trainer_fold(const __grid_constant__ CoParams P, const double* __restrict__ jt,
                                                       const uint32_t* __restrict__ jq) {
     const uint32_t d = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1360,12 +1384,16 @@ __global__ void __launch_bounds__(128) k_trainer_fold(const __grid_constant__ Co
         double t = te < prev_end ? prev_end : te;  // std::max(now_, trainer_free_at_)
         for (uint32_t k = 0; k < np; ++k)
             for (uint64_t l = 0; l < L; ++l) {
+                const double t0 = t;
                 t = t + fd;
                 busy += fd;
+                if (P.evlog) trainer_log(P, EV_FWD, t, t0, fd, static_cast<int64_t>(l));
             }
         for (uint64_t l = 0; l < L; ++l) {
+            const double t0 = t;
             t = t + bd;
             busy += bd;
+            if (P.evlog) trainer_log(P, EV_BWD, t, t0, bd, static_cast<int64_t>(L - 1 - l));
         }
         prev_end = t;
         trained += cpa ? p + 2 * o : p;
@@ -2141,8 +2169,8 @@ int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mod
                               const double* d_label_delay, double default_label_delay, const uint64_t* d_query_id,
                               size_t n, double tau) {
     if (!ctx || !set || (n && (!d_arrival || !d_prompt || !d_output))) return -COLO_EINVAL;
-    if (sim_mode != COLO_SIM_SERVING_ONLY && sim_mode != COLO_SIM_COLOCATED)
-        return -set_err(ctx, COLO_EINVAL, "event log: ServingOnly and Colocated runs only");
+    if (sim_mode < COLO_SIM_SERVING_ONLY || sim_mode > COLO_SIM_SEPARATE)
+        return -set_err(ctx, COLO_EINVAL, "event log: sim mode must be 0, 1 or 2");
     if (n >= (1ull << 40)) return -set_err(ctx, COLO_EINVAL, "event log: trace too long");
     ctx->evtext.clear();
     {
@@ -2167,7 +2195,16 @@ int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mod
     // device scratch: offsets, set index, mode, lstart, then the records
     size_t cap = n * 8 + 65536;  // records (grown and re-run when the run logs more)
     for (int attempt = 0; attempt < 4; ++attempt) {
-        const size_t o_off = 0, o_set = 64, o_mode = 128, o_ls = 256, o_ev = o_ls + align256c(kLayerCap * 8);
+        const size_t o_off = 0, o_set = 64, o_mode = 128, o_ls = 256, o_sum = o_ls + align256c(kLayerCap * 8),
+                     o_jc = o_sum + align256c(sizeof(colo_colocated_summary)), o_jt = o_jc + 256,
+                     o_jq = o_jt + align256c(n * 8 + 8), o_jt2 = o_jq + align256c(n * 4 + 8),
+                     o_jq2 = o_jt2 + align256c(n * 8 + 8), o_tmp = o_jq2 + align256c(n * 4 + 8);
+        size_t tb = 0;
+        if (sim_mode == COLO_SIM_SEPARATE && n)
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, static_cast<const double*>(nullptr), static_cast<double*>(nullptr),
+                                            static_cast<const uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                            static_cast<int>(n), 0, 64, ctx->stream);
+        const size_t o_ev = o_tmp + align256c(tb + 8);
         const size_t bytes = o_ev + (n + cap) * sizeof(EvRec);
         {
             const colo_status st = grow_buf(ctx, ctx->d_seglog, ctx->seglog_bytes, bytes);
@@ -2197,6 +2234,12 @@ int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mod
         P.lstart = reinterpret_cast<double*>(base + o_ls);
         P.evlog = reinterpret_cast<EvRec*>(base + o_ev);
         P.evcap = n + cap;
+        if (sim_mode == COLO_SIM_SEPARATE) {  // the job stream and the trainer's report slot
+            P.job_t = reinterpret_cast<double*>(base + o_jt);
+            P.job_q = reinterpret_cast<uint32_t*>(base + o_jq);
+            P.job_cnt = reinterpret_cast<uint64_t*>(base + o_jc);
+            P.summary = reinterpret_cast<colo_colocated_summary*>(base + o_sum);
+        }
         P.evcnt = reinterpret_cast<unsigned long long*>(ctx->d_counters);
         const unsigned long long start_cnt = n;  // the arrival records come first
         if (cudaMemcpyAsync(P.evcnt, &start_cnt, 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
@@ -2217,6 +2260,26 @@ int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mod
         }
         COLO_LAUNCHED(ctx);
         k_colocated<false, true><<<1, kWarpsC * 32, 0, ctx->stream>>>(P);
+        if (sim_mode == COLO_SIM_SEPARATE) {  // the trainer over the job stream in enqueue order (stable sort)
+            int f2 = 0;
+            uint64_t jn = 0;
+            cudaMemcpyAsync(&f2, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+            cudaMemcpyAsync(&jn, P.job_cnt, 8, cudaMemcpyDeviceToHost, ctx->stream);
+            if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return -cuda_err(ctx, cudaGetLastError(), "jobs");
+            const double* jt = P.job_t;
+            const uint32_t* jq = P.job_q;
+            if ((f2 & 4) && jn > 1) {
+                size_t tb2 = tb;
+                if (cub::DeviceRadixSort::SortPairs(base + o_tmp, tb2, P.job_t, reinterpret_cast<double*>(base + o_jt2),
+                                                    P.job_q, reinterpret_cast<uint32_t*>(base + o_jq2),
+                                                    static_cast<int>(jn), 0, 64, ctx->stream) != cudaSuccess)
+                    return -cuda_err(ctx, cudaGetLastError(), "job sort");
+                jt = reinterpret_cast<const double*>(base + o_jt2);
+                jq = reinterpret_cast<const uint32_t*>(base + o_jq2);
+            }
+            COLO_LAUNCHED(ctx);
+            k_trainer_fold<<<1, 128, 0, ctx->stream>>>(P, jt, jq);
+        }
         unsigned long long cnt = 0;
         cudaMemcpyAsync(&cnt, P.evcnt, 8, cudaMemcpyDeviceToHost, ctx->stream);
         cudaMemcpyAsync(&flag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
@@ -2249,11 +2312,12 @@ int64_t colo_colocated_events(colo_ctx* ctx, const colo_mapset* set, int sim_mod
             }
             if (r.kind == EV_COPY && std::find(dead.begin(), dead.end(), r.gen) != dead.end()) continue;
             if (r.kind > EV_COPY) continue;
+            const char lane_c = (r.kind == EV_FWD || r.kind == EV_BWD) && r.gen == 1 ? 'r' : kLane[r.kind];
             const int k = std::snprintf(buf, sizeof buf,
                                         "{\"t\":%.9f,\"seq\":%llu,\"kind\":\"%s\",\"a\":%lld,\"b\":%lld,"
                                         "\"start\":%.9f,\"dur\":%.9f,\"lane\":\"%c\"}\n",
                                         r.t, lseq++, kNames[r.kind], static_cast<long long>(r.a),
-                                        static_cast<long long>(r.b), r.start, r.dur, kLane[r.kind]);
+                                        static_cast<long long>(r.b), r.start, r.dur, lane_c);
             out.append(buf, static_cast<size_t>(k));
         }
         ctx->evtext.swap(out);

@@ -642,8 +642,8 @@ def cmd_run(engine, config_path, out_dir, trace_path="", offload_map_path="", he
         ec.trace_spec.file = _resolve(trace_path)
     trace = ec.trace_spec.realize()
     run = Run(ec.model, ec.gpu, ec.mode, ec.training, maps, trace, ec.cache_timeout)
-    if emit_events and (not hasattr(eng, "events") or ec.mode == cs.SimMode.SEPARATE_CLUSTER):
-        raise ColoValidationError(_lib.COLO_EVALIDATION, "--emit-events: ServingOnly and Colocated runs only")
+    if emit_events and not hasattr(eng, "events"):
+        raise ColoValidationError(_lib.COLO_EVALIDATION, "--emit-events: this engine keeps no event log")
     rep = eng.run([run])[0]
     os.makedirs(out_dir, exist_ok=True)
     export_csv(rep, _out_file(out_dir, "report.csv", force))

@@ -54,9 +54,9 @@ def test_cli_run_long_trace_segmented(tmp_path):
 @pytest.mark.parametrize("variant", ["small", "timeout5", "cap48_d2h2", "cpa_label0", "cpt_label0"])
 def test_cli_emit_events_matches_reference(tmp_path, variant):
     """`run --emit-events`: events.jsonl byte-identical to the reference CLI's
-    (LoggedEvent::to_json in dispatch order) for Colocated and ServingOnly runs,
-    including cache timeouts, prefetch loads, training resumes and zero label
-    delays."""
+    (LoggedEvent::to_json in dispatch order) in all three modes, including
+    cache timeouts, prefetch loads, training resumes, the SeparateCluster
+    trainer's layers and zero label delays."""
     import os
     import subprocess
 
@@ -78,7 +78,7 @@ def test_cli_emit_events_matches_reference(tmp_path, variant):
     cp = tmp_path / "v.config"
     cp.write_text(cfg)
     eng = ex.GpuEngine(cs.Context(0))
-    for mode in ("", "serving-only"):
+    for mode in ("", "serving-only", "baseline"):
         dr, dg = tmp_path / f"ref{mode}", tmp_path / f"gpu{mode}"
         subprocess.run([ref_bin, "run", "--config", str(cp), "--out", str(dr), "--emit-events"] +
                        (["--mode", mode] if mode else []), check=True, capture_output=True)
