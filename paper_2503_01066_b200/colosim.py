@@ -924,8 +924,8 @@ def colocated_events(ctx: Context, mapset: MapSet, arrival, prompt, output, labe
                      default_label_delay: float = 0.01, query_id=None, cache_timeout: float = 60.0,
                      sim_mode=None, tau: float = math.inf) -> str:
     """colo_colocated_events: the event log of one device's Simulation::run
-    (tools/colosim.cpp --emit-events) in ServingOnly or Colocated mode, as the
-    reference's JSON lines (LoggedEvent::to_json, engine.hpp:109-129).
+    (tools/colosim.cpp --emit-events) in any SimMode, as the reference's JSON
+    lines (LoggedEvent::to_json, engine.hpp:109-129).
     Device tensors: arrival f64, prompt/output int32, label_delay f64
     (optional), query_id int64 (optional)."""
     _need_cuda(arrival, "arrival", 8)
