@@ -423,4 +423,61 @@ Report run_simulation(Context& ctx, const SimConfig& cfg) {
     return run_simulations<Report>(ctx, std::vector<SimConfig>{cfg})[0];
 }
 
+/// Simulation::events_json() of the run (engine.hpp:166-175, with
+/// SimConfig::collect_events): every logged event in dispatch order as
+/// LoggedEvent::to_json lines, from the run on the GPU
+/// (colo_colocated_events).  Throws invariant_breach where run() does.
+template <class SimConfig>
+std::string events_json(Context& ctx, const SimConfig& cfg) {
+    colo_ctx* c = ctx.get();
+    const colo_model m = to_c_model(cfg.model);
+    const colo_gpu g = to_c_gpu(cfg.gpu);
+    check(colo_validate_profile_pair(&m, &g), c, "sim config");
+    colo_mapset* ms = detail::mapset_of(ctx, cfg);
+    std::vector<double> a, ld;
+    std::vector<std::uint32_t> p, o;
+    std::vector<std::uint64_t> q;
+    for (const auto& r : cfg.trace.records) {
+        a.push_back(r.arrival_time);
+        p.push_back(static_cast<std::uint32_t>(r.prompt_tokens));
+        o.push_back(static_cast<std::uint32_t>(r.output_tokens));
+        ld.push_back(r.label_delay ? *r.label_delay : -1.0);
+        q.push_back(static_cast<std::uint64_t>(r.query_id));
+    }
+    const std::size_t n = a.size();
+    void *d_a = nullptr, *d_p = nullptr, *d_o = nullptr, *d_ld = nullptr, *d_q = nullptr;
+    std::string text;
+    try {
+        check(colo_dev_alloc(c, n * 8 + 8, &d_a), c, "alloc");
+        check(colo_dev_alloc(c, n * 4 + 4, &d_p), c, "alloc");
+        check(colo_dev_alloc(c, n * 4 + 4, &d_o), c, "alloc");
+        check(colo_dev_alloc(c, n * 8 + 8, &d_ld), c, "alloc");
+        check(colo_dev_alloc(c, n * 8 + 8, &d_q), c, "alloc");
+        check(colo_memcpy_h2d(c, d_a, a.data(), n * 8), c, "h2d");
+        check(colo_memcpy_h2d(c, d_p, p.data(), n * 4), c, "h2d");
+        check(colo_memcpy_h2d(c, d_o, o.data(), n * 4), c, "h2d");
+        check(colo_memcpy_h2d(c, d_ld, ld.data(), n * 8), c, "h2d");
+        check(colo_memcpy_h2d(c, d_q, q.data(), n * 8), c, "h2d");
+        const std::int64_t len = colo_colocated_events(
+            c, ms, detail::sim_mode_of(cfg), cfg.cache_timeout, static_cast<const double*>(d_a),
+            static_cast<const std::uint32_t*>(d_p), static_cast<const std::uint32_t*>(d_o),
+            static_cast<const double*>(d_ld), -1.0, static_cast<const std::uint64_t*>(d_q), n,
+            std::numeric_limits<double>::infinity());
+        if (len < 0) {
+            if (-len == COLO_EBREACH) throw invariant_breach("colo-b200: invariant breach in run_simulation");
+            check(static_cast<colo_status>(-len), c, "events_json");
+        }
+        text.resize(static_cast<std::size_t>(len) + 1);
+        colo_events_text(c, text.data(), text.size());
+        text.resize(static_cast<std::size_t>(len));
+    } catch (...) {
+        for (void* x : {d_a, d_p, d_o, d_ld, d_q}) colo_dev_free(c, x);
+        colo_mapset_destroy(ms);
+        throw;
+    }
+    for (void* x : {d_a, d_p, d_o, d_ld, d_q}) colo_dev_free(c, x);
+    colo_mapset_destroy(ms);
+    return text;
+}
+
 }  // namespace colosim_gpu

@@ -167,6 +167,24 @@ int main() {
         }
         EXPECT(bad == 0, "%zu of %zu MetricsReports differ from Simulation::run", bad, cfgs.size());
         EXPECT(got.back().oom_flag && got.back().oom_jobs == 2, "trainer OOM datapoint");
+        // the event log (SimConfig::collect_events, Simulation::events_json, engine.hpp:166-175)
+        size_t ev_bad = 0, ev_done = 0;
+        for (size_t i = 0; i < cfgs.size() && ev_done < 8; i += 3) {
+            SimConfig ec = cfgs[i];
+            ec.collect_events = true;
+            Simulation sim(ec);
+            try {
+                sim.run();
+            } catch (const std::exception&) {
+                continue;  // a breaching run has no log
+            }
+            ++ev_done;
+            if (colosim_gpu::events_json(ctx, cfgs[i]) != sim.events_json()) {
+                ++ev_bad;
+                std::printf("  events of run %zu differ\n", i);
+            }
+        }
+        EXPECT(ev_done >= 4 && ev_bad == 0, "%zu of %zu event logs differ from Simulation::events_json", ev_bad, ev_done);
         // the constructor's refusals (engine.hpp:60-75)
         SimConfig badhash = cfgs[0];
         badhash.offload_map.profile_hash_value ^= 1;
