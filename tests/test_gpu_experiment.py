@@ -85,3 +85,48 @@ def test_cli_emit_events_matches_reference(tmp_path, variant):
         ex.cmd_run(eng, str(cp), str(dg), mode_override=mode, emit_events=True)
         for nm in ("events.jsonl", "report.csv", "report.jsonl", "tpt_cdf.csv"):
             assert (dr / nm).read_bytes() == (dg / nm).read_bytes(), (variant, mode, nm)
+
+
+def test_cli_emit_events_random_configs(tmp_path):
+    """Random configs (load, horizon, cache timeout, CPA/CPT, label delays,
+    capacity and copy bandwidths) x the three modes: the run succeeds or
+    breaches exactly when the reference's does, and events.jsonl is
+    byte-identical."""
+    import os
+    import random
+    import subprocess
+
+    from experiment_check import CLI
+
+    ref_bin = os.path.join(os.path.dirname(CLI), "..", "..", "oracle", "_ref", "colosim")
+    if not os.path.exists(ref_bin):
+        pytest.skip("oracle/_ref/colosim not built")
+    base = open(os.path.join(CLI, "small.config")).read()
+    base = base.replace("histogram:lengths.jsonl", "histogram:" + os.path.join(CLI, "lengths.jsonl"))
+    rng = random.Random(31)
+    eng = ex.GpuEngine(cs.Context(0))
+    for it in range(8):
+        cfg = (base.replace("trace.qps = 0.12", f"trace.qps = {rng.choice([0.03, 0.12, 0.3, 0.8])}")
+               .replace("trace.duration = 900", f"trace.duration = {rng.choice([300, 900, 2000])}")
+               .replace("sim.cache_timeout = 60", f"sim.cache_timeout = {rng.choice([2, 10, 60, 600])}")
+               .replace("sim.training = cpa", f"sim.training = {rng.choice(['cpa', 'cpt'])}")
+               .replace("sim.seed = 11", f"sim.seed = {rng.randint(1, 10**6)}")
+               .replace("trace.label_delay = uniform:0,30",
+                        "trace.label_delay = " + rng.choice(["uniform:0,30", "fixed:0", "fixed:0.5", "uniform:0,200"]))
+               .replace("gpu.capacity_bytes = 85899345920", f"gpu.capacity_bytes = {rng.choice([48, 64, 80]) * 1024**3}")
+               .replace("gpu.d2h_bandwidth = 24000000000", f"gpu.d2h_bandwidth = {rng.choice([2, 8, 24]) * 10**9}")
+               .replace("gpu.h2d_bandwidth = 24000000000", f"gpu.h2d_bandwidth = {rng.choice([4, 24]) * 10**9}"))
+        cp = tmp_path / f"c{it}.config"
+        cp.write_text(cfg)
+        for mode in ("", "serving-only", "baseline"):
+            dr, dg = tmp_path / f"r{it}{mode}", tmp_path / f"g{it}{mode}"
+            pr = subprocess.run([ref_bin, "run", "--config", str(cp), "--out", str(dr), "--emit-events"] +
+                                (["--mode", mode] if mode else []), capture_output=True)
+            try:
+                ex.cmd_run(eng, str(cp), str(dg), mode_override=mode, emit_events=True)
+                ok = True
+            except cs.ColoBreachError:
+                ok = False
+            assert ok == (pr.returncode == 0), (it, mode, pr.returncode)
+            if ok:
+                assert (dr / "events.jsonl").read_bytes() == (dg / "events.jsonl").read_bytes(), (it, mode)
