@@ -542,6 +542,18 @@ def _jdump(d: dict) -> str:
     return "{" + ",".join(f"{json.dumps(k)}:{_jval(d[k])}" for k in sorted(d)) + "}"
 
 
+def save_trace(t: "Trace", path: str) -> None:
+    """save_trace (workload.hpp:256-270): one nlohmann::json object per record,
+    keys sorted, label_delay null when absent."""
+    lines = []
+    for q, a, p, o, ld in zip(t.query_id, t.arrival, t.prompt, t.output, t.label_delay):
+        ldv = None if (ld != ld or ld < 0) else float(ld)
+        lines.append(_jdump({"query_id": int(q), "arrival_time": float(a), "prompt_tokens": int(p),
+                             "output_tokens": int(o), "label_delay": ldv}))
+    with open(path, "w", newline="") as f:
+        f.write("".join(ln + "\n" for ln in lines))
+
+
 def export_jsonl(r: dict, path: str) -> None:
     """metrics.hpp:191-226."""
     groups = [

@@ -143,3 +143,20 @@ def test_histogram_jsonl(tmp_path):  # proj/profiles/sharegpt_like_lengths.jsonl
     path.write_text('{"tokens": 64, "probability": 0.5}\n{"tokens": 128, "probability": 0.6}\n')
     with pytest.raises(cs.ColoValidationError, match="sum"):
         cs.load_histogram(str(path))
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built")
+def test_save_trace_matches_reference(orc, tmp_path):
+    """save_trace (workload.hpp:256-270): byte-identical file, label_delay null when absent."""
+    from paper_2503_01066_b200 import experiment as ex
+
+    ref = OracleLib("ref").lib
+    hv, hp = cs.sharegpt_histogram()
+    a, p, o = orc.generate_trace(0.7, 800.0, ("histogram", hv, hp), 5)
+    ld = np.where(np.arange(len(a)) % 3 == 0, np.nan, np.arange(len(a)) * 0.001)
+    rpath, gpath = str(tmp_path / "r.jsonl"), str(tmp_path / "g.jsonl")
+    assert ref.ref_save_trace(a.ctypes.data_as(C.c_void_p), p.ctypes.data_as(C.c_void_p),
+                              o.ctypes.data_as(C.c_void_p), ld.ctypes.data_as(C.c_void_p), C.c_size_t(len(a)),
+                              rpath.encode()) == 0
+    ex.save_trace(ex.Trace(a, p, o, ld, np.arange(len(a), dtype=np.uint64)), gpath)
+    assert open(gpath, "rb").read() == open(rpath, "rb").read()
