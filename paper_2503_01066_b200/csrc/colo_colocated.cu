@@ -35,7 +35,15 @@
 //   loads     the current prefetch plan (shared memory), a sorted stream;
 //             a bumped plan_generation_ makes all of it no-ops.
 // CopyDone events only update host_bytes, which no report field reads; they
-// consume their sequence numbers and are not materialised.
+// consume their sequence numbers and are not materialised (the event log
+// records them with their time and sequence number instead).
+//
+// Instantiations: k_colocated<false> runs device w on warp w over its whole
+// trace; k_colocated<true> runs P.tasks[w] -- a whole trace, a speculative
+// segment or an output segment of one long device (see SegTask); and
+// k_colocated<false, true> additionally appends every event the reference
+// logs (see EvRec; colo_colocated_events).  SeparateCluster devices serve as
+// ServingOnly and emit their trainer jobs (k_trainer_fold folds them).
 //
 // Every f64 operation is the reference's, in the reference's order
 // (-fmad=false), so each device's MetricsReport fields and TPT samples equal
