@@ -46,7 +46,7 @@ constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
 #ifndef COLO_REPLAY_BLOCKS
-#define COLO_REPLAY_BLOCKS 4
+#define COLO_REPLAY_BLOCKS 6
 #endif
 constexpr int kReplayBlocks = COLO_REPLAY_BLOCKS;  // resident CTAs per SM the replay pass is compiled for
 constexpr int kTileBytes = kWarps * 32 * 33 * 8;   // k_replay_full's dynamic shared memory
@@ -1029,11 +1029,15 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
 }
 
 __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(const __grid_constant__ ReplayParams P) {
-    __shared__ uint2 spo[kWarps][kStage];
-    __shared__ double spd[kWarps][kStage];
-    __shared__ __align__(16) double sdk[kWarps][128];
-    extern __shared__ double stile[];  // idle-start blocks: one row of 33 step times per batch, per warp
+    // one region per warp: the idle-start tile (32 rows of 33 step times), which
+    // the per-batch path's member stage and step durations alias (never live
+    // at the same time)
+    extern __shared__ double stile[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* const wreg = stile + warp * (32 * 33);
+    uint2* const spo_w = reinterpret_cast<uint2*>(wreg);
+    double* const spd_w = wreg + kStage;
+    double* const sdk_w = wreg + 2 * kStage;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
     const Seg sg = P.segs[w];
@@ -1049,8 +1053,7 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
     }
     bool synced;
     if (head < sg.end)
-        run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo[warp], spd[warp], sdk[warp],
-                              stile + warp * (32 * 33));
+        run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo_w, spd_w, sdk_w, wreg);
     const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
     const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
 #pragma unroll
@@ -1081,11 +1084,12 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
 // (an idle start forms the same one-query batch from T = -inf; a queued batch
 // starts at the previous end, T = start).  One warp per replay segment.
 __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_sparse_hist(const __grid_constant__ ReplayParams P) {
-    __shared__ uint2 spo[kWarps][kStage];
-    __shared__ double spd[kWarps][kStage];
-    __shared__ __align__(16) double sdk[kWarps][128];
-    extern __shared__ double stile[];
+    extern __shared__ double stile[];  // as k_replay_full: the tile with the member stage aliased
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* const wreg = stile + warp * (32 * 33);
+    uint2* const spo_w = reinterpret_cast<uint2*>(wreg);
+    double* const spd_w = wreg + kStage;
+    double* const sdk_w = wreg + 2 * kStage;
     const uint32_t w = blockIdx.x * kWarps + warp;
     if (w >= P.nsegs) return;
     const Seg sg = P.segs[w];
@@ -1110,8 +1114,8 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_sparse_hist(cons
             uint64_t head = j0 + l;
             double T = (b2 >> 62) & 1ull ? -INFINITY : P.sparse_start[lo + head];
             bool synced;
-            run_batches<RUN_FULL>(P, sg.dev, head, T, j0 + l + 1, sg.start, nullptr, synced, A, spo[warp], spd[warp],
-                                  sdk[warp], stile + warp * (32 * 33));
+            run_batches<RUN_FULL>(P, sg.dev, head, T, j0 + l + 1, sg.start, nullptr, synced, A, spo_w, spd_w, sdk_w,
+                                  wreg);
         }
     }
 }
