@@ -317,6 +317,41 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * n * e2e_steps / float(te.item())
     assert torch.equal(hv.cuda(), out), "host-buffer path disagrees with the device path"
+    # the PCIe bound of that call: pinned copies of the same bytes, each direction alone
+    cs_ = torch.cuda.Stream()
+    dbuf = torch.empty(2 * n, dtype=torch.int32, device="cuda")
+    hin = torch.empty(2 * n, dtype=torch.int32, pin_memory=True)
+    pcie = {}
+    for name, dst, src in (("h2d", dbuf, hin), ("d2h", hv, dbuf[:n])):
+        best = float("inf")
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(cs_):
+                e0.record(cs_)
+                dst.copy_(src, non_blocking=True)
+                e1.record(cs_)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 1e3)
+        pcie[name + "_gbs"] = src.numel() * 4 / best / 1e9
+    # both directions at once, as the call moves them: the step's transfer floor
+    cs2 = torch.cuda.Stream()
+    best = float("inf")
+    for _ in range(3):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(cs_)
+        cs2.wait_event(e0)
+        with torch.cuda.stream(cs_):
+            dbuf.copy_(hin, non_blocking=True)
+            e1.record(cs_)
+        with torch.cuda.stream(cs2):
+            hv.copy_(out, non_blocking=True)
+            e2.record(cs2)
+        e1.synchronize()
+        e2.synchronize()
+        best = min(best, max(e0.elapsed_time(e1), e0.elapsed_time(e2)) / 1e3)
+    pcie["duplex_s"] = best
+    del dbuf, hin
+    pcie_bound = n / best
 
     line = None
     if rank == 0:
@@ -330,7 +365,9 @@ def run_ours(args, world, rank, local):
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback"},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n * world,
                         "d2h_bytes_per_step": 4 * n * world, "steps": e2e_steps,
-                        "api": "colo_features_decide_host (pinned host buffers, wall clock)"},
+                        "api": "colo_features_decide_host (pinned host buffers, wall clock)",
+                        "pcie": dict(pcie, bound=pcie_bound * world, frac=e2e_value / (pcie_bound * world),
+                                     how="bound = queries / duplex_s, the pinned 8 B/q h2d and 4 B/q d2h copies run concurrently; h2d_gbs/d2h_gbs each alone")},
                 "gpu_launches": launches, "clocks": clk.report(), "counters": cnt}
         if world == 1 and not args.no_cpu_baseline:
             try:
