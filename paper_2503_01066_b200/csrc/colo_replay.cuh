@@ -206,22 +206,32 @@ __device__ __forceinline__ uint64_t find_tail(const double* __restrict__ arr, ui
     return lo < N ? lo : N;
 }
 
-// hist[key] += cnt for every lane with act; lanes of the warp that share a key
-// add once, so consecutive decode steps of a batch, whose TPT samples fall in
-// one or a few bins, cost one atomic per distinct bin: the warp takes the
-// distinct keys one at a time (the lowest active lane's key, a ballot of its
-// peers, one warp-wide REDUX of their counts).  Call from all lanes.
+// hist[key] += cnt for every lane with act.  The lanes are consecutive decode
+// steps of a batch, whose TPT samples rise slowly with the context, so equal
+// keys come in runs of neighbouring lanes: the lane that starts a run adds the
+// run's total (an inclusive scan of the counts, differenced at the run's ends),
+// and every run head issues its atomic in the same instruction.  Keys that
+// repeat in separate runs just add separately, so the histogram is the same
+// integer sum whatever the order.  Call from all lanes.
 __device__ __forceinline__ void hist_add(uint64_t* hist, uint32_t key, uint32_t cnt, bool act) {
-    unsigned rem = __ballot_sync(kFullMask, act);
-    while (rem) {
-        const int ld = __ffs(rem) - 1;
-        const uint32_t k0 = __shfl_sync(kFullMask, key, ld);
-        const bool mine = act && key == k0;
-        const unsigned total = __reduce_add_sync(kFullMask, mine ? cnt : 0u);
-        if ((threadIdx.x & 31) == static_cast<unsigned>(ld))
-            atomicAdd(reinterpret_cast<unsigned long long*>(&hist[k0]), static_cast<unsigned long long>(total));
-        rem &= ~__ballot_sync(kFullMask, mine);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t c = act ? cnt : 0u;
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFullMask, incl, o);
+        if (lane >= static_cast<uint32_t>(o)) incl += y;
     }
+    const uint32_t pkey = __shfl_up_sync(kFullMask, key, 1);
+    const unsigned am = __ballot_sync(kFullMask, act);
+    const bool pact = lane > 0 && ((am >> (lane - 1)) & 1u);
+    const bool head = act && !(pact && pkey == key);
+    // a run ends just before the next head or inactive lane
+    const unsigned brk = __ballot_sync(kFullMask, head || !act);
+    const unsigned above = lane == 31 ? 0u : brk & (~0u << (lane + 1));
+    const uint32_t last = above ? static_cast<uint32_t>(__ffs(above) - 2) : 31u;
+    const uint32_t iend = __shfl_sync(kFullMask, incl, last);
+    if (head) atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(iend - incl + c));
 }
 
 // Sequential f64 fold t = (((t + d0) + d1) + ...) over K durations staged in
