@@ -234,6 +234,19 @@ __device__ __forceinline__ void hist_add(uint64_t* hist, uint32_t key, uint32_t 
     if (head) atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(iend - incl + c));
 }
 
+// hist_add with cnt == 1 on every active lane: a run's total is its length.
+__device__ __forceinline__ void hist_add1(uint64_t* hist, uint32_t key, bool act) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pkey = __shfl_up_sync(kFullMask, key, 1);
+    const unsigned am = __ballot_sync(kFullMask, act);
+    const bool pact = lane > 0 && ((am >> (lane - 1)) & 1u);
+    const bool head = act && !(pact && pkey == key);
+    const unsigned brk = __ballot_sync(kFullMask, head || !act);
+    const unsigned above = lane == 31 ? 0u : brk & (~0u << (lane + 1));
+    const uint32_t end = above ? static_cast<uint32_t>(__ffs(above) - 1) : 32u;
+    if (head) atomicAdd(reinterpret_cast<unsigned long long*>(&hist[key]), static_cast<unsigned long long>(end - lane));
+}
+
 // Sequential f64 fold t = (((t + d0) + d1) + ...) over K durations staged in
 // 16-B aligned shared memory, on one lane.  Pairs come in with one LDS.128 and
 // the K == 128 case (the default output length) is fully unrolled, so the

@@ -277,10 +277,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                                       (nf > 2 && hb == P.prefix[2]));
                             if (__any_sync(FULL, any))
                                 for (uint32_t f = 0; f < nf; ++f)
-                                    hist_add(P.hist,
-                                             f * COLO_HIST_BINS +
-                                                 static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
-                                             1u, live && hb == P.prefix[f]);
+                                    hist_add1(P.hist,
+                                              f * COLO_HIST_BINS +
+                                                  static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1)),
+                                              live && hb == P.prefix[f]);
                         }
                         if (live && !((tlm >> b) & 1u)) acc_fixed(A.acc, A.flags, s, 1u);
                         const uint64_t sb = __shfl_sync(FULL, spos, b);
