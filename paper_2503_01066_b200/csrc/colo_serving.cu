@@ -229,7 +229,29 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             const uint32_t ov = v ? oq : 0u;
             double now = t_pre, kd = 0.0;
             if (MODE != RUN_FULL) {
-                for (uint32_t k = 0; k < ov; ++k, kd += 1.0) now = now + (0.0 + (gam + del * (tq + kd)));
+                // only the block's last batch's end is used here (T for the next
+                // query), so its chain alone runs, 128 steps at a time across the
+                // warp: a scan while it stays in one binade, else sequentially
+                const uint32_t L = nv - 1;
+                double t = __shfl_sync(FULL, t_pre, L);
+                const double tqL = __shfl_sync(FULL, tq, L);
+                const uint32_t oL = __shfl_sync(FULL, ov, L);
+                for (uint32_t k0 = 0; k0 < oL; k0 += 128) {
+                    const uint32_t K = min(128u, oL - k0);
+                    double dk[4];
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const uint32_t i = 32 * r + lane;
+                        dk[r] = i < K ? 0.0 + (gam + del * (tqL + static_cast<double>(k0 + i))) : 0.0;
+                    }
+                    double te;
+                    if (chain_fast_end(t, dk, K, te)) {
+                        t = te;
+                    } else {
+                        for (uint32_t i = 0; i < K; ++i) t = t + (0.0 + (gam + del * (tqL + static_cast<double>(k0 + i))));
+                    }
+                }
+                now = t;
             } else {
                 uint32_t kmax = ov;
 #pragma unroll
@@ -290,7 +312,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 }
                 if (tl) acc_fixed(A.acc, A.flags, now, 1u);
                 const uint64_t need = v ? serving_memory(m, static_cast<uint64_t>(pq) + oq, 1) : 0ull;
-                if (v && P.bmeta_bins) {
+                if (MODE == RUN_FULL && v && P.bmeta_bins) {
                     // a conservative bin range without looking at the samples: d_k grows with k
                     // (delta >= 0) and each sample is d_k within one rounding of the time (<= ulp(T_end))
                     const double d_first = 0.0 + (gam + del * tq);
@@ -302,7 +324,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                     P.bmeta_start[lo + q] = aq + 0.0;
                     P.bmeta_bins[lo + q] = (1ull << 63) | (1ull << 62) | (static_cast<uint64_t>(bhi) << 21) | blo;
                 }
-                if (v) {
+                if (MODE == RUN_FULL && v) {  // (the speculative passes write no outputs)
                     const bool slowq = (slowm >> lane) & 1u;  // a lone query's tokens are every step
                     A.gen += ov;
                     A.slow_q += slowq;
