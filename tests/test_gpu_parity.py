@@ -300,6 +300,7 @@ def test_replay_segmented_speculation(ctx, orc, segment_len, qps):
     S = cs.summaries_to_numpy(r["summary"])[0]
     nb = int(S["batches"])
     assert r["batches"].cpu().numpy()[:nb].tobytes() == ref["batches"].tobytes()
+    assert not r["batches"].cpu().numpy()[nb:].any()  # no records left by the speculative passes
     assert S["end_time"] == ref["summary"]["end_time"] and int(S["slow_tokens"]) == ref["summary"]["slow_tokens"]
     exact = sum(int(x) for x in (ref["samples"] * 2.0**96))  # every sample is a multiple of 2^-96 here
     limbs = [int(v) for v in S["tpt_sum"]]
