@@ -46,7 +46,7 @@ constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
 #ifndef COLO_REPLAY_BLOCKS
-#define COLO_REPLAY_BLOCKS 6
+#define COLO_REPLAY_BLOCKS 5
 #endif
 constexpr int kReplayBlocks = COLO_REPLAY_BLOCKS;  // resident CTAs per SM the replay pass is compiled for
 constexpr int kTileBytes = kWarps * 32 * 33 * 8;   // k_replay_full's dynamic shared memory
