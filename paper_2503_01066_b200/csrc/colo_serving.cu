@@ -639,11 +639,14 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             const uint32_t cnt = min(128u, maxo - k0);
             if (!chain_fast_store(now, sDK, cnt) && lane == 0) chain_fold_store(now, sDK, cnt);
             __syncwarp();
-            double sv[4] = {0.0, 0.0, 0.0, 0.0};
+            // the four 32-step rows are post-processed by one (not unrolled)
+            // body, which reads its samples and alive counts back from shared
+            // memory: a smaller kernel for the instruction cache
+            const double now0 = now;
+            uint32_t* const sAL = reinterpret_cast<uint32_t*>(sDK + 128);  // FULL: inside the warp's tile region
+            if (MODE == RUN_FULL) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {  // sample = now - last_token_time
-                const uint32_t i = 32 * r + lane;
-                if (i < cnt) sv[r] = sDK[i] - (i ? sDK[i - 1] : now);
+                for (int r = 0; r < 4; ++r) sAL[32 * r + lane] = alive[r];
             }
             if (MODE == RUN_FULL && tele) {  // members whose last step is in this window: + T_{o_j - 1}
                 for (uint64_t j = lane; j < nb; j += 32) {
@@ -653,14 +656,15 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             }
             now = sDK[cnt - 1];
             __syncwarp();
-#pragma unroll
+#pragma unroll 1
             for (int r = 0; r < 4; ++r) {
             const uint32_t kr0 = k0 + 32 * r;
             if (kr0 >= maxo) break;
             const uint32_t k = kr0 + lane;
-            const double s = sv[r];
             if (MODE == RUN_FULL) {
-                const uint32_t alv = alive[r];
+                const uint32_t i = 32 * r + lane;  // sample = now - last_token_time
+                const double s = i < cnt ? sDK[i] - (i ? sDK[i - 1] : now0) : 0.0;
+                const uint32_t alv = sAL[i];
                 const bool live = k < maxo;
                 if (P.bmeta_bins && live && !(s < 0.0)) {  // (negative samples never match a filter)
                     const uint32_t bn = static_cast<uint32_t>(static_cast<uint64_t>(__double_as_longlong(s)) >> 42);
@@ -701,6 +705,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 }
             }
             }
+            __syncwarp();  // the rows' reads of sDK / sAL before the next window writes them
         }
         if (MODE == RUN_FULL) {
             // labels: a query is slow iff one of its tokens is (o_j > first slow step)
