@@ -890,12 +890,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
             const uint32_t cnt = min(128u, maxo - k0);
             if (lane == 0) chain_fold_store(tnow, S.dk, cnt);  // (a warp scan is slower here: other warps hide this)
             __syncwarp();
-            double sv[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {  // sample = now - last_token_time
-                const uint32_t i = 32 * r + lane;
-                if (i < cnt) sv[r] = S.dk[i] - (i ? S.dk[i - 1] : tnow);
-            }
+            const double tnow0 = tnow;  // the rows below read their samples back (one rolled body)
             if (LOG) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -968,13 +963,14 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                 }
             }
             __syncwarp();
-#pragma unroll
+#pragma unroll 1
             for (int r = 0; r < 4; ++r) {
                 const uint32_t kr0 = k0 + 32 * r;
                 if (kr0 >= maxo) break;
                 const uint32_t k = kr0 + lane;
-                const double s = sv[r];
-                const uint32_t alv = alive[r];
+                const uint32_t i = 32 * r + lane;  // sample = now - last_token_time
+                const double s = i < cnt ? S.dk[i] - (i ? S.dk[i - 1] : tnow0) : 0.0;
+                const uint32_t alv = r == 0 ? alive[0] : r == 1 ? alive[1] : r == 2 ? alive[2] : alive[3];
                 const bool lv = k < maxo;
                 const bool slow = lv && s > P.tau;
                 const uint32_t sb = __ballot_sync(kFullMask, slow);
@@ -1003,6 +999,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_colocated(const __grid_constan
                     sample_pos += tot;
                 }
             }
+            __syncwarp();  // the rows' reads of dk before the next window writes them
         }
         for (uint64_t j = lane; j < nb; j += 32) {  // a query is slow iff one of its tokens is
             const uint32_t oj = staged ? S.po[j].y : po[head + j];
