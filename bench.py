@@ -162,9 +162,10 @@ def host_trace(seed: int):
     return prompt, output, offs
 
 
-def reference_decide(prompt, output, offs, devices, threads):
+def reference_decide(prompt, output, offs, devices, threads, collect=None):
     """The reference's own composition over its own OffloadingMap/HedgingMap
-    (oracle/_ref, ref_features_decide), one device per task, all host threads."""
+    (oracle/_ref, ref_features_decide), one device per task, all host threads.
+    collect: optional u32 array of every query's verdict (filled per device)."""
     from oracle.oracle import OracleLib, default_gpu, default_grid, default_model, phi14b_model
 
     ref = OracleLib("ref")
@@ -175,8 +176,10 @@ def reference_decide(prompt, output, offs, devices, threads):
     def one(d):
         lo, hi = int(offs[d]), int(offs[d + 1])
         m, gg, cpa = sets[dev_set_of(d)]
-        ref.features_decide([(m, gg, cpa)], grid, prompt[lo:hi], output[lo:hi], np.array([0, hi - lo], np.uint64),
-                            np.zeros(1, np.uint16))
+        v = ref.features_decide([(m, gg, cpa)], grid, prompt[lo:hi], output[lo:hi], np.array([0, hi - lo], np.uint64),
+                                np.zeros(1, np.uint16))
+        if collect is not None:
+            collect[lo:hi] = v
         return hi - lo
 
     t0 = time.perf_counter()
@@ -222,13 +225,25 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline_leg(prompt_h, output_h, offs_h):
+def cpu_baseline_leg(prompt_h, output_h, offs_h, gpu_verdicts=None):
+    """The reference on the host cores over the same 100M queries; also holds
+    every GPU verdict to the reference's (an untimed second pass collects them)."""
     threads = os.cpu_count() or 1
     devices = list(range(DEVICES))
     reference_decide(prompt_h, output_h, offs_h, devices[:1], threads)  # warm
     n, t = reference_decide(prompt_h, output_h, offs_h, devices, threads)
     n1, t1 = reference_decide(prompt_h, output_h, offs_h, devices[:4], 1)  # the reference is single-threaded
-    return {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference", "cpu": cpu_model(),
+    parity = None
+    if gpu_verdicts is not None:
+        want = np.empty(len(prompt_h), np.uint32)
+        reference_decide(prompt_h, output_h, offs_h, devices, threads, collect=want)
+        diff = int(np.count_nonzero(want != gpu_verdicts))
+        parity = {"c2_verdicts_equal": diff == 0, "n": int(len(want)), "mismatches": diff,
+                  "how": "every GPU verdict of the step vs oracle/_ref (the reference's own map lookups composed as "
+                         "engine.hpp:434-448,513-557) on the same 100M queries"}
+        if diff:
+            print(f"bench: {diff} C2 verdicts differ from the reference", file=sys.stderr)
+    return parity, {"value": n / t, "unit": UNIT, "cores": threads, "kind": "reference", "cpu": cpu_model(),
             "single_thread": {"value": n1 / t1, "cores": 1, "sample": f"4 devices ({n1} queries), {t1:.2f} s"},
             "sample": f"the same GPU-generated C2 arrays, all 64 devices ({n} queries), {threads} host threads, "
                       f"oracle/_ref (reference headers compiled unchanged), {t:.2f} s"}
@@ -371,10 +386,21 @@ def run_ours(args, world, rank, local):
                 "gpu_launches": launches, "clocks": clk.report(), "counters": cnt}
         if world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_baseline_leg(hp.numpy().view(np.uint32), ho.numpy().view(np.uint32), offs_h)
+                line["parity"], line["cpu_baseline"] = cpu_baseline_leg(
+                    hp.numpy().view(np.uint32), ho.numpy().view(np.uint32), offs_h, hv.numpy().view(np.uint32))
             except Exception as e:  # oracle/_ref missing on this box
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": f"unavailable: {e}"}
+    del out, hp, ho, hv, prompt, output
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    if not args.no_sub:
+        # stage 3 beside the headline (SURVEY §8(d) C3 and C4's per-rank step), device-timed on this box
+        sub = {"c3": c3_measure(args, world, rank, local, dist, args.sub_steps, 3, cpu=True),
+               "c4": c4_measure(args, world, rank, local, dist, C4_CHUNK, args.sub_steps, 3, cpu=True)}
+        if rank == 0:
+            line.update(sub)
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -712,116 +738,151 @@ def run_colo(args, world, rank, local):
 
 
 C4_FLEET, C4_PER_DEVICE = 1024, 7_812_500
+C4_SEED = 4040
+C4_CHUNK = 128  # devices per chunk context (1B queries): one rank's 8-GPU share
 
 
-def run_c4(args, world, rank, local):
-    """C4 (BASELINE.json configs[3]): the 1024-device fleet of 8B queries,
-    device d on rank d % world (C2's profiles/modes/rates per device).  Each
-    rank runs, per step, the trace-fused decisions over all its queries, the
-    serving replay with slow labels, and the exact TPT statistics (three
-    radix-select replay passes); the counters, histograms and exact sums are
-    the only data that cross ranks (NCCL all-reduce).  --c4-devices caps the
-    devices a rank holds (one B200 holds the 8-GPU share, 128 devices = 1B
-    queries; the 1-2 GPU shares do not fit next to the replay's records)."""
+def issue_roofline(kind: str, step_s: float, clk: dict, queries: int) -> dict:
+    """Issue-rate roofline of a replay step: the warp instructions one step
+    executes (smsp__inst_executed.sum summed over the step's kernels, from the
+    committed ncu capture profiles/r*_ncu_<kind>_step.json -- the count is a
+    property of the workload, not of the clock) over the live step time,
+    against 148 SMs x 4 schedulers x 1 warp-instruction/clk at the live SM
+    clock."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{kind}_step.json")))
+    mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    peak = 148 * 4 * mhz * 1e6
+    out = {"bound": "issue", "unit": "warp-inst/s", "peak": peak,
+           "peak_how": f"148 SMs x 4 schedulers x {mhz:.0f} MHz (live median SM clock)"}
+    if not files:
+        return dict(out, achieved=None, frac=None, inst_per_step=None, source="no ncu capture committed")
+    with open(files[-1]) as f:
+        d = json.load(f)
+    # instructions scale with the rank's queries (the capture's workload per query, the same traces' shape)
+    inst = float(d["inst_per_query"]) * queries if d.get("inst_per_query") else float(d["inst_per_step"])
+    ach = inst / step_s
+    return dict(out, achieved=ach, frac=ach / peak, inst_per_step=inst, inst_per_query=d.get("inst_per_query"),
+                kernels=d.get("kernels"), source=os.path.relpath(files[-1], ROOT))
+
+
+def c4_measure(args, world, rank, local, dist, devices_cap, steps, warmup, cpu=False):
+    """C4 (BASELINE.json configs[3]): the 1024-device fleet, fleet device g on
+    rank g % world.  Device g's trace is keyed on g (synth_trace dev_ids), so it
+    is the same at every world size.  The rank's devices are held in chunks of
+    C4_CHUNK devices, each with its own Context (segment entry states and sparse
+    records survive between the exact-stats passes; the first pass's transient
+    buffers are shared).  One step = the trace-fused decisions over all the
+    rank's queries + the serving replay with slow labels + the exact TPT stats
+    (three radix-select passes; counters, histograms and exact sums all-reduced
+    over NCCL).  Returns the record (every rank) with the max-over-ranks time."""
     import torch
 
     from paper_2503_01066_b200 import colosim as cs
 
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        init_dist(dist, torch, local)
-    ctx = cs.Context(local)
-    mine = [d for d in range(C4_FLEET) if d % world == rank][: args.c4_devices]
-    D, per = len(mine), args.c4_per_device
+    mine = [d for d in range(C4_FLEET) if d % world == rank]
+    if devices_cap:
+        mine = mine[:devices_cap]
+    per = args.c4_per_device
     g = cs.GpuProfile()
     models = (cs.ModelProfile(), cs.ModelProfile.phi14b_like())
-    sets = [cs.MapSet.build(ctx, m, g, mode=md) for m in models for md in (cs.TrainingMode.CPA, cs.TrainingMode.CPT)]
+    owner = cs.Context(local)
+    sets = [cs.MapSet.build(owner, m, g, mode=md) for m in models for md in (cs.TrainingMode.CPA, cs.TrainingMode.CPT)]
     profiles = [(m, g) for m in models]
-    arrival, prompt, output, offs = cs.synth_trace(ctx, [per] * D, [QPS[d % 4] for d in mine], 4040 + 7919 * rank)
-    dset = torch.tensor([dev_set_of(d) for d in mine], dtype=torch.int16, device="cuda")
-    dprof = torch.tensor([(d % 2) for d in mine], dtype=torch.int16, device="cuda")
-    n = D * per
-    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    parts, fparts = [], []
+    for c0 in range(0, len(mine), C4_CHUNK):
+        ch = mine[c0:c0 + C4_CHUNK]
+        cx = owner if c0 == 0 else cs.Context(local)
+        if cx is not owner:
+            cx.share_temps(owner)
+        arrival, prompt, output, offs = cs.synth_trace(cx, [per] * len(ch), [QPS[d % 4] for d in ch], C4_SEED,
+                                                       dev_ids=ch)
+        dset = torch.tensor([dev_set_of(d) for d in ch], dtype=torch.int16, device="cuda")
+        dprof = torch.tensor([d % 2 for d in ch], dtype=torch.int16, device="cuda")
+        parts.append((cx, arrival, prompt, output, offs, dprof))
+        fparts.append((cx, prompt, output, offs, dset))
+    nmax = max(p[1].shape[0] for p in fparts)
+    n = sum(p[1].shape[0] for p in fparts)
+    out = torch.empty(nmax, dtype=torch.int32, device="cuda")
     counters = torch.zeros(8, dtype=torch.int64, device="cuda")
-    group = None
 
     def step():
         counters.zero_()
-        cs.features_decide(ctx, sets, prompt, output, offs, dset, out=out, counters=counters)
-        st = cs.serving_stats(ctx, profiles, arrival, prompt, output, offs, dprof, tau=args.c4_tau, group=group)
+        for cx, prompt, output, offs, dset in fparts:
+            cs.features_decide(cx, sets, prompt, output, offs, dset, out=out[:prompt.shape[0]], counters=counters)
+        st = cs.fleet_stats(parts, profiles, tau=args.c4_tau)
         if dist:
             dist.all_reduce(counters)
         return st
 
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(max(warmup, 3) if steps else 0):
         st = step()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        l0 = ctx.launches()
+        l0 = sum(p[0].launches() for p in parts)
         ev0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             st = step()
         ev1.record()
-        launches = ctx.launches() - l0
         torch.cuda.synchronize()
+        launches = sum(p[0].launches() for p in parts) - l0
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    nt = torch.tensor([n], dtype=torch.int64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nt)
     sec = float(t.item()) / 1e3
-    total = world * n if dist else n
-    if rank == 0:
-        line = {"metric": "C4 fleet: admission decisions + serving replay labels + exact TPT stats, queries/s",
-                "value": total * args.steps / sec, "unit": "queries/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic",
-                "config": {"workload": f"C4: 1024-device fleet x {per} queries, device d on rank d % {world}; "
-                                       f"{D} devices ({n} queries) per rank this run",
-                           "per_step": "features_decide (all queries) + serving replay with slow labels + "
-                                       "3 radix-select stats passes, NCCL all-reduce of counters/histograms/exact sums",
-                           "tau_s": args.c4_tau, "parallelism": f"dp{world} (devices sharded by rank)"},
-                "stats": {k: st[k] for k in ("generated_tokens", "slow_tokens", "slow_queries", "batches", "p50", "p90",
-                                            "p99", "mean")},
-                "counters": dict(zip(cs.COUNTER_NAMES, [int(x) for x in counters.cpu().tolist()])),
-                "roofline": {"bound": "latency (sequential f64 time folds per device)", "achieved": None, "peak": None,
-                             "unit": "GB/s", "frac": None, "traffic": None},
-                "gpu_launches": launches, "clocks": clk.report()}
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                from oracle.oracle import default_model, phi14b_model
+    total = int(nt.item())
+    clocks = clk.report()
+    rec = {"metric": "C4 fleet: admission decisions + serving replay labels + exact TPT stats, queries/s",
+           "value": total * steps / sec, "unit": "queries/s", "n_gpus": world, "steps": steps, "warmup": max(warmup, 3),
+           "ms_per_step": float(t.item()) / steps, "higher_is_better": True, "scaling": "weak",
+           "per_rank_queries_per_s": n * steps / sec, "dtype": "u32+f64", "data": "synthetic",
+           "config": {"workload": f"C4: 1024-device fleet x {per} queries, fleet device g on rank g % {world}; "
+                                  f"{len(mine)} devices ({n} queries) per rank this run, "
+                                  f"{len(parts)} chunk(s) of <= {C4_CHUNK} devices",
+                      "devices_per_rank": len(mine), "queries_per_rank": n, "queries_total": total,
+                      "per_step": "features_decide (all queries) + serving replay with slow labels + "
+                                  "3 radix-select stats passes, NCCL all-reduce of counters/histograms/exact sums",
+                      "tau_s": args.c4_tau, "trace_seed": f"{C4_SEED}, keyed on the fleet device id",
+                      "l2": "inputs 16 GB/step per chunk > L2", "parallelism": f"dp{world} (devices sharded by rank)"},
+           "stats": {k: st[k] for k in ("generated_tokens", "slow_tokens", "slow_queries", "batches", "p50", "p90",
+                                        "p99", "mean", "mean_exact")},
+           "counters": dict(zip(cs.COUNTER_NAMES, [int(x) for x in counters.cpu().tolist()])),
+           "roofline": issue_roofline("c4", sec / steps, clocks, n),
+           "gpu_launches": launches, "clocks": clocks}
+    if cpu and world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import default_model, phi14b_model
 
-                threads = os.cpu_count() or 1
-                tr = reference_sample(arrival, prompt, output, offs, 16, 100_000, [default_model(), phi14b_model()])
-                nq, ts = reference_serving(tr, threads, with_stats=True)
-                line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
-                                        "cpu": cpu_model(),
-                                        "sample": f"first 100k queries of 16 of the rank's devices ({nq} queries), "
-                                                  f"Simulation::run ServingOnly + finalize via oracle/_ref, "
-                                                  f"{threads} host threads, {ts:.1f} s (the decision lookups "
-                                                  "are not included)"}
-            except Exception as e:
-                line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
-                                        "sample": f"unavailable: {e}"}
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
-    ctx.close()
+            threads = os.cpu_count() or 1
+            cx, arrival, prompt, output, offs, _ = parts[0]
+            tr = reference_sample(arrival, prompt, output, offs, 16, 100_000, [default_model(), phi14b_model()])
+            nq, ts = reference_serving(tr, threads, with_stats=True)
+            rec["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                   "cpu": cpu_model(),
+                                   "sample": f"first 100k queries of 16 of the rank's devices ({nq} queries), "
+                                             f"Simulation::run ServingOnly + finalize via oracle/_ref, "
+                                             f"{threads} host threads, {ts:.1f} s (the decision lookups "
+                                             "are not included)"}
+        except Exception as e:
+            rec["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    del parts, fparts, out
+    for s_ in sets:
+        s_.close()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rec
 
 
-def run_c3(args, world, rank, local):
-    """C3 (BASELINE.json configs[2]): 128 bursty devices x 7,812,500 queries =
-    1B queries per GPU, serving replay + slow labels + the first exact-stats
-    histogram pass.  tau = serving-only p99 of device 0's first 1M queries."""
+def run_c4(args, world, rank, local):
     import torch
-
-    from paper_2503_01066_b200 import colosim as cs
 
     torch.cuda.set_device(local)
     dist = None
@@ -829,9 +890,32 @@ def run_c3(args, world, rank, local):
         import torch.distributed as dist
 
         init_dist(dist, torch, local)
+    cap = args.c4_devices if args.c4_devices is not None else (None if world > 1 else C4_CHUNK)
+    rec = c4_measure(args, world, rank, local, dist, cap, args.steps, args.warmup, cpu=True)
+    if rank == 0:
+        print(json.dumps(rec), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def c3_measure(args, world, rank, local, dist, steps, warmup, cpu=False):
+    """C3 (BASELINE.json configs[2]): 128 bursty devices x 7,812,500 queries =
+    1B queries per GPU (qps 0.1 / 3.0 alternating every 600 s).  One step =
+    serving replay + slow labels + the first exact-stats histogram pass + the
+    replay-derived verdict of every batch (CPT/CPA alternate
+    by device with the profile -- llama8b/CPA even, phi14b/CPT odd).  tau =
+    serving-only p99 of device 0's first 1M queries."""
+    import torch
+
+    from paper_2503_01066_b200 import colosim as cs
+
     ctx = cs.Context(local)
     D, per = args.c3_devices, args.c3_per_device
-    profiles = [(cs.ModelProfile(), cs.GpuProfile()), (cs.ModelProfile.phi14b_like(), cs.GpuProfile())]
+    g = cs.GpuProfile()
+    profiles = [(cs.ModelProfile(), g), (cs.ModelProfile.phi14b_like(), g)]
+    sets = [cs.MapSet.build(ctx, profiles[0][0], g, mode=cs.TrainingMode.CPA),
+            cs.MapSet.build(ctx, profiles[1][0], g, mode=cs.TrainingMode.CPT)]
     arrival, prompt, output, offs = cs.synth_trace(ctx, [per] * D, [0.1] * D, 4242 + 7919 * rank,
                                                    dev_qps_hi=[3.0] * D, burst_period=600.0)
     dprof = torch.tensor([d % 2 for d in range(D)], dtype=torch.int16, device="cuda")
@@ -841,13 +925,14 @@ def run_c3(args, world, rank, local):
     tau = tau_stats["p99"]
     hist = torch.zeros(cs.HIST_BINS, dtype=torch.int64, device="cuda")
     n = D * per
+    verdicts = torch.empty(n, dtype=torch.int32, device="cuda")
 
     def step():
         hist.zero_()
         return cs.replay_serving(ctx, profiles, arrival, prompt, output, offs, dprof, tau=tau, labels=True,
-                                 summary=True, hist=hist)
+                                 summary=True, hist=hist, sets=sets, verdicts=verdicts)
 
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(max(warmup, 3)):
         r = step()
     torch.cuda.synchronize()
     if dist:
@@ -856,61 +941,94 @@ def run_c3(args, world, rank, local):
     with ClockSampler(local) as clk:
         l0 = ctx.launches()
         ev0.record()
-        for _ in range(args.steps):
+        for _ in range(steps):
             r = step()
         ev1.record()
-        launches = ctx.launches() - l0
         torch.cuda.synchronize()
+        launches = ctx.launches() - l0
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     S = cs.summaries_to_numpy(r["summary"])
+    # verdict outcome counts over every batch (COLO_V_OUTCOME: bits 21-22)
+    nb_dev = torch.from_numpy(S["batches"].astype(np.int64)).cuda()
+    offs_l = offs[:-1]
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    dev_of = torch.searchsorted(offs[1:], idx, right=True)
+    valid = (idx - offs_l[dev_of]) < nb_dev[dev_of]
+    outcome = ((verdicts.to(torch.int64) >> 21) & 3)[valid]
+    vc = torch.bincount(outcome, minlength=3)[:3]
+    del idx, dev_of, valid, outcome
     tot = torch.tensor([int(S["generated_tokens"].sum()), int(S["slow_tokens"].sum()), int(S["slow_queries"].sum()),
-                        int(S["batches"].sum())], dtype=torch.int64, device="cuda")
+                        int(S["batches"].sum())] + [int(x) for x in vc.tolist()], dtype=torch.int64, device="cuda")
     if dist:
         dist.all_reduce(tot)
         dist.all_reduce(hist)
     sec = float(t.item()) / 1e3
-    value = world * n * args.steps / sec
-    if rank == 0:
-        gen, slow_tok, slow_q, nb = [int(x) for x in tot.cpu().tolist()]
-        peaks = measured_peaks()
-        peak = peaks.get("hbm_gbs", 6650.0)
-        achieved = 17 * n / (sec / args.steps) / 1e9  # 16 B/query read + 1 B label written
-        line = {"metric": "serving-replay labeling queries/s (C3)", "value": value, "unit": "queries/s",
-                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": f"C3: {D} bursty devices x {per} queries per GPU (qps 0.1/3.0 alternating "
-                                       "every 600 s), serving-only replay + slow labels + exact-stats pass 1",
-                           "tau_s": tau, "tau_rule": "serving-only p99 of device 0's first 1M queries",
-                           "l2": "inputs 16 GB/step > L2", "parallelism": f"dp{world}"},
-                "tokens_per_s": world * gen * args.steps / sec,
-                "labels": {"tokens": gen, "slow_tokens": slow_tok, "slow_queries": slow_q, "batches": nb},
-                "roofline": {"bound": "latency (sequential f64 time fold per device)", "achieved": achieved,
-                             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None},
-                "gpu_launches": launches, "clocks": clk.report()}
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                from oracle.oracle import default_model, phi14b_model
+    gen, slow_tok, slow_q, nb, v_admit, v_free, v_recomp = [int(x) for x in tot.cpu().tolist()]
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    clocks = clk.report()
+    hbm = 17 * n / (sec / steps) / 1e9  # 16 B/query read + 1 B label written
+    rec = {"metric": "C3: bursty serving replay + slow labels + replay-derived verdicts, queries/s",
+           "value": world * n * steps / sec, "unit": "queries/s", "n_gpus": world, "steps": steps,
+           "warmup": max(warmup, 3), "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64+u32", "data": "synthetic",
+           "decisions_per_s": nb * steps / sec, "tokens_per_s": gen * steps / sec,
+           "config": {"workload": f"C3: {D} bursty devices x {per} queries per GPU (qps 0.1/3.0 alternating "
+                                  "every 600 s), serving-only replay + slow labels + exact-stats pass 1 + one verdict "
+                                  "per batch (llama8b/CPA even devices, phi14b/CPT odd)",
+                      "tau_s": tau, "tau_rule": "serving-only p99 of device 0's first 1M queries",
+                      "decision_rule": "cached = charged tokens of the device's last single-query batch, incoming = "
+                                       "max_incoming, batch = n, pending 0, dev_layers L (SURVEY §8(d) C3)",
+                      "l2": "inputs 16 GB/step > L2", "parallelism": f"dp{world}"},
+           "labels": {"tokens": gen, "slow_tokens": slow_tok, "slow_queries": slow_q, "batches": nb},
+           "verdicts": {"admit": v_admit, "free_loadback": v_free, "recompute_drop": v_recomp},
+           "roofline": issue_roofline("c3", sec / steps, clocks, n),
+           "hbm": {"achieved": hbm, "peak": peak, "unit": "GB/s", "frac": hbm / peak,
+                   "note": "17 B/query algorithmic; the replay is bound by dependent f64 time chains, not HBM"},
+           "gpu_launches": launches, "clocks": clocks}
+    if cpu and world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import default_model, phi14b_model
 
-                threads = os.cpu_count() or 1
-                tr = reference_sample(arrival, prompt, output, offs, 16, 250_000, [default_model(), phi14b_model()])
-                nq, ts = reference_serving(tr, threads)
-                line["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
-                                        "cpu": cpu_model(),
-                                        "sample": f"first 250k queries of 16 of the C3 devices ({nq} queries), "
-                                                  f"Simulation::run ServingOnly via oracle/_ref, {threads} host "
-                                                  f"threads, {ts:.1f} s"}
-            except Exception as e:
-                line["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
-                                        "sample": f"unavailable: {e}"}
-        print(json.dumps(line), flush=True)
+            threads = os.cpu_count() or 1
+            tr = reference_sample(arrival, prompt, output, offs, 16, 250_000, [default_model(), phi14b_model()])
+            nq, ts = reference_serving(tr, threads)
+            rec["cpu_baseline"] = {"value": nq / ts, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                   "cpu": cpu_model(),
+                                   "sample": f"first 250k queries of 16 of the C3 devices ({nq} queries), "
+                                             f"Simulation::run ServingOnly via oracle/_ref, {threads} host "
+                                             f"threads, {ts:.1f} s"}
+        except Exception as e:
+            rec["cpu_baseline"] = {"value": None, "unit": "queries/s", "cores": 0, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    del r, arrival, prompt, output, verdicts
+    for s_ in sets:
+        s_.close()
+    ctx.release_scratch()
+    ctx.close()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rec
+
+
+def run_c3(args, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        init_dist(dist, torch, local)
+    rec = c3_measure(args, world, rank, local, dist, args.steps, args.warmup, cpu=True)
+    if rank == 0:
+        print(json.dumps(rec), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
-    ctx.close()
 
 
 def main():
@@ -924,7 +1042,11 @@ def main():
                          "reference Simulation; c3: 1B-query bursty replay + labels; c5: map vs exact sweep; "
                          "c4: 1024-device fleet sharded by rank (decisions + replay + exact stats, NCCL reduce); "
                          "colo: colocated replay (C1 trace + device fleet)")
-    ap.add_argument("--c4-devices", type=int, default=128, help="devices per rank (cap)")
+    ap.add_argument("--c4-devices", type=int, default=None,
+                    help="cap on devices per rank (default: all of the rank's 1024/world at world >= 2, "
+                         "the 8-GPU share of 128 at world 1)")
+    ap.add_argument("--sub-steps", type=int, default=3, help="timed steps of the C3/C4 sub-records of the headline")
+    ap.add_argument("--no-sub", action="store_true", help="headline line without the C3/C4 sub-records")
     ap.add_argument("--c4-per-device", type=int, default=C4_PER_DEVICE)
     ap.add_argument("--c4-tau", type=float, default=0.05)
     ap.add_argument("--colo-devices", type=int, default=1184)  # 8 resident warps x 148 SMs

@@ -33,6 +33,8 @@
  *                                                                    include/colosim/engine.hpp:297, 422-423
  *   colo_features_decide(_host)     per-query feature extraction fused with the decision
  *                                   (SURVEY.md §8(d) C2 rule)
+ *   colo_validate_trace             validate_trace (stable sort by (arrival, id), checks)
+ *                                                                    include/colosim/workload.hpp:164-188
  *   colo_replay_serving             Simulation::run in SimMode::ServingOnly
  *                                                                    include/colosim/engine.hpp:140-164, 270-387
  *   colo_replay_colocated           Simulation::run in SimMode::Colocated (the admission loop:
@@ -174,6 +176,14 @@ colo_status colo_sync(colo_ctx* ctx);
  * billion-query replay -- decode tables, host-pipeline buffers).  They are
  * re-created on demand; colo_ctx_destroy frees them too. */
 colo_status colo_ctx_release_scratch(colo_ctx* ctx);
+/* Let ctx use owner's per-call replay temporaries (the serving replay's
+ * all-queued batch records and their step-duration pool, only live during one
+ * colo_replay_serving call) instead of growing its own.  For several contexts
+ * that each hold one chunk of a rank's devices across the three exact-stats
+ * passes (their segment entry states and sparse-pass records stay per
+ * context): calls on ctx and owner must not overlap (one host thread, one
+ * stream).  owner = NULL or ctx restores ctx's own buffers. */
+colo_status colo_ctx_share_temps(colo_ctx* ctx, colo_ctx* owner);
 const char* colo_last_error(const colo_ctx* ctx);
 int colo_ctx_sm_count(const colo_ctx* ctx);
 /* Kernels this context has launched so far (the library's own kernels; the
@@ -294,17 +304,36 @@ typedef struct colo_replay_opts {
     uint32_t filter_shift;            /* 63 with prefix 0 selects every sample */
     uint32_t segment_len;             /* queries per replay segment (0 = automatic), see below */
     uint64_t filter_prefix[3];
-    uint32_t reuse_entries;           /* 1: the previous call on this context replayed the same trace
-                                         (same buffers, sizes, profiles, segment_len): skip validation,
-                                         speculation and resolution and reuse its segment entry states
-                                         (histogram passes 2-3 of the exact-stats protocol).  Falls back
-                                         to a full replay when the context cannot prove that. */
+    uint32_t reuse_entries;           /* 1: the previous call on this context replayed the same trace:
+                                         skip validation, speculation and resolution and reuse its segment
+                                         entry states (histogram passes 2-3 of the exact-stats protocol).
+                                         The context checks the buffers' addresses, the sizes, the profile
+                                         contents and segment_len, and replays in full when they differ;
+                                         it cannot see the buffers' contents, so the CALLER must guarantee
+                                         the trace arrays were not rewritten in between. */
     uint32_t stats_mode;              /* sparse exact-stats passes: 1 = also record, per batch, its start
                                          and the range of its samples' top-21-bit bins (the first histogram
                                          pass); 2 (with reuse_entries, after a mode-1 call on the same
                                          trace) = replay only the batches whose range covers a filter bin
                                          (the narrowing passes; same histograms).  0 = off. */
+    uint32_t* d_verdicts;             /* [n] replay-derived verdict of batch b of device d at
+                                         d_dev_offsets[d] + b (needs sets; the same words d_batches'
+                                         verdict field carries, without the 40 B records: SURVEY §8(d)
+                                         C3, engine.hpp:513-557 composed per batch).  NULL = none. */
 } colo_replay_opts;
+
+/* validate_trace (workload.hpp:164-188) on the device, for every device of a
+ * CSR trace: each device's rows [off[d], off[d+1]) are reordered in place by
+ * (arrival, query_id) -- the reference's stable_sort -- across every given
+ * column.  EVALIDATION (colo_last_error names the query, in the reference's
+ * words) for a negative or NaN arrival, zero prompt or output tokens, or a
+ * query_id repeated within one device.  d_query_id may be NULL (ids = the row
+ * order, so equal arrivals keep their order); d_label_delay may be NULL.
+ * n < 2^32.  Synchronous.  The replay entry points below take validated
+ * traces (they reject unsorted input). */
+colo_status colo_validate_trace(colo_ctx* ctx, uint64_t* d_query_id, double* d_arrival, uint32_t* d_prompt,
+                                uint32_t* d_output, double* d_label_delay, size_t n, const uint64_t* d_dev_offsets,
+                                size_t ndev);
 
 /* Serving-only replay of every device's trace.  Each device is cut into
  * segments of segment_len queries; the replay runs in three passes:
@@ -515,6 +544,14 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
                              const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
                              double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
                              uint32_t* d_output);
+/* The same with the RNG keyed on (d_dev_ids[d], query index within the
+ * device) instead of the global query index, so fleet device g's trace is the
+ * same whichever rank or array position holds it (C4: device g on rank
+ * g % world at every world size).  Device ids < 2^28, devices < 2^36 queries. */
+colo_status colo_synth_fleet_trace(colo_ctx* ctx, const double* h_bin_values, const double* h_bin_probs, size_t nbins,
+                                   const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
+                                   double burst_period, size_t ndev, const uint32_t* d_dev_ids, uint64_t seed,
+                                   double* d_arrival, uint32_t* d_prompt, uint32_t* d_output);
 
 /* ------------------------------------------------------------ file formats */
 /* Offloading / hedging map text files, byte-identical to OffloadingMap::save /

@@ -439,14 +439,13 @@ int orc_replay_serving(const orc_model* m, const orc_gpu* g, const double* arriv
     }
     uint64_t max_need_total = 0, sample_pos = 0, slot_charged = 0;
     double T = -INFINITY;
-    uint64_t head = 0;
+    uint64_t head = 0, tail = 0;
     while (head < n) {
-        uint64_t tail;
         if (arrival[head] > T) {                 /* idle: first arrival starts a batch alone */
             T = arrival[head];
             tail = head + 1;
         } else {                                 /* queued: everything that arrived by T */
-            tail = head;
+            if (tail < head) tail = head;        /* T never decreases: resume the scan (linear overall) */
             while (tail < n && arrival[tail] <= T) ++tail;
         }
         uint64_t end = head, need_total = 0;

@@ -409,6 +409,28 @@ class OracleLib:
         res["pctl"] = pctl
         return res
 
+    def serving_samples(self, m, g, arrival, prompt, output, want_samples=True):
+        """oracle/_ref only: the reference's Simulation::run (ServingOnly) without
+        its event log.  Returns dict(samples, generated_tokens, peak_device_bytes, pctl)."""
+        assert self.which == "ref"
+        arrival = np.ascontiguousarray(arrival, np.float64)
+        prompt = np.ascontiguousarray(prompt, np.uint32)
+        output = np.ascontiguousarray(output, np.uint32)
+        n = len(prompt)
+        ns = int(output.astype(np.uint64).sum())
+        samples = np.empty(max(ns, 1), np.float64) if want_samples else None
+        gen, peak = C.c_uint64(0), C.c_uint64(0)
+        pctl = np.full(4, np.nan)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p) if a is not None else None
+        f = self.lib.ref_serving_samples
+        f.restype = C.c_int
+        rc = f(C.byref(m), C.byref(g), vp(arrival), vp(prompt), vp(output), C.c_uint64(n), vp(samples), C.byref(gen),
+               C.byref(peak), vp(pctl))
+        if rc:
+            raise ValueError(f"ref_serving_samples rc={rc}")
+        return {"samples": samples[:ns] if samples is not None else None, "generated_tokens": gen.value,
+                "peak_device_bytes": peak.value, "pctl": pctl}
+
     def replay_colocated(self, m, g, grid, cpa, arrival, prompt, output, label_delay=None, cache_timeout=60.0,
                          tau=float("inf"), want_samples=True, want_batches=True, sim_mode="colocated", cells=None):
         """Simulation::run in ``sim_mode`` (colocated | baseline | serving-only; maps from build_maps).

@@ -407,6 +407,44 @@ int ref_replay_serving(const orc_model* m, const orc_gpu* g, const double* arriv
     }
 }
 
+/* Serving-only Simulation::run without the event log (for BASELINE-size
+ * devices, whose log would not fit in host memory): the reference's TPT
+ * samples in its own order, generated_tokens, peak_device_bytes and its
+ * finalize (pctl[0..3] = p50, p90, p99, mean; NaN without samples).
+ * samples may be NULL. */
+int ref_serving_samples(const orc_model* m, const orc_gpu* g, const double* arrival, const uint32_t* prompt,
+                        const uint32_t* output, uint64_t n, double* samples, uint64_t* generated_tokens,
+                        uint64_t* peak_device_bytes, double* pctl) {
+    try {
+        SimConfig cfg;
+        cfg.mode = SimMode::ServingOnly;
+        cfg.model = to_model(m);
+        cfg.gpu = to_gpu(g);
+        cfg.trace.records.reserve(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            QueryRecord r;
+            r.query_id = i;
+            r.arrival_time = arrival[i];
+            r.prompt_tokens = prompt[i];
+            r.output_tokens = output[i];
+            cfg.trace.records.push_back(r);
+        }
+        validate_trace(cfg.trace);
+        MetricsReport rep = run_simulation(std::move(cfg));
+        *generated_tokens = rep.generated_tokens;
+        *peak_device_bytes = rep.peak_device_bytes;
+        const double nan = std::nan("");
+        pctl[0] = rep.tpt_p50 ? *rep.tpt_p50 : nan;
+        pctl[1] = rep.tpt_p90 ? *rep.tpt_p90 : nan;
+        pctl[2] = rep.tpt_p99 ? *rep.tpt_p99 : nan;
+        pctl[3] = rep.tpt_mean ? *rep.tpt_mean : nan;
+        if (samples) std::memcpy(samples, rep.tpt_samples.data(), rep.tpt_samples.size() * sizeof(double));
+        return ORC_OK;
+    } catch (const std::exception&) {
+        return ORC_EVALIDATION;
+    }
+}
+
 /* Colocated replay through the reference's own Simulation::run in
  * SimMode::Colocated (engine.hpp:140-822) with maps from build_maps
  * (experiment.hpp:144-152: hedge grid = the offload grid's cached axis,

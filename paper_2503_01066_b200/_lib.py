@@ -92,6 +92,7 @@ class ReplayOpts(C.Structure):
         ("filter_prefix", C.c_uint64 * 3),
         ("reuse_entries", C.c_uint32),
         ("stats_mode", C.c_uint32),
+        ("d_verdicts", C.c_void_p),
     ]
 
 
@@ -173,11 +174,11 @@ EXPORTS = [
     "colo_validate_grid", "colo_mapset_build", "colo_mapset_from_cells", "colo_mapset_shape",
     "colo_mapset_cells", "colo_mapset_hash", "colo_mapset_destroy", "colo_decide", "colo_decide_exact",
     "colo_features_decide", "colo_features_decide_host", "colo_decide_host", "colo_features",
-    "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
-    "colo_generate_trace", "colo_synth_trace", "colo_synth_tuples", "colo_compare_verdicts",
+    "colo_validate_trace", "colo_replay_serving", "colo_hist_select", "colo_nearest_rank_index", "colo_serving_stats",
+    "colo_generate_trace", "colo_synth_trace", "colo_synth_fleet_trace", "colo_synth_tuples", "colo_compare_verdicts",
     "colo_map_save", "colo_map_load", "colo_mapset_save", "colo_mapset_load", "colo_load_trace_jsonl",
     "colo_load_histogram_jsonl", "colo_replay_colocated", "colo_colocated_stats", "colo_trace_hash",
-    "colo_sort_f64", "colo_json_doubles", "colo_ctx_release_scratch", "colo_stats_allreduce",
+    "colo_sort_f64", "colo_json_doubles", "colo_ctx_release_scratch", "colo_ctx_share_temps", "colo_stats_allreduce",
     "colo_serving_stats_nccl", "colo_finalize", "colo_ctx_launches", "colo_colocated_events", "colo_events_text",
 ]
 
@@ -206,6 +207,7 @@ def lib() -> C.CDLL:
         "colo_ctx_stream": (vp, [vp]),
         "colo_sync": (i32, [vp]),
         "colo_ctx_release_scratch": (i32, [vp]),
+        "colo_ctx_share_temps": (i32, [vp, vp]),
         "colo_stats_allreduce": (i32, [vp, vp, vp, sz]),
         "colo_serving_stats_nccl": (i32, [vp, vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, dbl, vp,
                                          C.POINTER(DeviceSummary)]),
@@ -231,6 +233,7 @@ def lib() -> C.CDLL:
         "colo_features_decide_host": (i32, [vp, vp, sz, vp, vp, sz, vp, vp, sz, vp, vp]),
         "colo_decide_host": (i32, [vp, vp, vp, sz, vp, vp]),
         "colo_features": (i32, [vp, MP, i32, vp, vp, sz, vp, vp, vp]),
+        "colo_validate_trace": (i32, [vp, vp, vp, vp, vp, vp, sz, vp, sz]),
         "colo_replay_serving": (i32, [vp, MP, GP, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ReplayOpts)]),
         "colo_hist_select": (i32, [vp, sz, u64, C.POINTER(C.c_uint32), C.POINTER(u64)]),
         "colo_nearest_rank_index": (u64, [dbl, u64]),
@@ -247,6 +250,7 @@ def lib() -> C.CDLL:
         "colo_colocated_stats": (i32, [vp, vp, sz, vp, vp, vp, sz, vp, vp, sz, C.POINTER(ColocatedOpts), vp,
                                        C.POINTER(ColocatedSummary)]),
         "colo_synth_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, u64, vp, vp, vp]),
+        "colo_synth_fleet_trace": (i32, [vp, vp, vp, sz, vp, vp, vp, dbl, sz, vp, u64, vp, vp, vp]),
         "colo_synth_tuples": (i32, [vp, u64, sz, C.c_uint32, vp, vp, sz, vp]),
         "colo_compare_verdicts": (i32, [vp, vp, vp, sz, C.c_uint32, vp]),
         "colo_map_save": (i32, [C.c_char_p, C.POINTER(MapHeader), vp, sz]),

@@ -232,6 +232,13 @@ class Context:
         """Free the context's grow-only device scratch (colo_ctx_release_scratch)."""
         check(lib().colo_ctx_release_scratch(self.h), self.h)
 
+    def share_temps(self, owner: "Context") -> None:
+        """Use ``owner``'s per-call replay temporaries (colo_ctx_share_temps):
+        chunk contexts of one rank keep their own pass state but share the
+        first pass's transient buffers."""
+        self._temps_owner = owner  # keep the owner alive while borrowed
+        check(lib().colo_ctx_share_temps(self.h, owner.h if owner is not None else None), self.h)
+
     def close(self) -> None:
         if getattr(self, "h", None):
             lib().colo_ctx_destroy(self.h)
@@ -606,14 +613,32 @@ def _profiles_arrays(profiles: Sequence[Tuple[ModelProfile, GpuProfile]]):
     return ms, gs
 
 
+def validate_trace(ctx: Context, arrival, prompt, output, dev_offsets, query_id=None, label_delay=None) -> None:
+    """validate_trace (workload.hpp:164-188) in place on device tensors: every
+    device's rows ordered by (arrival, query_id) across all given columns;
+    raises ColoValidationError (the reference's message) for a negative
+    arrival, zero tokens or a repeated query_id within a device."""
+    _need_cuda(arrival, "arrival", 8)
+    _need_cuda(prompt, "prompt", 4)
+    _need_cuda(output, "output", 4)
+    _need_cuda(dev_offsets, "dev_offsets", 8)
+    _need_cuda(query_id, "query_id", 8)
+    _need_cuda(label_delay, "label_delay", 8)
+    check(lib().colo_validate_trace(ctx.h, _ptr(query_id), _ptr(arrival), _ptr(prompt), _ptr(output),
+                                    _ptr(label_delay), prompt.shape[0], _ptr(dev_offsets), dev_offsets.shape[0] - 1),
+          ctx.h, "validate_trace")
+
+
 def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfile]], arrival, prompt, output,
                    dev_offsets, dev_profile, tau: float = math.inf, sets: Optional[Sequence[MapSet]] = None,
                    samples: bool = False, labels: bool = True, batches: bool = False, summary: bool = True,
                    hist=None, hist_shift: int = 42, filter_shift: int = 63, filter_prefix=(0,), segment_len: int = 0,
-                   reuse_entries: bool = False, stats_mode: int = 0):
+                   reuse_entries: bool = False, stats_mode: int = 0, verdicts=None):
     """Serving-only replay of every device (engine.hpp:140-387, SimMode::ServingOnly).
     Returns a dict of device tensors: samples (f64, reference order),
-    labels (u8 per query), batches (raw bytes, BATCH_DTYPE), summary (DeviceSummary bytes)."""
+    labels (u8 per query), batches (raw bytes, BATCH_DTYPE), summary (DeviceSummary bytes),
+    verdicts (u32 per batch: device d's batch b at dev_offsets[d] + b; needs ``sets``;
+    ``verdicts`` may be True or a caller-owned int32 tensor of n words)."""
     torch = _torch()
     dev = prompt.device
     _need_cuda(arrival, "arrival", 8)
@@ -650,6 +675,16 @@ def replay_serving(ctx: Context, profiles: Sequence[Tuple[ModelProfile, GpuProfi
     if batches:
         res["batches"] = torch.zeros((max(n, 1), BATCH_DTYPE.itemsize), dtype=torch.uint8, device=dev)
         opts.d_batches = res["batches"].data_ptr()
+    if verdicts is not None and verdicts is not False:
+        if sets is None:
+            raise ColoError(_lib.COLO_EINVAL, "replay-derived verdicts need map sets")
+        if verdicts is True:
+            verdicts = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)[:n]
+        _need_cuda(verdicts, "verdicts", 4)
+        if verdicts.shape[0] < n:
+            raise ColoError(_lib.COLO_EINVAL, "verdicts buffer shorter than the trace")
+        res["verdicts"] = verdicts
+        opts.d_verdicts = verdicts.data_ptr() if n else 0
     if summary:
         res["summary"] = torch.zeros((ndev, C.sizeof(_lib.DeviceSummary)), dtype=torch.uint8, device=dev)
         opts.d_summary = res["summary"].data_ptr()
@@ -691,9 +726,19 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
     metrics.hpp:56-66) by three radix-select replay passes; with a
     torch.distributed ``group`` the histograms, counters and exact sums are
     all-reduced across ranks (each rank holds its own device shard)."""
+    return fleet_stats([(ctx, arrival, prompt, output, dev_offsets, dev_profile)], profiles, tau, group, quantiles)
+
+
+def fleet_stats(parts, profiles, tau: float = math.inf, group=None, quantiles=(0.50, 0.90, 0.99)):
+    """serving_stats over a rank's devices held as several parts (chunks of
+    devices, each with its own Context so its replay scratch -- segment entry
+    states and the sparse passes' batch records -- survives between the three
+    passes).  ``parts``: list of (ctx, arrival, prompt, output, dev_offsets,
+    dev_profile); every pass replays every part into the same histogram, so
+    the result equals one replay over the union of the parts' devices."""
     torch = _torch()
     dist = torch.distributed if (torch.distributed.is_available() and torch.distributed.is_initialized()) else None
-    dev = prompt.device
+    dev = parts[0][2].device
     hist = torch.zeros(len(quantiles) * HIST_BINS, dtype=torch.int64, device=dev)
     sparse = os.environ.get("COLO_SPARSE_STATS", "1") != "0"
 
@@ -701,20 +746,26 @@ def serving_stats(ctx: Context, profiles, arrival, prompt, output, dev_offsets, 
         h = hist[: len(prefixes) * HIST_BINS]
         h.zero_()
         first = filter_shift == 63
-        r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
-                           summary=first, hist=h, hist_shift=hist_shift, filter_shift=filter_shift,
-                           filter_prefix=tuple(prefixes), reuse_entries=not first,
-                           stats_mode=(1 if first else 2) if sparse else 0)
-        if not first:
-            return h, None
-        S = summaries_to_numpy(r["summary"])
-        return h, {"generated_tokens": int(S["generated_tokens"].sum()), "slow_tokens": int(S["slow_tokens"].sum()),
-                   "slow_queries": int(S["slow_queries"].sum()), "batches": int(S["batches"].sum()),
-                   "flags": int(np.bitwise_or.reduce(S["flags"])) if len(S) else 0,
-                   "exact_sum": sum(int(a) | (int(b) << 64) | (int(c) << 128) for a, b, c in S["tpt_sum"])}
+        tot = {"generated_tokens": 0, "slow_tokens": 0, "slow_queries": 0, "batches": 0, "flags": 0, "exact_sum": 0}
+        for ctx, arrival, prompt, output, dev_offsets, dev_profile in parts:
+            r = replay_serving(ctx, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=tau, labels=False,
+                               summary=first, hist=h, hist_shift=hist_shift, filter_shift=filter_shift,
+                               filter_prefix=tuple(prefixes), reuse_entries=not first,
+                               stats_mode=(1 if first else 2) if sparse else 0)
+            if not first:
+                continue
+            S = summaries_to_numpy(r["summary"])
+            for k in ("generated_tokens", "slow_tokens", "slow_queries", "batches"):
+                tot[k] += int(S[k].sum())
+            tot["flags"] |= int(np.bitwise_or.reduce(S["flags"])) if len(S) else 0
+            tot["exact_sum"] += sum(int(a) | (int(b) << 64) | (int(c) << 128) for a, b, c in S["tpt_sum"])
+        return h, (tot if first else None)
 
     reduce = (lambda t: dist.all_reduce(t, group=group)) if dist is not None else None
     return stats_protocol(run_pass, reduce, quantiles)
+
+
+FLAG_BITS = 8  # low flag bits OR-ed across ranks (bit 0: a sample outside the exact fixed-point sum's range)
 
 
 def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
@@ -730,18 +781,20 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
     nf = len(quantiles)
     hist, tot = run_pass(42, 63, (0,))
     exact = tot["exact_sum"]
-    # int64-safe all-reduce: counters, then the exact sum as 32-bit chunks
-    vec = torch.tensor([tot["generated_tokens"], tot["slow_tokens"], tot["slow_queries"], tot["batches"], tot["flags"]]
-                       + [(exact >> (32 * i)) & 0xFFFFFFFF for i in range(8)], dtype=torch.int64, device=hist.device)
+    # int64-safe all-reduce: counters, the exact sum as 32-bit chunks, and the
+    # flag word OR-ed across ranks as per-bit counts (a sum-only reduction)
+    fl = int(tot["flags"])
+    vec = torch.tensor([tot["generated_tokens"], tot["slow_tokens"], tot["slow_queries"], tot["batches"]]
+                       + [(exact >> (32 * i)) & 0xFFFFFFFF for i in range(8)]
+                       + [(fl >> b) & 1 for b in range(FLAG_BITS)], dtype=torch.int64, device=hist.device)
     if reduce is not None:
-        flags = vec[4].clone()
         reduce(vec)
-        vec[4] = flags  # flags are OR-ed below from the local value (informational)
         reduce(hist)
     v = [int(x) for x in vec.cpu().tolist()]
-    exact = sum(c << (32 * i) for i, c in enumerate(v[5:]))
+    exact = sum(c << (32 * i) for i, c in enumerate(v[4:12]))
+    flags = (fl & ~((1 << FLAG_BITS) - 1)) | sum(1 << b for b, c in enumerate(v[12:]) if c)
     n = v[0]
-    out = {"generated_tokens": n, "slow_tokens": v[1], "slow_queries": v[2], "batches": v[3], "flags": v[4],
+    out = {"generated_tokens": n, "slow_tokens": v[1], "slow_queries": v[2], "batches": v[3], "flags": flags,
            "exact_sum": exact}
     if n == 0:
         out.update({f"p{int(round(q * 100))}": None for q in quantiles})
@@ -764,6 +817,9 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
     for q, p in zip(quantiles, prefixes):
         out[f"p{int(round(q * 100))}"] = float(np.array([p], np.uint64).view(np.float64)[0])
     out["mean"] = float(Fraction(exact, 1 << 96) / n)
+    # bit 0/1: a sample below the sum's 2^-96 resolution or beyond its range on some rank -- the
+    # exact-sum mean is then not exact (the percentiles and counters still are)
+    out["mean_exact"] = not (flags & 3)
     return out
 
 
@@ -1033,11 +1089,14 @@ def compare_verdicts(ctx: Context, map_verdicts, exact_verdicts, num_layers: int
 
 
 def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float], seed: int, bins=None,
-                dev_qps_hi: Optional[Sequence[float]] = None, burst_period: float = 0.0):
+                dev_qps_hi: Optional[Sequence[float]] = None, burst_period: float = 0.0,
+                dev_ids: Optional[Sequence[int]] = None):
     """Bench-scale synthetic device traces generated on the GPU (counter-based
     RNG); bursty when dev_qps_hi/burst_period are given (rate alternates every
-    burst_period seconds).  Returns (arrival f64, prompt i32, output i32,
-    dev_offsets i64) CUDA tensors."""
+    burst_period seconds).  ``dev_ids``: fleet device ids -- the RNG is then
+    keyed on (id, query index in the device), so a device's trace does not
+    depend on which rank or array position holds it.  Returns (arrival f64,
+    prompt i32, output i32, dev_offsets i64) CUDA tensors."""
     torch = _torch()
     v, p = bins if bins is not None else sharegpt_histogram()
     dev = torch.device("cuda", ctx.device)
@@ -1051,9 +1110,17 @@ def synth_trace(ctx: Context, dev_sizes: Sequence[int], dev_qps: Sequence[float]
     v = np.ascontiguousarray(v, np.float64)
     p = np.ascontiguousarray(p, np.float64)
     d_hi = torch.tensor(list(dev_qps_hi), dtype=torch.float64, device=dev) if dev_qps_hi is not None else None
-    check(lib().colo_synth_trace(ctx.h, v.ctypes.data, p.ctypes.data, len(v), _ptr(d_off), _ptr(d_qps), _ptr(d_hi),
-                                 burst_period, len(dev_qps), seed, _ptr(arrival), _ptr(prompt), _ptr(output)),
-          ctx.h, "synth_trace")
+    if dev_ids is None:
+        check(lib().colo_synth_trace(ctx.h, v.ctypes.data, p.ctypes.data, len(v), _ptr(d_off), _ptr(d_qps), _ptr(d_hi),
+                                     burst_period, len(dev_qps), seed, _ptr(arrival), _ptr(prompt), _ptr(output)),
+              ctx.h, "synth_trace")
+    else:
+        ids = torch.tensor(list(dev_ids), dtype=torch.int32, device=dev)
+        if len(dev_ids) != len(dev_qps) or (len(dev_ids) and (min(dev_ids) < 0 or max(dev_ids) >= 1 << 28)):
+            raise ColoInvalidArgument(_lib.COLO_EINVAL, "dev_ids: one id in [0, 2^28) per device")
+        check(lib().colo_synth_fleet_trace(ctx.h, v.ctypes.data, p.ctypes.data, len(v), _ptr(d_off), _ptr(d_qps),
+                                           _ptr(d_hi), burst_period, len(dev_qps), _ptr(ids), seed, _ptr(arrival),
+                                           _ptr(prompt), _ptr(output)), ctx.h, "synth_trace")
     return arrival, prompt, output, d_off
 
 

@@ -18,6 +18,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -319,6 +320,9 @@ std::vector<Report> run_simulations(Context& ctx, const std::vector<SimConfig>& 
                 a.push_back(r.arrival_time);
                 p.push_back(static_cast<std::uint32_t>(r.prompt_tokens));
                 o.push_back(static_cast<std::uint32_t>(r.output_tokens));
+                // the device keeps "no label" as a negative delay: a present negative delay is refused
+                if (r.label_delay && !(*r.label_delay >= 0.0))
+                    throw std::invalid_argument("colo-b200: negative or NaN label_delay is not supported");
                 ld.push_back(r.label_delay ? *r.label_delay : -1.0);
             }
             std::uint64_t ns = soff.back();
@@ -341,6 +345,7 @@ std::vector<Report> run_simulations(Context& ctx, const std::vector<SimConfig>& 
         check(colo_dev_alloc(c, nd * sizeof(colo_colocated_summary), &d_sum), c, "alloc");
         std::vector<colo_colocated_summary> sum(nd);
         std::vector<double> smp(ns);
+        std::vector<std::array<double, 4>> fin(nd);  // finalize per report, on the device
         colo_status st = COLO_OK;
         try {
             check(colo_memcpy_h2d(c, d_a, a.data(), n * 8), c, "h2d");
@@ -365,6 +370,11 @@ std::vector<Report> run_simulations(Context& ctx, const std::vector<SimConfig>& 
             if (st != COLO_OK && st != COLO_EBREACH) check(st, c, "run_simulation");
             check(colo_memcpy_d2h(c, sum.data(), d_sum, nd * sizeof(colo_colocated_summary)), c, "d2h");
             check(colo_memcpy_d2h(c, smp.data(), d_s, ns * 8), c, "d2h");
+            for (std::size_t k = 0; k < nd; ++k)  // finalize (metrics.hpp:56-69), bit-exact: colo_finalize
+                if (sum[k].status == COLO_OK && sum[k].generated_tokens)
+                    check(colo_finalize(c, static_cast<const double*>(d_s) + soff[k], sum[k].generated_tokens, nullptr,
+                                        fin[k].data()),
+                          c, "finalize");
         } catch (...) {
             for (void* q : {d_a, d_p, d_o, d_ld, d_off, d_soff, d_set, d_sm, d_s, d_sum}) colo_dev_free(c, q);
             for (auto* ms : sets) colo_mapset_destroy(ms);
@@ -396,20 +406,12 @@ std::vector<Report> run_simulations(Context& ctx, const std::vector<SimConfig>& 
             r.generated_tokens = s.generated_tokens;
             r.trace_hash = cfg.trace.content_hash();                                   // engine.hpp:157
             r.mode_tag = std::string(to_string(cfg.mode)) + "/" + to_string(cfg.training);  // :158
-            // finalize (metrics.hpp:56-69) on the host copy of the samples
+            // finalize (metrics.hpp:56-69): nearest ranks and the sorted sequential mean from colo_finalize
             if (!r.tpt_samples.empty()) {
-                std::vector<double> sorted = r.tpt_samples;
-                std::sort(sorted.begin(), sorted.end());
-                auto rank = [&](double q) {
-                    std::size_t k2 = static_cast<std::size_t>(std::ceil(q * static_cast<double>(sorted.size())));
-                    return sorted[(k2 == 0 ? 1 : k2) - 1];
-                };
-                r.tpt_p50 = rank(0.50);
-                r.tpt_p90 = rank(0.90);
-                r.tpt_p99 = rank(0.99);
-                double acc = 0;
-                for (double v : sorted) acc += v;
-                r.tpt_mean = acc / static_cast<double>(sorted.size());
+                r.tpt_p50 = fin[k][0];
+                r.tpt_p90 = fin[k][1];
+                r.tpt_p99 = fin[k][2];
+                r.tpt_mean = fin[k][3];
             }
             if (r.training_busy_time > 0)
                 r.training_throughput = static_cast<double>(r.trained_tokens) / r.training_busy_time;
@@ -441,6 +443,8 @@ std::string events_json(Context& ctx, const SimConfig& cfg) {
         a.push_back(r.arrival_time);
         p.push_back(static_cast<std::uint32_t>(r.prompt_tokens));
         o.push_back(static_cast<std::uint32_t>(r.output_tokens));
+        if (r.label_delay && !(*r.label_delay >= 0.0))
+            throw std::invalid_argument("colo-b200: negative or NaN label_delay is not supported");
         ld.push_back(r.label_delay ? *r.label_delay : -1.0);
         q.push_back(static_cast<std::uint64_t>(r.query_id));
     }

@@ -220,6 +220,12 @@ colo_status colo_ctx_release_scratch(colo_ctx* ctx) {
     return COLO_OK;
 }
 
+colo_status colo_ctx_share_temps(colo_ctx* ctx, colo_ctx* owner) {
+    if (!ctx || (owner && owner->device != ctx->device)) return COLO_EINVAL;
+    ctx->temps = (owner == ctx) ? nullptr : owner;
+    return COLO_OK;
+}
+
 colo_status colo_ctx_set_stream(colo_ctx* ctx, void* s) {
     if (!ctx) return COLO_EINVAL;
     ctx->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream

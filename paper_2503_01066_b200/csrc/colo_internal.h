@@ -42,9 +42,11 @@ struct colo_ctx {
     // serving replay: identity of the last full replay whose segment entry
     // states are still in d_rscratch (reuse_entries); any other d_rscratch
     // user clears rs_valid
-    uint64_t rs_sig[10] = {};
+    uint64_t rs_sig[11] = {};
     bool rs_valid = false;
     uint64_t launches = 0;          // kernels this context launched (colo_ctx_launches)
+    colo_ctx* temps = nullptr;      // colo_ctx_share_temps: the context whose per-call replay temporaries
+                                    // (d_sat, d_satpool, d_tmp of the first pass) this one uses
 };
 
 #define COLO_LAUNCHED(ctx) (++(ctx)->launches)

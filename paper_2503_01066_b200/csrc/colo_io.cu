@@ -335,6 +335,10 @@ int64_t colo_load_trace_jsonl(const char* path, double* arrival, uint32_t* promp
             return put_err(err, errlen, where + "output_tokens not an unsigned integer"), -2;
         if (ld && ld->kind != JVal::NUL && ld->kind != JVal::NUM)
             return put_err(err, errlen, where + "label_delay not a number"), -2;
+        // A present label delay is scheduled at arrival + delay (engine.hpp:389-408); this build keeps
+        // "no label" as a negative value, so a negative delay is refused rather than silently dropped.
+        if (ld && ld->kind == JVal::NUM && ld->num < 0.0)
+            return put_err(err, errlen, where + "negative label_delay is not supported by this build"), -2;
         recs.push_back(Rec{qid->u, at->num, pt->u, (ot && ot->kind == JVal::NUM) ? ot->u : 128ull,
                            (ld && ld->kind == JVal::NUM) ? ld->num : std::nan("")});
     }

@@ -81,6 +81,7 @@ struct SynthParams {
     double period;
     uint32_t ndev;
     uint64_t seed;
+    const uint32_t* dev_ids;  // NULL: keyed on the global query index; else on (fleet device id, local index)
     double* arrival;
     uint32_t* prompt;
     uint32_t* output;
@@ -107,7 +108,8 @@ __global__ void k_synth(const __grid_constant__ SynthParams P) {
     for (uint64_t j0 = lo; j0 < hi; j0 += 32) {
         const double rate = (P.period > 0.0 && (static_cast<uint64_t>(t / P.period) & 1ull)) ? rate_hi : rate_lo;
         uint64_t j = j0 + lane;
-        uint64_t h = mix64(P.seed ^ mix64(j * 2 + 1));
+        const uint64_t key = P.dev_ids ? ((static_cast<uint64_t>(P.dev_ids[d]) << 36) | (j - lo)) : j;
+        uint64_t h = mix64(P.seed ^ mix64(key * 2 + 1));
         double gap = -log(1.0 - u01(h)) / rate;
         double x = gap;
 #pragma unroll
@@ -285,6 +287,14 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
                              const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
                              double burst_period, size_t ndev, uint64_t seed, double* d_arrival, uint32_t* d_prompt,
                              uint32_t* d_output) {
+    return colo_synth_fleet_trace(ctx, h_bin_values, h_bin_probs, nbins, d_dev_offsets, d_dev_qps, d_dev_qps_hi,
+                                  burst_period, ndev, nullptr, seed, d_arrival, d_prompt, d_output);
+}
+
+colo_status colo_synth_fleet_trace(colo_ctx* ctx, const double* h_bin_values, const double* h_bin_probs, size_t nbins,
+                                   const uint64_t* d_dev_offsets, const double* d_dev_qps, const double* d_dev_qps_hi,
+                                   double burst_period, size_t ndev, const uint32_t* d_dev_ids, uint64_t seed,
+                                   double* d_arrival, uint32_t* d_prompt, uint32_t* d_output) {
     if (!ctx || !h_bin_values || !h_bin_probs || nbins == 0 || nbins > 32 || ndev == 0) return COLO_EINVAL;
     SynthParams P{};
     double acc = 0;
@@ -300,6 +310,7 @@ colo_status colo_synth_trace(colo_ctx* ctx, const double* h_bin_values, const do
     P.period = d_dev_qps_hi ? burst_period : 0.0;
     P.ndev = static_cast<uint32_t>(ndev);
     P.seed = seed;
+    P.dev_ids = d_dev_ids;
     P.arrival = d_arrival;
     P.prompt = d_prompt;
     P.output = d_output;

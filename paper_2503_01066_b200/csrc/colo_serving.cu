@@ -105,6 +105,8 @@ struct ReplayParams {
     uint8_t* labels;
     colo_batch* bstage;       // batch record staged at its first query's global index
     uint8_t* bflag;
+    uint64_t* vstage;         // compact stage for d_verdicts: (n << 32) | max_incoming at the first query, 0 elsewhere
+    uint32_t* verdicts;
     colo_batch* batches;
     colo_device_summary* summary;
     uint64_t* hist;
@@ -341,6 +343,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         b.verdict = 0;
                         P.bstage[lo + q] = b;
                         P.bflag[lo + q] = 1;
+                    }
+                    if (P.vstage) {
+                        const uint64_t inc = static_cast<uint64_t>(pq) + oq;
+                        P.vstage[lo + q] = (1ull << 32) | (inc < 0xffffffffull ? inc : 0xffffffffull);
                     }
                 }
                 A.max_need = max(A.max_need, warp_max_u64(need));
@@ -738,6 +744,8 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 P.bstage[lo + head] = b;
                 P.bflag[lo + head] = 1;
             }
+            if (lane == 0 && P.vstage)
+                P.vstage[lo + head] = (static_cast<uint64_t>(nb) << 32) | (max_inc < 0xffffffffull ? max_inc : 0xffffffffull);
             A.max_need = max(A.max_need, need_total);
             A.maxb = max(A.maxb, nb);
             ++A.nbatch;
@@ -1239,6 +1247,100 @@ __global__ void __launch_bounds__(kWarps * 32) k_batches(const __grid_constant__
     }
 }
 
+// The same verdicts from the compact 8 B stage (d_verdicts without batch
+// records), segment-parallel.  The slot a batch sees is the charged tokens of
+// the device's last single-query batch before it, and its output position is
+// the number of batches before it: both are scans over the device's queries.
+// k_vseg_count: per replay segment (one warp), its batch count and its last
+// single-query batch's charged tokens (+1; 0 = none).  k_vseg_scan: per
+// device (one warp), exclusive scans of both over its segments.
+// k_vseg_emit: per segment, the verdicts from the scanned entry state.
+struct VSeg {
+    uint64_t count, last;
+};
+
+__device__ __forceinline__ uint64_t single_charged(const ReplayParams& P, uint64_t g, uint32_t pi) {
+    return charged_tokens(P.p[g], P.o[g], P.sets[pi].cpa);
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_vseg_count(const __grid_constant__ ReplayParams P, VSeg* vs) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const uint64_t lo = P.dev_off[sg.dev];
+    const uint32_t pi = P.dev_prof[sg.dev];
+    uint64_t cnt = 0, last = 0;
+    for (uint64_t j0 = sg.start; j0 < sg.end; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        const uint64_t x = j < sg.end ? P.vstage[lo + j] : 0ull;
+        const bool f = x != 0;
+        cnt += __popc(__ballot_sync(FULL, f));
+        const bool single = f && (x >> 32) == 1;
+        const uint32_t sm = __ballot_sync(FULL, single);
+        if (sm) {
+            const uint32_t src = 31 - __clz(sm);
+            const uint64_t ch = (lane == src) ? single_charged(P, lo + j, pi) : 0ull;
+            last = __shfl_sync(FULL, ch, src) + 1;
+        }
+    }
+    if (lane == 0) vs[w] = VSeg{cnt, last};
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_vseg_scan(const __grid_constant__ ReplayParams P, VSeg* vs) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t d = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (d >= P.ndev) return;
+    uint64_t pos = 0, slot = 0;  // the device's slot starts empty (0 charged tokens)
+    for (uint32_t s0 = P.dev_seg[d]; s0 < P.dev_seg[d + 1]; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const bool in = s < P.dev_seg[d + 1];
+        const VSeg v = in ? vs[s] : VSeg{0, 0};
+        uint64_t incl = v.count;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t m = __ballot_sync(FULL, v.last != 0);
+        const uint32_t below = m & ((1u << lane) - 1u);
+        const uint64_t from = __shfl_sync(FULL, v.last, below ? 31 - __clz(below) : 0);
+        if (in) vs[s] = VSeg{pos + incl - v.count, below ? from - 1 : slot};
+        pos += __shfl_sync(FULL, incl, 31);
+        if (m) slot = __shfl_sync(FULL, v.last, 31 - __clz(m)) - 1;
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_vseg_emit(const __grid_constant__ ReplayParams P, const VSeg* vs) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t w = blockIdx.x * kWarps + (threadIdx.x >> 5);
+    if (w >= P.nsegs) return;
+    const Seg sg = P.segs[w];
+    const uint64_t lo = P.dev_off[sg.dev];
+    const uint32_t pi = P.dev_prof[sg.dev];
+    const MapView& mv = P.sets[pi];
+    uint64_t pos = vs[w].count, slot = vs[w].last;
+    for (uint64_t j0 = sg.start; j0 < sg.end; j0 += 32) {
+        const uint64_t j = j0 + lane;
+        const uint64_t x = j < sg.end ? P.vstage[lo + j] : 0ull;
+        const bool f = x != 0;
+        const uint32_t bal = __ballot_sync(FULL, f);
+        if (!bal) continue;
+        const uint32_t nb = static_cast<uint32_t>(x >> 32);
+        const uint64_t ch = f ? charged_tokens(P.p[lo + j], P.o[lo + j], mv.cpa) : 0ull;
+        const uint32_t sm = __ballot_sync(FULL, f && nb == 1);
+        const uint32_t below = sm & ((1u << lane) - 1u);
+        const uint64_t from = __shfl_sync(FULL, ch, below ? 31 - __clz(below) : 0);
+        if (f) {
+            const uint64_t my_slot = below ? from : slot;
+            P.verdicts[lo + pos + __popc(bal & ((1u << lane) - 1u))] =
+                compose(mv, mv.off, mv.hed, my_slot, static_cast<uint32_t>(x), nb, 0, mv.L) | stream_bits(mv, mv.off, ch);
+        }
+        if (sm) slot = __shfl_sync(FULL, ch, 31 - __clz(sm));
+        pos += __popc(bal);
+    }
+}
+
 // Grow-only context buffers (allocating tens of GB per call costs more than
 // the passes themselves).
 colo_status grow_buf(colo_ctx* ctx, void** buf, size_t* have, size_t bytes) {
@@ -1272,6 +1374,7 @@ constexpr uint64_t kPSeg = 131072;  // queries per partition segment
 colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64_t>& off, SatBuffers& sb,
                         cudaStream_t st) {
     P.sat_on = 0;
+    colo_ctx* sc = ctx->temps ? ctx->temps : ctx;  // owner of the per-call temporaries (colo_ctx_share_temps)
     const size_t ndev = P.ndev, n = off[ndev];
     const char* env = std::getenv("COLO_SAT");
     if ((env && env[0] == '0') || n >= (1ull << 32) || n == 0) return COLO_OK;
@@ -1293,16 +1396,16 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         if (nsat * 50 < P.nsegs || nsat < 2) return COLO_OK;
     }
     const size_t need_rec = n * 24 + ns * 64 + 512;
-    if (ctx->sat_bytes < need_rec) {
+    if (sc->sat_bytes < need_rec) {
         size_t freeb = 0, totb = 0;
         COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
-        if (need_rec + (4ull << 30) > freeb + ctx->sat_bytes) return COLO_OK;  // no room: replay every batch
+        if (need_rec + (4ull << 30) > freeb + sc->sat_bytes) return COLO_OK;  // no room: replay every batch
     }
     {
-        const colo_status g = grow_buf(ctx, &ctx->d_sat, &ctx->sat_bytes, need_rec);
+        const colo_status g = grow_buf(ctx, &sc->d_sat, &sc->sat_bytes, need_rec);
         if (g != COLO_OK) return g;
     }
-    auto* bp = static_cast<uint8_t*>(ctx->d_sat);
+    auto* bp = static_cast<uint8_t*>(sc->d_sat);
     P.sat_doff = reinterpret_cast<uint64_t*>(bp);
     P.sat_pre = reinterpret_cast<double*>(bp + n * 8);
     P.sat_end = reinterpret_cast<uint32_t*>(bp + n * 16);
@@ -1333,26 +1436,26 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
     size_t tb = 0;
     COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
     {
-        const colo_status gs = grow_buf(ctx, &ctx->d_tmp, &ctx->tmp_bytes, tb + 16);
+        const colo_status gs = grow_buf(ctx, &sc->d_tmp, &sc->tmp_bytes, tb + 16);
         if (gs != COLO_OK) return gs;
     }
     uint64_t last_in = 0, last_base = 0;
     COLO_CK(ctx, cudaMemcpyAsync(&last_in, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
-    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
+    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(sc->d_tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
     COLO_CK(ctx, cudaMemcpyAsync(&last_base, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
     COLO_CK(ctx, cudaStreamSynchronize(st));
     const uint64_t np = last_base + last_in;
-    if (ctx->satpool_bytes < np * 8 + 8) {
+    if (sc->satpool_bytes < np * 8 + 8) {
         size_t freeb = 0, totb = 0;
         COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
-        if (np * 8 + (2ull << 30) > freeb + ctx->satpool_bytes) return COLO_OK;  // no room for the step durations
+        if (np * 8 + (2ull << 30) > freeb + sc->satpool_bytes) return COLO_OK;  // no room for the step durations
     }
     if (timing) cudaEventRecord(ev[1], st);
     {
-        const colo_status g = grow_buf(ctx, &ctx->d_satpool, &ctx->satpool_bytes, np * 8 + 8);
+        const colo_status g = grow_buf(ctx, &sc->d_satpool, &sc->satpool_bytes, np * 8 + 8);
         if (g != COLO_OK) return g;
     }
-    P.sat_dk = static_cast<double*>(ctx->d_satpool);
+    P.sat_dk = static_cast<double*>(sc->d_satpool);
     COLO_LAUNCHED(ctx);
     k_sat_durations<<<blocks, kWarps * 32, 0, st>>>(P);
     COLO_CK(ctx, cudaGetLastError());
@@ -1384,28 +1487,33 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Cross-rank totals of the first stats pass (colo_serving_stats_nccl): sums
 // of the counters and of the exact 192-bit TPT sum, the latter as six 32-bit
-// chunks so no carry is lost in the u64 reduction; max of the peaks.
+// chunks so no carry is lost in the u64 reduction; max of the peaks; the
+// flag words OR-ed (NCCL has no bitwise reduction: each of the 8 flag bits is
+// summed as a count, and a bit is set when any rank had it).
+constexpr int kFlagBits = 8;
 colo_status dist_totals(colo_ctx* ctx, void* comm, colo_device_summary* t) {
-    uint64_t hs[12] = {t->generated_tokens, t->slow_tokens, t->slow_queries, t->batches};
+    constexpr int NS = 10 + kFlagBits;
+    uint64_t hs[NS] = {t->generated_tokens, t->slow_tokens, t->slow_queries, t->batches};
     for (int i = 0; i < 6; ++i) hs[4 + i] = (t->tpt_sum[i / 2] >> (32 * (i & 1))) & 0xffffffffull;
-    uint64_t hm[4] = {t->peak_device_bytes, t->max_batch_size, t->flags, 0};
+    for (int b = 0; b < kFlagBits; ++b) hs[10 + b] = (t->flags >> b) & 1ull;
+    uint64_t hm[2] = {t->peak_device_bytes, t->max_batch_size};
     double he = t->end_time;
     uint64_t* d = nullptr;
-    COLO_CK(ctx, cudaMalloc(&d, 17 * 8));
+    COLO_CK(ctx, cudaMalloc(&d, (NS + 3) * 8));
     colo_status st = COLO_OK;
     do {
-        if (cudaMemcpy(d, hs, 10 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(d + 10, hm, 4 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-            cudaMemcpy(d + 14, &he, 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+        if (cudaMemcpy(d, hs, NS * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(d + NS, hm, 2 * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(d + NS + 2, &he, 8, cudaMemcpyHostToDevice) != cudaSuccess) {
             st = set_err(ctx, COLO_ECUDA, "dist_totals staging");
             break;
         }
-        if ((st = colo_stats_allreduce(ctx, comm, d, 10)) != COLO_OK) break;
-        if ((st = nccl_allreduce_raw(ctx, comm, d + 10, 4, /*ncclUint64*/ 5, /*ncclMax*/ 2)) != COLO_OK) break;
-        if ((st = nccl_allreduce_raw(ctx, comm, d + 14, 1, /*ncclFloat64*/ 8, /*ncclMax*/ 2)) != COLO_OK) break;
-        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || cudaMemcpy(hs, d, 10 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(hm, d + 10, 4 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
-            cudaMemcpy(&he, d + 14, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        if ((st = colo_stats_allreduce(ctx, comm, d, NS)) != COLO_OK) break;
+        if ((st = nccl_allreduce_raw(ctx, comm, d + NS, 2, /*ncclUint64*/ 5, /*ncclMax*/ 2)) != COLO_OK) break;
+        if ((st = nccl_allreduce_raw(ctx, comm, d + NS + 2, 1, /*ncclFloat64*/ 8, /*ncclMax*/ 2)) != COLO_OK) break;
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess || cudaMemcpy(hs, d, NS * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(hm, d + NS, 2 * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(&he, d + NS + 2, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
             st = set_err(ctx, COLO_ECUDA, "dist_totals readback");
             break;
         }
@@ -1427,7 +1535,10 @@ colo_status dist_totals(colo_ctx* ctx, void* comm, colo_device_summary* t) {
         t->tpt_sum[2] = acc[2];
         t->peak_device_bytes = hm[0];
         t->max_batch_size = hm[1];
-        t->flags = hm[2];
+        uint64_t fl = t->flags & ~((1ull << kFlagBits) - 1);
+        for (int b = 0; b < kFlagBits; ++b)
+            if (hs[10 + b]) fl |= 1ull << b;
+        t->flags = fl;
         t->end_time = he;
     } while (false);
     cudaFree(d);
@@ -1509,10 +1620,23 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     bytes += want_batches ? align256(n * sizeof(colo_batch) + 8) : 0;
     const size_t o_bflag = bytes;
     bytes += want_batches ? align256(n + 8) : 0;
-    const uint64_t sig[10] = {n, ndev, seg, nprofiles, reinterpret_cast<uintptr_t>(d_arrival),
+    const bool want_verdicts = opts->d_verdicts != nullptr;
+    if (want_verdicts && !opts->sets) return set_err(ctx, COLO_EINVAL, "d_verdicts needs map sets");
+    const size_t o_vstage = bytes;
+    bytes += want_verdicts ? align256(n * 8 + 8) : 0;
+    const size_t o_vseg = bytes;
+    bytes += want_verdicts ? align256(ns * sizeof(VSeg) + 8) : 0;
+    uint64_t prof_hash = 14695981039346656037ull;  // FNV-1a over the profile structs' bytes
+    for (size_t i = 0; i < nprofiles; ++i) {
+        const auto* mb = reinterpret_cast<const uint8_t*>(&models[i]);
+        const auto* gb = reinterpret_cast<const uint8_t*>(&gpus[i]);
+        for (size_t b = 0; b < sizeof(colo_model); ++b) prof_hash = (prof_hash ^ mb[b]) * 1099511628211ull;
+        for (size_t b = 0; b < sizeof(colo_gpu); ++b) prof_hash = (prof_hash ^ gb[b]) * 1099511628211ull;
+    }
+    const uint64_t sig[11] = {n, ndev, seg, nprofiles, reinterpret_cast<uintptr_t>(d_arrival),
                               reinterpret_cast<uintptr_t>(d_prompt), reinterpret_cast<uintptr_t>(d_output),
                               reinterpret_cast<uintptr_t>(d_dev_offsets), reinterpret_cast<uintptr_t>(d_dev_profile),
-                              ns};
+                              ns, prof_hash};
     const bool reuse = opts->reuse_entries && ctx->rs_valid && ctx->rscratch_bytes >= bytes &&
                        std::memcmp(sig, ctx->rs_sig, sizeof sig) == 0;
     if (!reuse) ctx->rs_valid = false;
@@ -1532,6 +1656,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         P.bstage = reinterpret_cast<colo_batch*>(base + o_bstage);
         P.bflag = base + o_bflag;
         COLO_CK(ctx, cudaMemsetAsync(P.bflag, 0, n + 8, ctx->stream));
+    }
+    if (want_verdicts) {
+        P.vstage = reinterpret_cast<uint64_t*>(base + o_vstage);
+        P.verdicts = opts->d_verdicts;
+        COLO_CK(ctx, cudaMemsetAsync(P.vstage, 0, n * 8 + 8, ctx->stream));
     }
     P.nprof = static_cast<uint32_t>(nprofiles);
     P.has_sets = opts->sets ? 1u : 0u;
@@ -1579,7 +1708,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             COLO_LAUNCHED(ctx);
             k_seg_scan<<<static_cast<uint32_t>((ndev + 127) / 128), 128, 0, ctx->stream>>>(P);
         }
-        if (opts->stats_mode == 2 && ctx->bmeta_valid && P.hist) {  // narrowing pass: only batches that can hit a filter bin
+        if (opts->stats_mode == 2 && ctx->bmeta_valid && P.hist && !P.vstage && !P.bstage) {  // narrowing pass: only batches that can hit a filter bin
             P.sparse_start = static_cast<const double*>(ctx->d_bmeta);
             P.sparse_bins = reinterpret_cast<const uint64_t*>(static_cast<const double*>(ctx->d_bmeta) + n);
             COLO_CK(ctx, cudaFuncSetAttribute(k_sparse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
@@ -1671,6 +1800,15 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     if (want_batches && ns) {
         COLO_LAUNCHED(ctx);
         k_batches<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P);
+    }
+    if (want_verdicts && ns) {
+        VSeg* vs = reinterpret_cast<VSeg*>(base + o_vseg);
+        COLO_LAUNCHED(ctx);
+        k_vseg_count<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P, vs);
+        COLO_LAUNCHED(ctx);
+        k_vseg_scan<<<dev_blocks, kWarps * 32, 0, ctx->stream>>>(P, vs);
+        COLO_LAUNCHED(ctx);
+        k_vseg_emit<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P, vs);
     }
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));

@@ -300,38 +300,61 @@ class Run:
 
 
 def finalize_report(r: dict) -> dict:
-    """metrics.hpp:56-69: nearest-rank percentiles and the mean as the sequential
-    sum of the ascending-sorted samples (the sort runs on the GPU when a
-    context is given via r['_sorted'])."""
-    s = r.get("_sorted_for_cdf")
+    """metrics.hpp:56-69 on a report whose samples were finalized on the device:
+    r['_finalized'] = [p50, p90, p99, mean] from colo_finalize (nearest ranks of
+    the ascending sort and the strictly sequential sum of the sorted samples,
+    bit-exact).  There is no host path: a report with samples and no device
+    result is an error."""
     x = r["tpt_samples"]
     for k in ("tpt_p50", "tpt_p90", "tpt_p99", "tpt_mean"):
         r[k] = None
     fin = r.pop("_finalized", None)
-    if len(x) and fin is not None:  # computed on the device by colo_finalize (same bits)
+    if len(x):
+        if fin is None:
+            raise cs.ColoError(_lib.COLO_EINVAL, "finalize_report: samples were not finalized on the device")
         r["tpt_p50"], r["tpt_p90"], r["tpt_p99"], r["tpt_mean"] = fin
-    elif len(x):
-        srt = s if s is not None else np.sort(x)
-        n = len(srt)
-
-        def rank(q):
-            k = math.ceil(q * float(n))
-            return float(srt[(1 if k == 0 else k) - 1])
-
-        r["tpt_p50"], r["tpt_p90"], r["tpt_p99"] = rank(0.50), rank(0.90), rank(0.99)
-        r["tpt_mean"] = float(np.cumsum(srt)[-1]) / float(n)  # add.accumulate: strictly sequential
     r["training_throughput"] = (float(r["trained_tokens"]) / r["training_busy_time"]
                                 if r["training_busy_time"] > 0 else None)
     return r
 
 
-def run_simulations(ctx: cs.Context, runs: Sequence[Run], sort_on_gpu: bool = True) -> List[dict]:
+def _runs_with_own_maps(ctx: cs.Context, runs: Sequence[Run]) -> List[Run]:
+    """Each device runs with its map set's model, GPU profile and mode, so the
+    set must be the run's own (SimConfig::validate, engine.hpp:60-68).
+    Colocated runs: the maps must carry profile_hash(model, gpu) and the run's
+    training mode, else ColoValidationError with the reference's message.  The
+    other modes never consult the maps: they get a set built from the run's own
+    (model, gpu, training), as the C++ drop-in's mapset_of does."""
+    own, built = [], {}
+    for r in runs:
+        cs.validate_profile_pair(r.model, r.gpu)
+        h = cs.profile_hash(r.model, r.gpu)
+        if int(r.mode) == int(cs.SimMode.COLOCATED):
+            if r.maps.profile_hash_value != h:
+                raise ColoValidationError(_lib.COLO_EVALIDATION, "sim config: map profile hash does not match the profiles")
+            if int(r.maps.mode) != int(r.training):
+                raise ColoValidationError(_lib.COLO_EVALIDATION, "sim config: map training mode does not match sim.training")
+            own.append(r)
+            continue
+        if r.maps.profile_hash_value == h and int(r.maps.mode) == int(r.training):
+            own.append(r)
+            continue
+        key = (h, int(r.training))
+        if key not in built:
+            built[key] = cs.MapSet.build(ctx, r.model, r.gpu, mode=cs.TrainingMode(int(r.training)))
+        own.append(Run(r.model, r.gpu, r.mode, r.training, built[key], r.trace, r.cache_timeout))
+    return own
+
+
+def run_simulations(ctx: cs.Context, runs: Sequence[Run], keep_sorted: bool = True) -> List[dict]:
     """Simulation::run for every run (engine.hpp:938-941), as GPU fleets: one
     launch per cache timeout and <= 16 map sets.  Returns MetricsReport dicts
-    (metrics.hpp:17-44 field names, finalized)."""
+    (metrics.hpp:17-44 field names), finalized on the device (colo_finalize);
+    keep_sorted also returns each run's sorted samples for export_tpt_cdf."""
     import torch
 
     out: List[Optional[dict]] = [None] * len(runs)
+    runs = _runs_with_own_maps(ctx, runs)
     todo = list(range(len(runs)))
     while todo:
         to = runs[todo[0]].cache_timeout
@@ -370,14 +393,15 @@ def run_simulations(ctx: cs.Context, runs: Sequence[Run], sort_on_gpu: bool = Tr
         smp_dev = res["samples"]
         srt_dev = None
         fin = {}
-        if sort_on_gpu and smp_dev.numel():
-            srt_dev = torch.empty_like(smp_dev)
+        if smp_dev.numel():
+            srt_dev = torch.empty_like(smp_dev) if keep_sorted else None
             # per run: finalize its own sample range on the device (colo_finalize: sort,
             # nearest ranks, the sequential sum of the sorted samples)
             for k in range(len(batch)):
                 lo_, hi_ = int(so[k]), int(so[k + 1])
                 if hi_ > lo_:
-                    fin[k] = cs.finalize(ctx, smp_dev[lo_:hi_], sorted_out=srt_dev[lo_:hi_])
+                    fin[k] = cs.finalize(ctx, smp_dev[lo_:hi_],
+                                         sorted_out=srt_dev[lo_:hi_] if srt_dev is not None else None)
         smp = smp_dev.cpu().numpy()
         srt = srt_dev.cpu().numpy() if srt_dev is not None else None
         for k, i in enumerate(batch):
@@ -410,11 +434,44 @@ class GpuEngine:
     def build_maps(self, model, gpu, steps, bounds, mode):
         return cs.MapSet.build(self.ctx, model, gpu, steps, bounds, mode)
 
-    def load_maps(self, model, gpu, offload_path, hedge_path):
-        return cs.load_mapset(self.ctx, model, gpu, offload_path, hedge_path)
+    def load_maps(self, model, gpu, offload_path, hedge_path, steps=None, bounds=None, mode=None):
+        """OffloadingMap::load / HedgingMap::load of the given files; a map whose file
+        is None is built from (steps, bounds, mode) as load_config does (the hedge
+        grid on the offload grid's cached axis, assumed output 128)."""
+        if offload_path and hedge_path:
+            return cs.load_mapset(self.ctx, model, gpu, offload_path, hedge_path)
+        h = cs.profile_hash(model, gpu)
+        built = cs.MapSet.build(self.ctx, model, gpu, steps, bounds, mode)
+        b_off, b_hed = built.cells()
+        if offload_path:
+            ho, off = cs.load_map_cells(offload_path, h)
+            o_steps, o_bounds, o_mode = ho["steps"], ho["bounds"], ho["mode"]
+            hs, hm, assumed, hed = steps.cached_token_step, bounds.max_cached_tokens, 128, b_hed
+        else:
+            hh, hed = cs.load_map_cells(hedge_path, h)
+            o_steps, o_bounds, o_mode, off = steps, bounds, mode, b_off
+            hs, hm, assumed = hh["steps"].cached_token_step, hh["bounds"].max_cached_tokens, hh["assumed_output_tokens"]
+            if hh["mode"] != mode:
+                o_mode = hh["mode"]
+        built.close()
+        if o_mode != mode:  # one map set carries one mode (engine.hpp:66-67 refuses the mix in Colocated runs)
+            raise ColoValidationError(_lib.COLO_EVALIDATION, "sim config: map training mode does not match sim.training")
+        return cs.MapSet.from_cells(self.ctx, model, gpu, o_steps, o_bounds, o_mode, hs, hm, assumed, h, off, hed)
 
-    def run(self, runs: Sequence[Run], sort_on_gpu: bool = True) -> List[dict]:
-        return run_simulations(self.ctx, runs, sort_on_gpu)
+    def run(self, runs: Sequence[Run], keep_sorted: bool = True) -> List[dict]:
+        return run_simulations(self.ctx, runs, keep_sorted)
+
+    def sort(self, samples) -> np.ndarray:
+        """Ascending sort of f64 samples on the device (colo_sort_f64)."""
+        import torch
+
+        x = np.ascontiguousarray(samples, np.float64)
+        if not len(x):
+            return x
+        d = torch.from_numpy(x).to(torch.device("cuda", self.ctx.device))
+        o = torch.empty_like(d)
+        _lib.check(lib().colo_sort_f64(self.ctx.h, cs._ptr(d), cs._ptr(o), len(x)), self.ctx.h, "sort")
+        return o.cpu().numpy()
 
     def events(self, run: Run) -> str:
         """The run's event log (colo_colocated_events)."""
@@ -461,14 +518,14 @@ def max_trainable_tokens(engine, m, g, training, maps, mode, hi_prompt: int) -> 
     eng = _engine(engine)
     ok = {}
     try:
-        reps = eng.run(runs, sort_on_gpu=False)
+        reps = eng.run(runs, keep_sorted=False)
         for t, r in zip(lengths, reps):
             ok[t] = r["completed_jobs"] == 1 and not r["oom_flag"]
     except (cs.ColoBreachError, ColoValidationError):
         # any exception is `false` (the reference catches std::exception): one run each
         for t, run in zip(lengths, runs):
             try:
-                r = eng.run([run], sort_on_gpu=False)[0]
+                r = eng.run([run], keep_sorted=False)[0]
                 ok[t] = r["completed_jobs"] == 1 and not r["oom_flag"]
             except (cs.ColoBreachError, ColoValidationError):
                 ok[t] = False
@@ -600,10 +657,12 @@ def import_jsonl(path: str) -> dict:
 
 
 def export_tpt_cdf(r: dict, path: str) -> None:
-    """metrics.hpp:280-288 (sorted samples from the GPU sort when available)."""
+    """metrics.hpp:280-288 (the samples sorted on the device by colo_finalize)."""
     srt = r.get("_sorted_for_cdf")
     if srt is None:
-        srt = np.sort(np.asarray(r["tpt_samples"], np.float64))
+        if len(r["tpt_samples"]):
+            raise cs.ColoError(_lib.COLO_EINVAL, "export_tpt_cdf: run the report with keep_sorted=True")
+        srt = np.zeros(0)
     n = len(srt)
     with open(path, "w") as f:
         f.write("tpt_seconds,cumulative_fraction\n")
@@ -632,9 +691,10 @@ def load_config(engine, path, offload_map_path="", hedge_map_path=""):
     eng = _engine(engine)
     ec = ExperimentConfig.from_file(_resolve(path))
     if offload_map_path or hedge_map_path:
-        if not (offload_map_path and hedge_map_path):
-            raise ColoValidationError(_lib.COLO_EVALIDATION, "this build loads map files as a pair")
-        maps = eng.load_maps(ec.model, ec.gpu, _resolve(offload_map_path), _resolve(hedge_map_path))
+        # whichever file is given is loaded; the other map is built from the config (colosim.cpp:58-67)
+        maps = eng.load_maps(ec.model, ec.gpu, _resolve(offload_map_path) if offload_map_path else None,
+                             _resolve(hedge_map_path) if hedge_map_path else None,
+                             steps=ec.map_steps, bounds=ec.map_bounds, mode=ec.training)
     else:
         maps = eng.build_maps(ec.model, ec.gpu, ec.map_steps, ec.map_bounds, ec.training)
     return ec, maps
@@ -667,9 +727,11 @@ def cmd_run(engine, config_path, out_dir, trace_path="", offload_map_path="", he
     return rep
 
 
-def cmd_plotdata(report_path, out_dir, force=False):
-    """tools/colosim.cpp:254-260."""
+def cmd_plotdata(report_path, out_dir, force=False, engine=None):
+    """tools/colosim.cpp:254-260 (the samples sorted by the engine: on the GPU, colo_sort_f64)."""
     r = import_jsonl(_resolve(report_path))
+    eng = _engine(engine if engine is not None else cs.Context(0))
+    r["_sorted_for_cdf"] = eng.sort(r["tpt_samples"])
     os.makedirs(out_dir, exist_ok=True)
     export_tpt_cdf(r, _out_file(out_dir, "tpt_cdf.csv", force))
 
@@ -694,7 +756,7 @@ def cmd_compare(engine, config_path, out_dir, force=False) -> None:
                 for sm in (cs.SimMode.COLOCATED, cs.SimMode.SEPARATE_CLUSTER):
                     runs.append(Run(ec.model, ec.gpu, sm, mode, mapsets[int(mode)], trace, ec.cache_timeout))
                 keys.append((mode, tokens))
-        reps = eng.run(runs, sort_on_gpu=False)
+        reps = eng.run(runs, keep_sorted=False)
         for k, (mode, tokens) in enumerate(keys):
             colo, base = reps[2 * k], reps[2 * k + 1]
             ct, bt = colo["training_throughput"], base["training_throughput"]

@@ -25,7 +25,10 @@ class OracleEngine:
         return (model, gpu, Grid(steps.cached_token_step, steps.incoming_token_step, steps.batch_step,
                                  bounds.max_cached_tokens, bounds.max_incoming_tokens, bounds.max_batch), int(mode))
 
-    def run(self, runs, sort_on_gpu=True):
+    def sort(self, samples):
+        return np.sort(np.asarray(samples, np.float64))
+
+    def run(self, runs, keep_sorted=True):
         out = []
         for r in runs:
             model, gpu, grid, cpa = r.maps
@@ -47,6 +50,9 @@ class OracleEngine:
             rep["tpt_samples"] = res["samples"].copy()
             rep["trace_hash"] = t.content_hash()
             rep["mode_tag"] = f"{ex._sm_str(r.mode)}/{ex._tm_str(r.training)}"
+            if len(rep["tpt_samples"]):  # what the GPU engine gets from colo_finalize, here from the oracle
+                rep["_finalized"] = list(self.orc.finalize(rep["tpt_samples"]))
+                rep["_sorted_for_cdf"] = np.sort(rep["tpt_samples"])
             out.append(ex.finalize_report(rep))
         return out
 
@@ -94,7 +100,7 @@ def test_plotdata_roundtrip(tmp_path):
         ex.cmd_run(OracleEngine(), "small.config", str(tmp_path / "r"))
     finally:
         os.chdir(cwd)
-    ex.cmd_plotdata(str(tmp_path / "r" / "report.jsonl"), str(tmp_path / "p"))
+    ex.cmd_plotdata(str(tmp_path / "r" / "report.jsonl"), str(tmp_path / "p"), engine=OracleEngine())
     assert open(tmp_path / "p" / "tpt_cdf.csv").read() == open(tmp_path / "r" / "tpt_cdf.csv").read()
     r = ex.import_jsonl(str(tmp_path / "r" / "report.jsonl"))
     assert r["mode_tag"] == "colocated/cpa" and len(r["tpt_samples"]) == r["generated_tokens"]

@@ -85,8 +85,9 @@ def test_pack_tuples_layout():
     assert list(a["cached"]) == [1, 2] and list(a["charged"]) == [5, 6]
 
 
-def numpy_pass(samples_list):
-    """A stats pass computed from explicit samples (what the replay kernel accumulates)."""
+def numpy_pass(samples_list, flags=0):
+    """A stats pass computed from explicit samples (what the replay kernel accumulates);
+    ``flags`` is the pass's summary flag word (bit 0: a sample the exact sum could not hold)."""
     bits = np.concatenate(samples_list).view(np.uint64) if samples_list else np.zeros(0, np.uint64)
     samples = bits.view(np.float64)
 
@@ -98,7 +99,7 @@ def numpy_pass(samples_list):
             h[f * cs.HIST_BINS:(f + 1) * cs.HIST_BINS] += torch.from_numpy(np.bincount(keys, minlength=cs.HIST_BINS))
         tot = None
         if fs == 63:
-            tot = {"generated_tokens": len(samples), "slow_tokens": 0, "slow_queries": 0, "batches": 0, "flags": 0,
+            tot = {"generated_tokens": len(samples), "slow_tokens": 0, "slow_queries": 0, "batches": 0, "flags": flags,
                    "exact_sum": sum(int(x) for x in (samples * 2.0**96))}
         return h, tot
 

@@ -45,6 +45,9 @@ def _worker(rank, world, port, outq):
     mine = [t for d, t in enumerate(_traces()) if d % world == rank]
     samples = [orc.replay_serving(default_model(), default_gpu(), *t)["samples"] for t in mine]
     out = cs.stats_protocol(numpy_pass(samples), reduce=lambda t: dist.all_reduce(t))
+    # flags are OR-ed across ranks: only rank 1 saw a sample outside the exact sum's range
+    flagged = cs.stats_protocol(numpy_pass(samples, flags=1 if rank == 1 else 0), reduce=lambda t: dist.all_reduce(t))
+    out["or_flags"], out["or_mean_exact"] = flagged["flags"], flagged["mean_exact"]
     outq.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
@@ -73,3 +76,5 @@ def test_two_rank_stats_reduce():
         assert o["generated_tokens"] == len(alls)
         assert (o["p50"], o["p90"], o["p99"]) == (p50, p90, p99)
         assert abs(o["mean"] - mean) <= 1e-12 * mean
+        assert o["flags"] == 0 and o["mean_exact"]
+        assert o["or_flags"] & 1 and not o["or_mean_exact"]
