@@ -170,18 +170,18 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
 constexpr uint32_t kTile = 1024;  // tuples per bulk copy (16 KB)
 constexpr uint32_t kStages = 4;
 
-template <bool COUNT, bool FAST>
+template <bool COUNT, bool FAST, uint32_t STAGES>
 __global__ void __launch_bounds__(kThreads) k_decide_tma(const __grid_constant__ DecideParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     const MapView mv = P.mv;
     uint4* tiles = reinterpret_cast<uint4*>(sm);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kStages * kTile * 16);
-    uint8_t* off = sm + kStages * kTile * 16 + 64;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + STAGES * kTile * 16);
+    uint8_t* off = sm + STAGES * kTile * 16 + 64;
     const uint32_t ob = (mv.off_bytes + 15u) & ~15u;
     uint8_t* hed = off + ob;
     const uint64_t ntiles = (P.n + kTile - 1) / kTile;
     if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        for (uint32_t s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     for (uint32_t i = threadIdx.x; i < mv.off_bytes; i += blockDim.x) off[i] = mv.off[i];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) k_decide_tma(const __grid_constant__
         bulk_g2s(tiles + s * kTile, P.in + t * kTile, bytes, &bars[s]);
     };
     if (threadIdx.x == 0)
-        for (uint32_t s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < STAGES; ++s) {
             const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
             if (t < ntiles) issue(s, t);
         }
@@ -206,8 +206,8 @@ __global__ void __launch_bounds__(kThreads) k_decide_tma(const __grid_constant__
     uint32_t cnt[COLO_NCOUNTERS] = {};
     uint32_t it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const uint32_t s = it % kStages;
-        mbar_wait(&bars[s], (it / kStages) & 1u);
+        const uint32_t s = it % STAGES;
+        mbar_wait(&bars[s], (it / STAGES) & 1u);
         const uint64_t base = t * kTile;
         const uint64_t rest = P.n - base;
         const uint32_t len = static_cast<uint32_t>(rest < kTile ? rest : kTile);
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) k_decide_tma(const __grid_constant__
         }
         __syncthreads();  // stage s consumed by every thread
         if (threadIdx.x == 0) {
-            const uint64_t nt = t + static_cast<uint64_t>(kStages) * gridDim.x;
+            const uint64_t nt = t + static_cast<uint64_t>(STAGES) * gridDim.x;
             if (nt < ntiles) issue(s, nt);
         }
     }
@@ -244,52 +244,183 @@ struct ExactParams {
     uint32_t* out;
     uint64_t n;
     uint64_t* counters;
+    // launch constants of offload_cell_decision (maps.hpp:215-231), all mod 2^64
+    // like the reference's own products: acts + kv = cached * (L*abpt + kvbpt[CPA])
+    uint64_t ak;       // L * abpt (+ kvbpt in CPA)
+    uint64_t abpt, kvbpt;
+    uint32_t L;
+    uint32_t wf_mode;  // 1: workspace_factor == 1.0 (need = 2 kv below 2^53), 0: generic llround
+    const uint16_t* tab;  // kExactTab entries: bits 0-7 hedge threshold, bit 8 stream bit (k_exact_tab)
 };
 
-// Exact per-query verdicts: offload_cell_decision (maps.hpp:215-231) at the
-// raw point + the hedge inequality (maps.hpp:341-356, 380) evaluated directly.
+// Per-value tables for the exact path, indexed by a 16-bit token count c.
+//  - bits 0-7: the hedge threshold.  For a fixed cached value the residual
+//    load time is non-decreasing in the freed-layer count f (bytes grow with
+//    f, the credit shrinks, and every rounding step is monotone), so
+//    recompute(c, f) = residual(c, f) > recompute_time(c) (maps.hpp:341-356,
+//    380) holds exactly for f >= thr[c].  The entry is found by evaluating the
+//    same inequality at every f in [0, L]; an entry whose bits are not of that
+//    shape (u64 wrap in the byte product) is 0xff and the kernel evaluates the
+//    inequality directly.  L + 1 = never.
+//  - bit 8: offload_cell_decision(c, 1, 1) == AllToHost, the stream flag of a
+//    query charged c tokens (engine.hpp:437-444).
+constexpr uint32_t kExactTab = 65536;
+
+__global__ void k_exact_tab(const __grid_constant__ colo_model m, const __grid_constant__ colo_gpu g, uint32_t cpa,
+                            uint64_t assumed, uint64_t budget, uint16_t* __restrict__ tab) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= kExactTab) return;
+    const uint32_t L = static_cast<uint32_t>(m.num_layers);
+    uint32_t t = 0xffu;
+    if (c != 0) {  // c == 0: HedgingMap nullopt, never read
+        const double rc = hedge_recompute_time(m, cpa != 0, c, assumed);
+        t = L + 1;
+        bool ok = true;
+        for (uint32_t f = 0; f <= L; ++f) {
+            const bool r = hedge_residual_load_time(m, g, c, f) > rc;
+            if (r && t == L + 1) t = f;
+            ok &= r == (t != L + 1);
+        }
+        if (!ok) t = 0xffu;
+    }
+    const uint32_t stream = offload_cell_code(m, budget, cpa != 0, c, 1, 1) == 1;
+    tab[c] = static_cast<uint16_t>(t | (stream << 8));
+}
+
+// offload_cell_decision (maps.hpp:215-231) at a raw point without the u64
+// divide and without data-dependent branches: every check of the reference,
+// in its order, on the same mod-2^64 products, evaluated for every lane and
+// selected at the end.  n = ceil(deficit / per_layer) > L is decided by the
+// exact 128-bit product L * per_layer; otherwise n <= L and
+// floor(deficit / per_layer) comes from an fp32 quotient estimate (relative
+// error < 2^-21, so within one of the floor for quotients <= 253) corrected
+// with exact u64 products.  Lanes where the reference's (deficit + per_layer
+// - 1) wraps or per_layer >= 2^56 take the reference's own expression.
+__device__ __forceinline__ uint32_t exact_code(const ExactParams& P, uint32_t cached, uint32_t incoming,
+                                               uint32_t batch) {
+    const uint64_t ak = static_cast<uint64_t>(cached) * P.ak;  // acts + kv (maps.hpp:54-61)
+    const uint64_t headroom = P.budget - ak;
+    const uint64_t kv = static_cast<uint64_t>(batch * static_cast<uint64_t>(incoming)) * P.kvbpt;  // cost_model.hpp:54-56
+    uint64_t need = kv + kv;  // serving_memory (cost_model.hpp:59-66): llround(1.0 * (double)kv) == kv below 2^53
+    if (P.wf_mode != 1 || kv >= (1ull << 53))
+        need = kv + static_cast<uint64_t>(llround(P.m.workspace_factor * static_cast<double>(kv)));
+    const uint64_t deficit = need - headroom;
+    const uint64_t per_layer = static_cast<uint64_t>(cached) * P.abpt;
+    const uint64_t sum = deficit + (per_layer - 1);
+    const uint64_t lp = per_layer * P.L;
+    const bool over = __umul64hi(per_layer, P.L) == 0 && deficit > lp;  // n > L
+    const float fq = __fmul_rz(__ull2float_rn(deficit), __frcp_rn(__ull2float_rn(per_layer)));
+    uint32_t q = static_cast<uint32_t>(fminf(fq, static_cast<float>(P.L + 1)));
+    uint64_t pr = q * per_layer;
+    const bool hi = pr > deficit;
+    const bool lo = !hi && deficit - pr >= per_layer;
+    q = hi ? q - 1 : (lo ? q + 1 : q);
+    pr = hi ? pr - per_layer : (lo ? pr + per_layer : pr);
+    uint64_t n = q + (pr != deficit);
+    const bool ref_div = sum < deficit || (per_layer >> 56) != 0;
+    const bool a2h = ak > P.budget;
+    const bool noact = need <= headroom;
+    if (ref_div && !a2h && !noact && per_layer != 0) n = sum / per_layer;  // maps.hpp:227, wrap-around included
+    else if (over) n = P.L + 1;
+    const uint32_t code = n > P.L ? 1u : 2u + static_cast<uint32_t>(n);
+    return a2h ? 1u : (noact ? 0u : (per_layer == 0 ? 1u : code));
+}
+
+// One exact verdict: exact_code, the hedge inequality through the threshold
+// table, the stream bit (engine.hpp:437-444).  thr / sbits: the per-value
+// tables of k_exact_tab staged in shared memory for values below kSmemTab.
+constexpr uint32_t kSmemTab = 16384;
+
+__device__ __forceinline__ uint32_t exact_verdict(const ExactParams& P, bool cpa, const uint4 t, const uint8_t* thr,
+                                                  const uint32_t* sbits) {
+    const uint32_t cached = t.x, incoming = t.y, charged = t.z;
+    const uint32_t batch = t.w & 0xffffu, pending = (t.w >> 16) & 0xffu, dev = t.w >> 24;
+    const uint32_t L = P.L;
+    const bool fallback = incoming == 0 || batch == 0;
+    const uint32_t code = fallback ? 1u : exact_code(P, cached, incoming, batch);
+    const bool a2h = code == 1;
+    const uint32_t layers = code >= 2 ? code - 2 : 0u;
+    const uint32_t free_now = a2h ? dev : min(layers, dev);
+    const uint32_t total = min(pending + (a2h ? L : layers), L);
+    const bool hoor = cached == 0;  // HedgingMap nullopt at c == 0 (maps.hpp:278)
+    uint32_t th = thr[min(cached, kSmemTab - 1)];
+    if (cached >= kSmemTab) th = cached < kExactTab ? (__ldg(P.tab + cached) & 0xffu) : 0xffu;
+    bool rec = total >= th;
+    if (th == 0xffu && !fallback && !hoor) {  // not of threshold shape: the inequality itself
+        const double rc = hedge_recompute_time(P.m, cpa, cached, P.assumed);
+        rec = hedge_residual_load_time(P.m, P.g, cached, total) > rc;
+    }
+    const uint32_t recompute = (fallback || hoor) ? 1u : static_cast<uint32_t>(rec);
+    const uint32_t v = (a2h ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS) | (layers << 2) | (free_now << 10) |
+                       (recompute << 18) | (fallback ? COLO_V_OFFLOAD_OOR : 0u) |
+                       ((!fallback && hoor) ? COLO_V_HEDGE_OOR : 0u) | ((COLO_VD_FREE_LOADBACK + recompute) << 21);
+    bool stream = (sbits[min(charged, kSmemTab - 1) >> 5] >> (charged & 31)) & 1u;
+    if (charged >= kSmemTab)
+        stream = charged < kExactTab ? (__ldg(P.tab + charged) >> 8) != 0 : exact_code(P, charged, 1, 1) == 1;
+    return (code == 0 ? 0u : v) | (stream ? COLO_V_STREAM : 0u);
+}
+
+// Exact per-query verdicts through a TMA tuple pipeline like k_decide_tma's
+// (kExactStages 16-KB tiles in flight per CTA, one elected thread
+// refilling), with the per-value tables in shared memory so the gathers stay
+// out of L1.
+constexpr uint32_t kExactStages = 2;
+
 template <bool COUNT>
 __global__ void __launch_bounds__(kThreads) k_decide_exact(const __grid_constant__ ExactParams P) {
-    uint64_t cnt[COLO_NCOUNTERS];
-    if (COUNT)
-#pragma unroll
-        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] = 0;
-    const colo_model m = P.m;
-    const colo_gpu g = P.g;
-    const uint32_t L = static_cast<uint32_t>(m.num_layers);
-    const bool cpa = P.cpa != 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < P.n;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint4 t = __ldcs(P.in + i);
-        const uint32_t cached = t.x, incoming = t.y, charged = t.z;
-        const uint32_t batch = t.w & 0xffffu, pending = (t.w >> 16) & 0xffu, dev = t.w >> 24;
-        const uint32_t fallback = incoming == 0 || batch == 0;
-        const uint32_t code = fallback ? 1u : offload_cell_code(m, P.budget, cpa, cached, incoming, batch);
-        uint32_t v;
-        if (code == 0) {
-            v = 0;
-        } else {
-            const uint32_t layers = code >= 2 ? code - 2 : 0;
-            const uint32_t free_now = code == 1 ? dev : min(layers, dev);
-            const uint32_t total = min(pending + (code == 1 ? L : layers), L);
-            uint32_t recompute = 1, hedge_oor = 0;
-            if (!fallback) {
-                if (cached == 0) {
-                    hedge_oor = 1;
-                } else {
-                    const double rc = hedge_recompute_time(m, cpa, cached, P.assumed);
-                    const double res = hedge_residual_load_time(m, g, cached, total);
-                    recompute = res > rc;
-                }
-            }
-            v = pack_verdict(code == 1 ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS, layers, free_now, recompute, fallback,
-                             hedge_oor, recompute ? COLO_VD_RECOMPUTE_DROP : COLO_VD_FREE_LOADBACK);
-        }
-        if (offload_cell_code(m, P.budget, cpa, charged, 1, 1) == 1) v |= COLO_V_STREAM;
-        __stcs(P.out + i, v);
-        if (COUNT) count_verdict(v, cnt);
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint4* tiles = reinterpret_cast<uint4*>(sm);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kExactStages * kTile * 16);
+    uint32_t* sbits = reinterpret_cast<uint32_t*>(sm + kExactStages * kTile * 16 + 64);
+    uint8_t* thr = reinterpret_cast<uint8_t*>(sbits + kSmemTab / 32);
+    const uint64_t ntiles = (P.n + kTile - 1) / kTile;
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < kExactStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
     }
-    if (COUNT) flush_counters(cnt, P.counters);
+    for (uint32_t w = threadIdx.x; w < kSmemTab / 32; w += blockDim.x) {
+        uint32_t bits = 0;
+        for (uint32_t b = 0; b < 32; ++b) bits |= static_cast<uint32_t>(__ldg(P.tab + 32 * w + b) >> 8) << b;
+        sbits[w] = bits;
+    }
+    for (uint32_t c = threadIdx.x; c < kSmemTab; c += blockDim.x) thr[c] = static_cast<uint8_t>(__ldg(P.tab + c));
+    __syncthreads();
+    auto issue = [&](uint32_t s, uint64_t t) {
+        const uint64_t rest = P.n - t * kTile;
+        const uint32_t bytes = static_cast<uint32_t>(rest < kTile ? rest : kTile) * 16u;
+        mbar_arrive_expect_tx(&bars[s], bytes);
+        bulk_g2s(tiles + s * kTile, P.in + t * kTile, bytes, &bars[s]);
+    };
+    if (threadIdx.x == 0)
+        for (uint32_t s = 0; s < kExactStages; ++s) {
+            const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
+            if (t < ntiles) issue(s, t);
+        }
+    const bool cpa = P.cpa != 0;
+    uint32_t cnt[COLO_NCOUNTERS] = {};
+    uint32_t it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const uint32_t s = it % kExactStages;
+        mbar_wait(&bars[s], (it / kExactStages) & 1u);
+        const uint64_t base = t * kTile;
+        const uint64_t rest = P.n - base;
+        const uint32_t len = static_cast<uint32_t>(rest < kTile ? rest : kTile);
+#pragma unroll
+        for (uint32_t q = 0; q < kTile / kThreads; ++q) {
+            const uint32_t i = threadIdx.x + q * kThreads;
+            const bool valid = i < len;
+            const uint4 tu = valid ? tiles[s * kTile + i] : make_uint4(0, 1, 0, 1);
+            const uint32_t v = exact_verdict(P, cpa, tu, thr, sbits);
+            if (valid) __stcs(P.out + base + i, v);
+            if (COUNT) count_warp(v, valid, cnt);
+        }
+        __syncthreads();  // stage s consumed by every thread
+        if (threadIdx.x == 0) {
+            const uint64_t nt = t + static_cast<uint64_t>(kExactStages) * gridDim.x;
+            if (nt < ntiles) issue(s, nt);
+        }
+    }
+    if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
 // --------------------------------------------------------------- fused path
@@ -573,10 +704,18 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
     const size_t smem = ((P.mv.off_bytes + 15u) & ~15u) + P.mv.hed_bytes;
     const bool use_smem = smem <= 96 * 1024;
     if (use_smem && !(reinterpret_cast<uintptr_t>(d_in) & 15u)) {  // TMA pipeline
-        const size_t dyn = kStages * kTile * 16 + 64 + smem;
+        // 4 stages while the cells are small; 2 for sweep-size grids, so two
+        // CTAs still fit next to 64 KB of cells
+        const bool deep = smem <= 32 * 1024;
+        const size_t dyn = (deep ? kStages : 2u) * kTile * 16 + 64 + smem;
         const bool fast = P.mv.hsame && P.mv.fc.d > 1 && P.mv.fi.d > 1 && P.mv.fb.d > 1;
-        const void* fn = d_counters ? (fast ? (const void*)k_decide_tma<true, true> : (const void*)k_decide_tma<true, false>)
-                                    : (fast ? (const void*)k_decide_tma<false, true> : (const void*)k_decide_tma<false, false>);
+        const void* fn;
+        if (deep)
+            fn = d_counters ? (fast ? (const void*)k_decide_tma<true, true, kStages> : (const void*)k_decide_tma<true, false, kStages>)
+                            : (fast ? (const void*)k_decide_tma<false, true, kStages> : (const void*)k_decide_tma<false, false, kStages>);
+        else
+            fn = d_counters ? (fast ? (const void*)k_decide_tma<true, true, 2> : (const void*)k_decide_tma<true, false, 2>)
+                            : (fast ? (const void*)k_decide_tma<false, true, 2> : (const void*)k_decide_tma<false, false, 2>);
         COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         int blocks = blocks_for(ctx, fn, kThreads, dyn);
         const uint64_t ntiles = (n + kTile - 1) / kTile;
@@ -632,13 +771,35 @@ colo_status colo_decide_exact(colo_ctx* ctx, const colo_model* m, const colo_gpu
     P.out = d_out;
     P.n = n;
     P.counters = d_counters;
+    P.L = static_cast<uint32_t>(m->num_layers);
+    P.abpt = m->act_bytes_per_token_per_layer;
+    P.kvbpt = m->kv_bytes_per_token;
+    P.ak = m->num_layers * m->act_bytes_per_token_per_layer + (P.cpa ? m->kv_bytes_per_token : 0ull);
+    P.wf_mode = m->workspace_factor == 1.0 ? 1u : 0u;
+    // per-value tables: rebuilt only when (model, gpu, mode, assumed) changes
+    unsigned char key[sizeof(ctx->htab_key)] = {};
+    std::memcpy(key, m, sizeof(colo_model));
+    std::memcpy(key + sizeof(colo_model), g, sizeof(colo_gpu));
+    std::memcpy(key + sizeof(colo_model) + sizeof(colo_gpu), &P.cpa, sizeof(uint32_t));
+    std::memcpy(key + sizeof(colo_model) + sizeof(colo_gpu) + 8, &assumed, sizeof(uint64_t));
+    if (!ctx->d_htab) COLO_CK(ctx, cudaMalloc(&ctx->d_htab, kExactTab * sizeof(uint16_t)));
+    if (!ctx->htab_valid || std::memcmp(key, ctx->htab_key, sizeof(key)) != 0) {
+        COLO_LAUNCHED(ctx);
+        k_exact_tab<<<kExactTab / 256, 256, 0, ctx->stream>>>(*m, *g, P.cpa, assumed, P.budget, ctx->d_htab);
+        COLO_CK(ctx, cudaGetLastError());
+        std::memcpy(ctx->htab_key, key, sizeof(key));
+        ctx->htab_valid = true;
+    }
+    P.tab = ctx->d_htab;
     const void* fn = d_counters ? (const void*)k_decide_exact<true> : (const void*)k_decide_exact<false>;
-    int blocks = blocks_for(ctx, fn, kThreads, 0);
-    const uint64_t need_blocks = (n + kThreads - 1) / kThreads;
-    if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+    const size_t dyn = kExactStages * kTile * 16 + 64 + kSmemTab / 8 + kSmemTab;
+    COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int blocks = blocks_for(ctx, fn, kThreads, dyn);
+    const uint64_t ntiles = (n + kTile - 1) / kTile;
+    if (static_cast<uint64_t>(blocks) > ntiles) blocks = static_cast<int>(ntiles);
     void* args[] = {&P};
     COLO_LAUNCHED(ctx);
-    COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, 0, ctx->stream));
+    COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kThreads), args, dyn, ctx->stream));
     return COLO_OK;
 }
 

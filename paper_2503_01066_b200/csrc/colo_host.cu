@@ -191,6 +191,7 @@ void colo_ctx_destroy(colo_ctx* ctx) {
     if (ctx->d_tmp) cudaFree(ctx->d_tmp);
     if (ctx->d_bmeta) cudaFree(ctx->d_bmeta);
     if (ctx->d_dtab) cudaFree(ctx->d_dtab);
+    if (ctx->d_htab) cudaFree(ctx->d_htab);
     if (ctx->own) cudaStreamDestroy(ctx->own);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     delete ctx;

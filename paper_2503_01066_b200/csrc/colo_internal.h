@@ -39,6 +39,9 @@ struct colo_ctx {
     void* d_bmeta = nullptr;        // serving stats: per-query batch start + sample-bin range (lazily grown)
     size_t bmeta_bytes = 0;
     bool bmeta_valid = false;       // d_bmeta holds the batch records of the replay rs_sig describes
+    uint16_t* d_htab = nullptr;     // exact decide: per-value hedge thresholds + stream bits (k_exact_tab)
+    unsigned char htab_key[sizeof(colo_model) + sizeof(colo_gpu) + 16] = {};  // what d_htab was built for
+    bool htab_valid = false;
     // serving replay: identity of the last full replay whose segment entry
     // states are still in d_rscratch (reuse_entries); any other d_rscratch
     // user clears rs_valid

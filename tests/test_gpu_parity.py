@@ -155,6 +155,41 @@ def test_decide_exact_random_vs_oracle(ctx, orc):
             assert (u32(cs.decide_exact(ctx, m, G, cs.TrainingMode(cpa), dt)) == orc.decide_exact(om, OG, cpa, t)).all()
 
 
+def test_decide_exact_quotient_edges(ctx, orc):
+    """The divide-free exact path (fp32 quotient estimate + u64 correction,
+    per-cached hedge thresholds) against the oracle where the ceil-divide of
+    maps.hpp:227 lands exactly on integers (tiny per-layer bytes), around n = L,
+    across the whole u32 range (u64 wrap in the byte products) and for
+    cached values past the threshold table."""
+    rng = np.random.default_rng(31)
+    small = [(cs.ModelProfile(num_layers=L, kv_bytes_per_token=kv, act_bytes_per_token_per_layer=a,
+                              workspace_factor=wf, weights_bytes=w),
+              cs.GpuProfile(capacity_bytes=cap, h2d_bandwidth=h2d, d2h_bandwidth=h2d, runtime_reserve_bytes=0))
+             for L, kv, a, wf, w, cap, h2d in ((32, 3, 1, 0.0, 1, 400_000, 1000), (40, 5, 2, 0.5, 1000, 2_000_000, 77),
+                                               (7, 1, 3, 0.25, 1, 60_000, 3), (253, 2, 1, 1.0, 1, 1_000_000, 10_000))]
+    big = [(m, G) for m, _ in MODELS.values()]
+    for m, g in small + big:
+        om, og = m.to_c(), g.to_c()
+        L = int(m.num_layers)
+        n = 400_000
+        t = np.zeros(n, TUPLE_DTYPE)
+        q = n // 4
+        t["cached"][:q] = rng.integers(0, 3000, q)                    # dense small values: exact quotients
+        t["cached"][q:2 * q] = rng.integers(60_000, 70_000, q)        # both sides of the 65536-entry table
+        t["cached"][2 * q:] = rng.integers(0, 2**32, n - 2 * q, dtype=np.uint64)  # wrap-around in acts / bytes
+        t["incoming"] = np.where(rng.random(n) < 0.5, rng.integers(0, 20_000, n), rng.integers(0, 2**32, n, dtype=np.uint64))
+        t["charged"] = np.where(rng.random(n) < 0.5, rng.integers(0, 20_000, n), rng.integers(0, 2**32, n, dtype=np.uint64))
+        t["batch"] = np.where(rng.random(n) < 0.8, rng.integers(0, 60, n), rng.integers(0, 65536, n))
+        t["pending"] = rng.integers(0, min(L + 5, 256), n)
+        t["dev_layers"] = rng.integers(0, min(L + 5, 256), n)
+        dt = to_dev_tuples(t)
+        for cpa in (0, 1):
+            got = u32(cs.decide_exact(ctx, m, g, cs.TrainingMode(cpa), dt))
+            want = orc.decide_exact(om, og, cpa, t)
+            bad = np.nonzero(got != want)[0]
+            assert bad.size == 0, (L, cpa, t[bad[:3]], got[bad[:3]], want[bad[:3]])
+
+
 def test_decide_host_pipeline(ctx, orc):
     rng = np.random.default_rng(13)
     t = random_tuples(rng, 9_000_001, 32)  # > one 8M pipeline chunk
