@@ -45,6 +45,7 @@ namespace {
 constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
+constexpr int kSatHdr = 4;   // per all-queued record: its chain sums in 4 candidate binades (k_sat_durations)
 #ifndef COLO_REPLAY_BLOCKS
 #define COLO_REPLAY_BLOCKS 5
 #endif
@@ -61,6 +62,22 @@ struct DevProfile {
 struct Seg {
     uint32_t dev, pad;
     uint64_t start, end;  // device-local query range
+};
+
+// One all-queued batch record (k_sat_durations), dense in the order
+// k_sat_partition's pass 2 forms them: within a partition segment record
+// r + 1 starts where record r ends, so the resolve pass streams records
+// instead of chasing sat_end.  R[c]: the decode chain's sum in units of the
+// binade (binade of the last arrival) + c (~0 = not usable); the step
+// durations are at sat_dk[doff], K of them.
+struct alignas(16) SatRec {
+    uint64_t R[kSatHdr];
+    uint64_t doff;
+    uint32_t start, end;  // device-local [start, end)
+    uint32_t K, dev;
+    double pre;           // prefill duration (engine.hpp:321-325)
+    double alast;         // the batch's last arrival (the fast path needs alast <= T)
+    uint64_t pad;
 };
 
 struct SpecOut {
@@ -115,12 +132,13 @@ struct ReplayParams {
     int* err;
     // Saturated fast path of the resolve pass (see k_sat_partition): per
     // query q, the batch start_serving_batch forms at q when every query has
-    // already arrived -- [q, sat_end[q]) -- with its step count, prefill and
-    // per-step decode durations.  sat_end == 0: no record at q.
+    // already arrived -- [q, sat_end[q]) -- and its record (SatRec: step count,
+    // prefill, chain sums, per-step decode durations).  sat_end == 0: no record at q.
     uint32_t* sat_end;     // [dev_off[d] + q]
-    uint32_t* sat_maxo;
-    uint64_t* sat_doff;    // first step duration in sat_dk
-    double* sat_pre;
+    uint32_t* sat_rec;     // [dev_off[d] + q] record index
+    SatRec* sat_recs;
+    uint64_t sat_nrec;     // records in sat_recs
+    uint64_t* sat_recbase; // [pseg] record count, then its base (exclusive scan)
     const Seg* psegs;      // partition segments (longer than the replay segments: the greedy
     uint32_t npsegs;       // partition from a segment's start needs a few batches to meet the true one)
     uint64_t* sat_seg;     // [pseg] step durations of the segment's records, then their base (exclusive scan)
@@ -382,110 +400,158 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 // already arrived is exactly the batch start_serving_batch forms
                 // (engine.hpp:292-306 never reaches the queue's end), so only the
                 // absolute-time chain remains: now = (T + 0.0) + prefill, then
-                // now += d_k for every step, in order.  Consecutive recorded
-                // batches run in a loop that loads batch i+1's record and
-                // durations while lane 0 chains batch i.
+                // now += d_k for every step, in order.  While now stays in its
+                // binade that chain is now + u * R with the record's precomputed
+                // R (exact, see chain_fast_end), so a record costs a few integer
+                // operations.  The records of a partition come dense in chain
+                // order: the warp loads 32 at a time (lane l: record r + l) and
+                // walks them on broadcasts, re-entering through sat_rec where a
+                // partition segment's chain does not continue.
                 const uint32_t* __restrict__ se = P.sat_end + lo;
-                const uint32_t* __restrict__ smo = P.sat_maxo + lo;
-                const uint64_t* __restrict__ sdo = P.sat_doff + lo;
-                const double* __restrict__ spre = P.sat_pre + lo;
+                const uint32_t* __restrict__ srec = P.sat_rec + lo;
                 const double* __restrict__ pool = P.sat_dk;
-                uint64_t bend = se[head];
                 bool progressed = false;
-                if (bend != 0) {
-                    // batch i = [head, bend): its record, its durations (cur) and
-                    // its last arrival; batch i+1 = [bend, e1): its record (n1*),
-                    // with its last arrival and durations loaded during batch i's
-                    // chain together with batch i+2's record -- no load waits in
-                    // front of a chain
-                    uint32_t K = smo[head];
-                    double pre = spre[head];
-                    double alast = arr[bend - 1];
-                    double cur[4];
-                    uint64_t dof = sdo[head];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        const uint32_t i = 32 * r + lane;
-                        cur[r] = (K <= 128 && i < K) ? pool[dof + i] : 0.0;
+                bool more = se[head] != 0;
+                uint64_t r = more ? srec[head] : 0;
+                auto load_rec = [&](uint64_t i) {
+                    SatRec y;
+                    if (i < P.sat_nrec) {
+                        y = P.sat_recs[i];
+                    } else {
+                        y.dev = 0xffffffffu;
+                        y.start = y.end = 0;
                     }
-                    const bool in1 = bend < stop && bend < N;
-                    uint64_t e1 = in1 ? se[bend] : 0;
-                    uint32_t K1 = in1 ? smo[bend] : 0;
-                    uint64_t dof1 = in1 ? sdo[bend] : 0;
-                    double pre1 = in1 ? spre[bend] : 0.0;
-                    for (;;) {
-                        if (!(alast <= T)) break;  // a member has not arrived: form it the slow way
-                        const bool hn = e1 != 0;
-                        double alast1 = 0.0, nxt[4] = {0.0, 0.0, 0.0, 0.0};
-                        uint64_t e2 = 0, dof2 = 0;
-                        uint32_t K2 = 0;
-                        double pre2 = 0.0;
-                        if (hn) {
-                            alast1 = arr[e1 - 1];
+                    return y;
+                };
+                // window r in x; window r + 32 is loaded while x is walked
+                SatRec x = more ? load_rec(r + lane) : SatRec{};
+                while (more) {
+                    const uint64_t rl = r + lane;
+                    const SatRec xn = load_rec(r + 32 + lane);
+                    const double al = x.dev == d ? x.alast : 0.0;
+                    if (P.dbg && lane == 0) atomicAdd(P.dbg + 3, 1ull);
+                    {  // the windows after that: into L2
+                        const char* q = reinterpret_cast<const char*>(P.sat_recs + r + 64) + lane * 160;
+                        if (r + 128 < P.sat_nrec) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                    }
+                    // The window in one step: while T stays in its binade e every
+                    // addend is an integer number of units u = 2^(e-52) (fl(T + x)
+                    // = T + RN_u(x), no ties), so record l moves T's bit pattern by
+                    // RN_u(pre_l)/u + R_l[e] and the T at every record boundary is an
+                    // exclusive warp scan.  Lanes up to the first one whose record
+                    // does not continue the chain, has not fully arrived, needs
+                    // another binade or has a tie are applied at once; that record
+                    // then goes through the per-record loop below.
+                    uint32_t l = 0;
+                    if (T >= 0x1p-190 && T <= 0x1p190) {
+                        const uint64_t t0 = static_cast<uint64_t>(__double_as_longlong(T));
+                        const int eT = binade_of(T);
+                        const double sc = pow2i(52 - eT);
+                        const uint32_t pend = __shfl_up_sync(FULL, x.end, 1);
+                        bool v = rl < P.sat_nrec && x.dev == d && x.K <= 128 && al >= 0x1p-190 &&
+                                 static_cast<uint64_t>(x.start) == (lane == 0 ? head : static_cast<uint64_t>(pend)) &&
+                                 x.start < stop && x.start < N;
+                        const int c = eT - binade_of(al);
+                        const uint64_t Rc = c == 0 ? x.R[0] : c == 1 ? x.R[1] : c == 2 ? x.R[2] : x.R[3];
+                        v = v && c >= 0 && c < kSatHdr && Rc != ~0ull;
+                        uint64_t rp = 0;
+                        v = v && rn_units(x.pre, sc, rp);
+                        const uint64_t a = v ? rp + Rc : 0ull;
+                        uint64_t incl = a;
 #pragma unroll
-                            for (int r = 0; r < 4; ++r) {
-                                const uint32_t i = 32 * r + lane;
-                                if (K1 <= 128 && i < K1) nxt[r] = pool[dof1 + i];
-                            }
-                            if (e1 < stop && e1 < N) {
-                                e2 = se[e1];
-                                K2 = smo[e1];
-                                dof2 = sdo[e1];
-                                pre2 = spre[e1];
-                            }
-                            {  // records and durations stream forward: keep a few batches ahead in L2
-                                const char* q;
-                                if (lane < 16) q = reinterpret_cast<const char*>(pool + dof1 + 512) + lane * 128;
-                                else if (lane < 20) q = reinterpret_cast<const char*>(se + e1 + 256) + (lane - 16) * 128;
-                                else if (lane < 24) q = reinterpret_cast<const char*>(smo + e1 + 256) + (lane - 20) * 128;
-                                else if (lane < 28) q = reinterpret_cast<const char*>(sdo + e1 + 256) + (lane - 24) * 256;
-                                else q = reinterpret_cast<const char*>(spre + e1 + 256) + (lane - 28) * 256;
-                                if (e1 + 1024 < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint64_t y = __shfl_up_sync(FULL, incl, o);
+                            if (lane >= static_cast<uint32_t>(o)) incl += y;
+                        }
+                        v = v && (t0 & ((1ull << 52) - 1)) + incl < (1ull << 52);
+                        v = v && al <= __longlong_as_double(static_cast<long long>(t0 + (incl - a)));
+                        const uint32_t bad = __ballot_sync(FULL, !v);
+                        l = bad ? static_cast<uint32_t>(__ffs(bad) - 1) : 32u;
+                        if (l > 0) {
+                            T = __longlong_as_double(static_cast<long long>(t0 + __shfl_sync(FULL, incl, l - 1)));
+                            head = __shfl_sync(FULL, x.end, l - 1);
+                            progressed = true;
+                            if (P.dbg && lane == 0) {
+                                atomicAdd(P.dbg, static_cast<unsigned long long>(l));
+                                atomicAdd(P.dbg + 2, static_cast<unsigned long long>(l));
                             }
                         }
+                    }
+                    bool chain_break = false;  // else: the window is done, or the fast path ends here
+                    const uint32_t l1 = l < 32 ? l + 1 : 32u;  // one record past the scanned ones, then rescan
+                    for (; l < l1; ++l) {
+                        const uint32_t xs = __shfl_sync(FULL, x.start, l), xe = __shfl_sync(FULL, x.end, l);
+                        const uint32_t xd = __shfl_sync(FULL, x.dev, l);
+                        if (head >= stop || head >= N) break;
+                        if (xd != d || xs != head) {
+                            chain_break = true;
+                            break;
+                        }
+                        const double alast = __shfl_sync(FULL, al, l);
+                        if (!(alast <= T)) break;  // a member has not arrived: form it the slow way
+                        const double pre = __shfl_sync(FULL, x.pre, l);
+                        const uint32_t K = __shfl_sync(FULL, x.K, l);
                         double now = (T + 0.0) + pre;
-                        double fast_end;
-                        if (K <= 128 && chain_fast_end(now, cur, K, fast_end)) {
-                            now = fast_end;
-                        } else if (K <= 128) {
-#pragma unroll
-                            for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = cur[r];
-                            __syncwarp();
-                            if (lane == 0) sDK[0] = chain_fold(now, sDK, K);
-                            __syncwarp();
-                            now = sDK[0];
-                            __syncwarp();
+                        const bool rng = K <= 128 && now >= 0x1p-190 && now <= 0x1p190 && alast >= 0x1p-190;
+                        const int c = rng ? binade_of(now) - binade_of(alast) : -1;
+                        const uint64_t Rc = c == 0 ? x.R[0] : c == 1 ? x.R[1] : c == 2 ? x.R[2] : x.R[3];
+                        const uint64_t R = __shfl_sync(FULL, Rc, l);
+                        const uint64_t nbits = static_cast<uint64_t>(__double_as_longlong(now));
+                        const uint64_t mnow = (nbits & ((1ull << 52) - 1)) | (1ull << 52);
+                        if (c >= 0 && c < kSatHdr && R != ~0ull && R < (1ull << 53) - mnow) {
+                            if (P.dbg && lane == 0) atomicAdd(P.dbg + 2, 1ull);
+                            now = __longlong_as_double(
+                                static_cast<long long>((nbits & ~((1ull << 52) - 1)) | ((mnow + R) & ((1ull << 52) - 1))));
                         } else {
-                            for (uint32_t k0 = 0; k0 < K; k0 += 128) {
-                                const uint32_t c = min(128u, K - k0);
+                            const uint64_t dof = __shfl_sync(FULL, x.doff, l);
+                            if (K <= 128) {
+                                double cur[4];
 #pragma unroll
-                                for (int r = 0; r < 4; ++r) {
-                                    const uint32_t i = 32 * r + lane;
-                                    if (i < c) sDK[i] = pool[dof + k0 + i];
+                                for (int q = 0; q < 4; ++q) {
+                                    const uint32_t i = 32 * q + lane;
+                                    cur[q] = i < K ? pool[dof + i] : 0.0;
                                 }
-                                __syncwarp();
-                                if (lane == 0) sDK[0] = chain_fold(now, sDK, c);
-                                __syncwarp();
-                                now = sDK[0];
-                                __syncwarp();
+                                double fast_end;
+                                if (chain_fast_end(now, cur, K, fast_end)) {
+                                    now = fast_end;
+                                } else {
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q) sDK[32 * q + lane] = cur[q];
+                                    __syncwarp();
+                                    if (lane == 0) sDK[0] = chain_fold(now, sDK, K);
+                                    __syncwarp();
+                                    now = sDK[0];
+                                    __syncwarp();
+                                }
+                            } else {
+                                for (uint32_t k0 = 0; k0 < K; k0 += 128) {
+                                    const uint32_t cc = min(128u, K - k0);
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q) {
+                                        const uint32_t i = 32 * q + lane;
+                                        if (i < cc) sDK[i] = pool[dof + k0 + i];
+                                    }
+                                    __syncwarp();
+                                    if (lane == 0) sDK[0] = chain_fold(now, sDK, cc);
+                                    __syncwarp();
+                                    now = sDK[0];
+                                    __syncwarp();
+                                }
                             }
                         }
                         T = now;
-                        head = bend;
+                        head = xe;
                         progressed = true;
                         if (P.dbg && lane == 0) atomicAdd(P.dbg, 1ull);
-                        if (!hn) break;
-                        bend = e1;
-                        K = K1;
-                        dof = dof1;
-                        pre = pre1;
-                        alast = alast1;
-#pragma unroll
-                        for (int r = 0; r < 4; ++r) cur[r] = nxt[r];
-                        e1 = e2;
-                        K1 = K2;
-                        dof1 = dof2;
-                        pre1 = pre2;
+                    }
+                    if (l == l1) {
+                        r += l;
+                        x = l == 32 ? xn : load_rec(r + lane);
+                    } else if (chain_break && se[head] != 0) {
+                        r = srec[head];  // the chain continues in another partition segment's records
+                        x = load_rec(r + lane);
+                    } else {
+                        more = false;
                     }
                 }
                 if (progressed) continue;
@@ -532,7 +598,8 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         // FULL pass: a batch the all-queued records describe exactly takes its
         // prefill and step durations from them (the same folds, done once)
         const bool recd = MODE == RUN_FULL && P.sat_on && P.sat_end[lo + head] == end;
-        const double* __restrict__ rdk = recd ? P.sat_dk + P.sat_doff[lo + head] : nullptr;
+        const SatRec* __restrict__ rrec = recd ? P.sat_recs + P.sat_rec[lo + head] : nullptr;
+        const double* __restrict__ rdk = recd ? P.sat_dk + rrec->doff : nullptr;
         // The replay walks each array sequentially: keep the next ~1K queries of
         // prompt/output and the arrivals around the queue tail warm in L2 so the
         // dependent loads of later batches hit L2 instead of DRAM.
@@ -554,7 +621,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         // cost_model.hpp:18-25 with batch 1: 1.0 * (lin*t + (quad*t)*t) == lin*t + (quad*t)*t
         double dur = 0.0;
         if (recd) {
-            dur = P.sat_pre[lo + head];
+            dur = rrec->pre;
         } else {
 #pragma unroll 4
             for (uint64_t j = 0; j < nb; ++j) {
@@ -793,12 +860,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_partition(const __grid_cons
     uint64_t h = sg.start, steps = 0;
     if (rec && sg.start > 0) h = P.sat_exit[w - 1];  // the previous segment of this device (same device: start > 0)
     if (lane == 0 && rec) P.sat_seg_start[w] = h;
+    uint64_t nrec = 0;
     auto record = [&](uint64_t start, uint64_t end, uint32_t mo) {
-        if (rec && lane == 0) {
-            P.sat_end[lo + start] = static_cast<uint32_t>(end);
-            P.sat_maxo[lo + start] = mo;
-        }
+        if (rec && lane == 0) P.sat_end[lo + start] = static_cast<uint32_t>(end);
         steps += mo;
+        ++nrec;
     };
     while (h < sg.end) {
         const uint64_t base = h;
@@ -885,8 +951,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_partition(const __grid_cons
         }
     }
     if (lane == 0) {
-        if (rec) P.sat_seg[w] = steps;
-        else P.sat_exit[w] = h;
+        if (rec) {
+            P.sat_seg[w] = steps;
+            P.sat_recbase[w] = nrec;
+        } else {
+            P.sat_exit[w] = h;
+        }
     }
 }
 
@@ -910,6 +980,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
     uint2* sPO = spo[warp];
     double* sPD = spd[warp];
     uint64_t doff = P.sat_seg[w];
+    uint64_t ridx = P.sat_recbase[w];
     uint64_t head = P.sat_seg_start[w];
     while (head < sg.end) {
         const uint64_t end = P.sat_end[lo + head];
@@ -932,8 +1003,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
             const double t = member_pd(j);
             dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
         }
-        const uint32_t maxo = P.sat_maxo[lo + head];
+        uint32_t maxo = 0;
+        for (uint64_t j = lane; j < nb; j += 32) maxo = max(maxo, staged ? sPO[j].y : po[head + j]);
+        maxo = static_cast<uint32_t>(warp_max_u64(maxo));
         double* dk = P.sat_dk + doff;
+        double first[4] = {0.0, 0.0, 0.0, 0.0};  // steps 0..127 (lane = step mod 32)
         for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {  // engine.hpp:358-365 per step
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             const uint32_t kb = k0 + lane;
@@ -960,13 +1034,51 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
                 }
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 4; ++r) {
                 if (kb + 32 * r < maxo) dk[kb + 32 * r] = acc[r];
+                if (k0 == 0) first[r] = acc[r];
+            }
         }
-        if (lane == 0) {
-            P.sat_pre[lo + head] = dur;
-            P.sat_doff[lo + head] = doff;
+        // Chain sums for the resolve pass: the batch's decode chain from now
+        // (after its prefill) is now + u * R with R = sum_k RN_u(d_k) / u
+        // while now stays in its binade e (u = 2^(e-52); see chain_fast_end).
+        // now >= the batch's last arrival whenever the record is used, so
+        // R is kept for the binades of that arrival and the three above;
+        // ~0 = not usable (a tie, a step count above 128, or out of range).
+        {
+            const double alast = P.arr[lo + end - 1];
+            const bool ok0 = maxo <= 128 && alast >= 0x1p-190 && alast <= 0x1p190;
+            const int eb = ok0 ? binade_of(alast) : 0;
+            uint64_t Rmine = ~0ull;
+#pragma unroll
+            for (int c = 0; c < kSatHdr; ++c) {
+                const double sc = pow2i(52 - (eb + c));
+                bool ok = ok0;
+                uint64_t sum = 0;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    uint64_t rk = 0;
+                    if (ok0 && static_cast<uint32_t>(32 * r) + lane < maxo) ok &= rn_units(first[r], sc, rk);
+                    sum += rk;
+                }
+                const bool all = __all_sync(FULL, ok);
+                const uint64_t R = warp_sum_small(sum);
+                if (lane == static_cast<uint32_t>(c)) Rmine = all ? R : ~0ull;
+            }
+            SatRec& rr = P.sat_recs[ridx];
+            if (lane < static_cast<uint32_t>(kSatHdr)) rr.R[lane] = Rmine;
+            if (lane == 0) {
+                rr.doff = doff;
+                rr.start = static_cast<uint32_t>(head);
+                rr.end = static_cast<uint32_t>(end);
+                rr.K = maxo;
+                rr.dev = d;
+                rr.pre = dur;
+                rr.alast = alast;
+                P.sat_rec[lo + head] = static_cast<uint32_t>(ridx);
+            }
         }
+        ++ridx;
         doff += maxo;
         head = end;
         __syncwarp();
@@ -1395,7 +1507,7 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         COLO_CK(ctx, cudaStreamSynchronize(st));
         if (nsat * 50 < P.nsegs || nsat < 2) return COLO_OK;
     }
-    const size_t need_rec = n * 24 + ns * 64 + 512;
+    const size_t need_rec = n * 8 + ns * 72 + 1024;
     if (sc->sat_bytes < need_rec) {
         size_t freeb = 0, totb = 0;
         COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
@@ -1406,14 +1518,13 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         if (g != COLO_OK) return g;
     }
     auto* bp = static_cast<uint8_t*>(sc->d_sat);
-    P.sat_doff = reinterpret_cast<uint64_t*>(bp);
-    P.sat_pre = reinterpret_cast<double*>(bp + n * 8);
-    P.sat_end = reinterpret_cast<uint32_t*>(bp + n * 16);
-    P.sat_maxo = reinterpret_cast<uint32_t*>(bp + n * 20);
-    P.sat_seg = reinterpret_cast<uint64_t*>(bp + n * 24 + 128);
+    P.sat_end = reinterpret_cast<uint32_t*>(bp);
+    P.sat_rec = reinterpret_cast<uint32_t*>(bp + n * 4);
     const size_t s8 = (ns * 8 + 127) & ~size_t(127);
-    Seg* dps = reinterpret_cast<Seg*>(bp + n * 24 + 128 + s8);
-    P.sat_exit = reinterpret_cast<uint64_t*>(bp + n * 24 + 128 + s8 + ((ns * sizeof(Seg) + 127) & ~size_t(127)));
+    P.sat_seg = reinterpret_cast<uint64_t*>(bp + n * 8 + 128);
+    P.sat_recbase = reinterpret_cast<uint64_t*>(bp + n * 8 + 128 + s8);
+    Seg* dps = reinterpret_cast<Seg*>(bp + n * 8 + 128 + 2 * s8);
+    P.sat_exit = reinterpret_cast<uint64_t*>(bp + n * 8 + 128 + 2 * s8 + ((ns * sizeof(Seg) + 127) & ~size_t(127)));
     P.sat_seg_start = P.sat_exit + ((ns + 15) & ~size_t(15));
     COLO_CK(ctx, cudaMemcpyAsync(dps, ps.data(), ns * sizeof(Seg), cudaMemcpyHostToDevice, st));
     P.psegs = dps;
@@ -1439,23 +1550,30 @@ colo_status sat_prepare(colo_ctx* ctx, ReplayParams& P, const std::vector<uint64
         const colo_status gs = grow_buf(ctx, &sc->d_tmp, &sc->tmp_bytes, tb + 16);
         if (gs != COLO_OK) return gs;
     }
-    uint64_t last_in = 0, last_base = 0;
-    COLO_CK(ctx, cudaMemcpyAsync(&last_in, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    // (the same scan for the record counts; both totals come back to size the pool)
+    uint64_t last[4] = {0, 0, 0, 0};
+    COLO_CK(ctx, cudaMemcpyAsync(&last[0], P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    COLO_CK(ctx, cudaMemcpyAsync(&last[2], P.sat_recbase + ns - 1, 8, cudaMemcpyDeviceToHost, st));
     COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(sc->d_tmp, tb, P.sat_seg, P.sat_seg, static_cast<int>(ns), st));
-    COLO_CK(ctx, cudaMemcpyAsync(&last_base, P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    COLO_CK(ctx, cub::DeviceScan::ExclusiveSum(sc->d_tmp, tb, P.sat_recbase, P.sat_recbase, static_cast<int>(ns), st));
+    COLO_CK(ctx, cudaMemcpyAsync(&last[1], P.sat_seg + ns - 1, 8, cudaMemcpyDeviceToHost, st));
+    COLO_CK(ctx, cudaMemcpyAsync(&last[3], P.sat_recbase + ns - 1, 8, cudaMemcpyDeviceToHost, st));
     COLO_CK(ctx, cudaStreamSynchronize(st));
-    const uint64_t np = last_base + last_in;
-    if (sc->satpool_bytes < np * 8 + 8) {
+    const uint64_t np = last[1] + last[0], nr = last[3] + last[2];
+    const size_t pool_bytes = ((np * 8 + 255) & ~size_t(255)) + nr * sizeof(SatRec) + 256;
+    if (sc->satpool_bytes < pool_bytes) {
         size_t freeb = 0, totb = 0;
         COLO_CK(ctx, cudaMemGetInfo(&freeb, &totb));
-        if (np * 8 + (2ull << 30) > freeb + sc->satpool_bytes) return COLO_OK;  // no room for the step durations
+        if (pool_bytes + (2ull << 30) > freeb + sc->satpool_bytes) return COLO_OK;  // no room for the step durations
     }
     if (timing) cudaEventRecord(ev[1], st);
     {
-        const colo_status g = grow_buf(ctx, &sc->d_satpool, &sc->satpool_bytes, np * 8 + 8);
+        const colo_status g = grow_buf(ctx, &sc->d_satpool, &sc->satpool_bytes, pool_bytes);
         if (g != COLO_OK) return g;
     }
     P.sat_dk = static_cast<double*>(sc->d_satpool);
+    P.sat_recs = reinterpret_cast<SatRec*>(static_cast<uint8_t*>(sc->d_satpool) + ((np * 8 + 255) & ~size_t(255)));
+    P.sat_nrec = nr;
     COLO_LAUNCHED(ctx);
     k_sat_durations<<<blocks, kWarps * 32, 0, st>>>(P);
     COLO_CK(ctx, cudaGetLastError());
@@ -1771,7 +1889,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (timing) cudaEventRecord(ev[1], ctx->stream);
         if (timing) {
             P.dbg = reinterpret_cast<unsigned long long*>(ctx->d_counters);
-            cudaMemsetAsync(ctx->d_counters, 0, 16, ctx->stream);
+            cudaMemsetAsync(ctx->d_counters, 0, 32, ctx->stream);
         }
         COLO_LAUNCHED(ctx);
         k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
@@ -1785,11 +1903,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             cudaEventElapsedTime(&a, ev[0], ev[1]);
             cudaEventElapsedTime(&b, ev[1], ev[2]);
             cudaEventElapsedTime(&c, ev[2], ev[3]);
-            unsigned long long hits[2] = {0, 0};
-            cudaMemcpy(hits, ctx->d_counters, 16, cudaMemcpyDeviceToHost);
-            std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms (%llu fast / "
-                                 "%llu formed batches), replay %.3f ms\n",
-                         ns, static_cast<unsigned long long>(seg), a, b, hits[0], hits[1], c);
+            unsigned long long hits[4] = {0, 0, 0, 0};
+            cudaMemcpy(hits, ctx->d_counters, 32, cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms (%llu fast "
+                                 "[%llu by chain sums, %llu record windows] / %llu formed batches), replay %.3f ms\n",
+                         ns, static_cast<unsigned long long>(seg), a, b, hits[0], hits[2], hits[3], hits[1], c);
             for (auto& e : ev) cudaEventDestroy(e);
         }
     }
