@@ -77,7 +77,7 @@ struct alignas(16) SatRec {
     uint32_t K, dev;
     double pre;           // prefill duration (engine.hpp:321-325)
     double alast;         // the batch's last arrival (the fast path needs alast <= T)
-    uint64_t pad;
+    uint64_t need;        // sum of the members' serving memory (engine.hpp:297-306)
 };
 
 struct SpecOut {
@@ -85,6 +85,11 @@ struct SpecOut {
     double exit_T;
     uint32_t nregen;
     uint32_t regen[kRegen + 1];  // device-local offsets from the segment start
+    // struct_out: batch count, peak need and largest batch of the speculative
+    // run's interval i (batches from regen[i-1] up to regen[i]; interval 0 from
+    // the segment start, interval kRegen to the segment end)
+    uint32_t ib[kRegen + 1], imaxb[kRegen + 1];
+    uint64_t ineed[kRegen + 1];
 };
 
 struct Entry {
@@ -164,6 +169,14 @@ struct ReplayParams {
     const double* dtab[kMaxSets];
     uint64_t dtab_n;        // 0 = no table
     unsigned long long* maxctx;  // k_validate: max p + o over the trace
+    // first stats pass: the speculative and resolve passes also write every
+    // batch's start to bmeta (member positions cleared, within the segment)
+    // and its counts (SpecOut intervals / Partial), so no separate structure
+    // pass runs before k_batch_stats
+    uint32_t struct_out;
+    // k_batch_stats, first stats pass: the histogram bins [hwin_base, hwin_base +
+    // kHistWin) are counted in shared memory per CTA (u32; hwin = 0: off)
+    uint32_t hwin_base, hwin;
 };
 
 enum { RUN_SPEC = 0, RUN_RESOLVE = 1, RUN_FULL = 2 };
@@ -196,6 +209,32 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
     uint32_t ridx = 0;
     const uint32_t nreg = MODE == RUN_RESOLVE ? min(sp->nregen, static_cast<uint32_t>(kRegen)) : 0u;
     synced = false;
+    // batch structure out (bmeta starts + counts): the speculative and
+    // resolve passes with struct_out
+    const bool so = (MODE == RUN_SPEC || MODE == RUN_RESOLVE) && P.struct_out;
+    uint32_t ib = 0, imaxb = 0;  // SPEC with struct_out: lane i holds interval i
+    uint64_t ineed = 0;
+    auto mark = [&](uint64_t h, uint64_t e, double st, bool idl) {  // warp-uniform; [h, e) one batch
+        const uint64_t ce = min(e, stop);
+        for (uint64_t j = h + 1 + lane; j < ce; j += 32) P.bmeta_bins[lo + j] = 0;
+        if (lane == 0) {
+            P.bmeta_start[lo + h] = st;
+            P.bmeta_bins[lo + h] = (1ull << 63) | (idl ? 1ull << 62 : 0ull);
+        }
+    };
+    auto count_batch = [&](uint64_t need, uint64_t nb) {  // warp-uniform, one batch
+        if (MODE == RUN_SPEC) {
+            if (lane == min(ridx, static_cast<uint32_t>(kRegen))) {
+                ++ib;
+                ineed = max(ineed, need);
+                imaxb = max(imaxb, static_cast<uint32_t>(min(nb, static_cast<uint64_t>(0xffffffffu))));
+            }
+        } else {
+            ++A.nbatch;
+            A.max_need = max(A.max_need, need);
+            A.maxb = max(A.maxb, nb);
+        }
+    };
     while (head < stop && head < N) {
         // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
         uint64_t tail;
@@ -230,16 +269,47 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             const bool fits = inr && (lane == 0 || aq > prev_hi);
             const uint32_t bad = __ballot_sync(FULL, !fits);
             const uint32_t nv = bad ? static_cast<uint32_t>(__ffs(bad) - 1) : 32u;  // lanes [0, nv): batches
+            uint32_t hb = 0;
             if (MODE == RUN_RESOLVE) {  // stop at the first idle start the speculative run also had
                 const uint32_t rel = static_cast<uint32_t>(q - seg_start);
                 bool hit = false;
                 for (uint32_t i = 0; i < nreg; ++i) hit |= sp->regen[i] == rel;
-                const uint32_t hb = __ballot_sync(FULL, hit && lane < nv);
-                if (hb) {
-                    head += __ffs(hb) - 1;
-                    synced = true;
-                    return;
+                hb = __ballot_sync(FULL, hit && lane < nv);
+            }
+            if (so && MODE != RUN_FULL) {  // the window's batches (up to a sync point) into bmeta and the counts
+                const uint32_t nw = hb ? static_cast<uint32_t>(__ffs(hb) - 1) : nv;
+                const bool vw = lane < nw;
+                if (vw) {
+                    P.bmeta_start[lo + q] = aq + 0.0;
+                    P.bmeta_bins[lo + q] = (1ull << 63) | (1ull << 62);
                 }
+                const uint64_t need = vw ? serving_memory(m, static_cast<uint64_t>(pq) + oq, 1) : 0ull;
+                if (MODE == RUN_SPEC) {  // lane l's batch is regen point ridx + l: it opens interval ridx + l + 1
+                    const int src = static_cast<int>(lane) - static_cast<int>(ridx) - 1;
+                    const uint64_t nd = __shfl_sync(FULL, need, static_cast<uint32_t>(src) & 31u);
+                    if (src >= 0 && src < static_cast<int>(nw) && lane < static_cast<uint32_t>(kRegen)) {
+                        ++ib;
+                        ineed = max(ineed, nd);
+                        imaxb = max(imaxb, 1u);
+                    }
+                    const bool capped = vw && ridx + lane + 1 >= static_cast<uint32_t>(kRegen);
+                    const uint32_t nc = __popc(__ballot_sync(FULL, capped));
+                    const uint64_t mc = warp_max_u64(capped ? need : 0ull);
+                    if (lane == static_cast<uint32_t>(kRegen) && nc) {
+                        ib += nc;
+                        ineed = max(ineed, mc);
+                        imaxb = max(imaxb, 1u);
+                    }
+                } else {
+                    A.nbatch += nw;
+                    A.max_need = max(A.max_need, warp_max_u64(need));
+                    if (nw) A.maxb = max(A.maxb, static_cast<uint64_t>(1));
+                }
+            }
+            if (hb) {
+                head += __ffs(hb) - 1;
+                synced = true;
+                return;
             }
             if (MODE == RUN_SPEC) {
                 if (lane < nv && ridx + lane < kRegen) sp->regen[ridx + lane] = static_cast<uint32_t>(q - seg_start);
@@ -371,6 +441,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 A.maxb = max(A.maxb, static_cast<uint64_t>(1));
                 A.nbatch += nv;
             }
+            if (MODE == RUN_FULL && P.dbg && lane == 0) {
+                atomicAdd(P.dbg + 4, static_cast<unsigned long long>(nv));
+                atomicAdd(P.dbg + 5, 1ull);
+            }
             T = __shfl_sync(FULL, now, nv - 1);
             head += nv;
             tail_ptr = head;
@@ -464,9 +538,24 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                             if (lane >= static_cast<uint32_t>(o)) incl += y;
                         }
                         v = v && (t0 & ((1ull << 52) - 1)) + incl < (1ull << 52);
-                        v = v && al <= __longlong_as_double(static_cast<long long>(t0 + (incl - a)));
+                        const double tl = __longlong_as_double(static_cast<long long>(t0 + (incl - a)));
+                        v = v && al <= tl;
                         const uint32_t bad = __ballot_sync(FULL, !v);
                         l = bad ? static_cast<uint32_t>(__ffs(bad) - 1) : 32u;
+                        if (so && l > 0) {
+                            const bool tk = lane < l;
+                            // members of the l records (within the segment), then their starts
+                            const uint64_t ce = min(static_cast<uint64_t>(__shfl_sync(FULL, x.end, l - 1)), stop);
+                            for (uint64_t j = head + lane; j < ce; j += 32) P.bmeta_bins[lo + j] = 0;
+                            __syncwarp();
+                            if (tk) {  // start = T + 0.0 (engine.hpp:319) = T here (T > 0)
+                                P.bmeta_start[lo + x.start] = tl;
+                                P.bmeta_bins[lo + x.start] = 1ull << 63;
+                            }
+                            A.nbatch += l;
+                            A.max_need = max(A.max_need, warp_max_u64(tk ? x.need : 0ull));
+                            A.maxb = max(A.maxb, warp_max_u64(tk ? static_cast<uint64_t>(x.end - x.start) : 0ull));
+                        }
                         if (l > 0) {
                             T = __longlong_as_double(static_cast<long long>(t0 + __shfl_sync(FULL, incl, l - 1)));
                             head = __shfl_sync(FULL, x.end, l - 1);
@@ -539,6 +628,12 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                 }
                             }
                         }
+                        if (so) {
+                            mark(head, xe, T + 0.0, false);
+                            ++A.nbatch;
+                            A.max_need = max(A.max_need, __shfl_sync(FULL, x.need, l));
+                            A.maxb = max(A.maxb, static_cast<uint64_t>(xe - xs));
+                        }
                         T = now;
                         head = xe;
                         progressed = true;
@@ -597,7 +692,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         const uint64_t nb = end - head;
         // FULL pass: a batch the all-queued records describe exactly takes its
         // prefill and step durations from them (the same folds, done once)
-        const bool recd = MODE == RUN_FULL && P.sat_on && P.sat_end[lo + head] == end;
+        const bool recd = (MODE == RUN_FULL || (MODE == RUN_RESOLVE && P.struct_out)) && P.sat_on && P.sat_end[lo + head] == end;
         const SatRec* __restrict__ rrec = recd ? P.sat_recs + P.sat_rec[lo + head] : nullptr;
         const double* __restrict__ rdk = recd ? P.sat_dk + rrec->doff : nullptr;
         // The replay walks each array sequentially: keep the next ~1K queries of
@@ -662,13 +757,14 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             double kd[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
-            if (MODE == RUN_FULL && recd) {
+            if (recd) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
                     const uint32_t k = kb + 32 * r;
                     if (k < maxo) dk[r] = rdk[k];
                 }
-                if (mino == maxo) {  // every member alive at every step
+                if (MODE != RUN_FULL) {
+                } else if (mino == maxo) {  // every member alive at every step
 #pragma unroll
                     for (int r = 0; r < 4; ++r) alive[r] = kb + 32 * r < maxo ? static_cast<uint32_t>(nb) : 0u;
                 } else {
@@ -706,10 +802,25 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) sDK[32 * r + lane] = dk[r];
+            const uint32_t cnt = min(128u, maxo - k0);
+            if (MODE != RUN_FULL) {
+                // only the batch's end is needed: the chain as one warp scan while
+                // it stays in its binade, else one lane's sequential fold
+                double te;
+                if (chain_fast_end(now, dk, cnt, te)) {
+                    now = te;
+                } else {
+                    __syncwarp();
+                    if (lane == 0) sDK[0] = chain_fold(now, sDK, cnt);
+                    __syncwarp();
+                    now = sDK[0];
+                }
+                __syncwarp();
+                continue;
+            }
             __syncwarp();
             // absolute-time chain now_k = now_{k-1} + d_k, sequential on one
             // lane; the durations are overwritten by the absolute times
-            const uint32_t cnt = min(128u, maxo - k0);
             if (!chain_fast_store(now, sDK, cnt) && lane == 0) chain_fold_store(now, sDK, cnt);
             __syncwarp();
             // the four 32-step rows are post-processed by one (not unrolled)
@@ -816,12 +927,25 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             A.max_need = max(A.max_need, need_total);
             A.maxb = max(A.maxb, nb);
             ++A.nbatch;
+            if (P.dbg && lane == 0) {
+                atomicAdd(P.dbg + 6, 1ull);
+                atomicAdd(P.dbg + 7, static_cast<unsigned long long>(nb));
+            }
+        }
+        if (so && MODE != RUN_FULL) {
+            mark(head, end, start, idle_b);
+            count_batch(need_total, nb);
         }
         T = now;
         head = end;
         __syncwarp();
     }
     if (MODE == RUN_SPEC && lane == 0) sp->nregen = ridx;
+    if (MODE == RUN_SPEC && so && lane <= static_cast<uint32_t>(kRegen)) {
+        sp->ib[lane] = ib;
+        sp->imaxb[lane] = imaxb;
+        sp->ineed[lane] = ineed;
+    }
 }
 
 // dtab[pi][x] = gamma + delta * (double)x: decode_step_latency(x, 1, false)
@@ -1004,8 +1128,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
             dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
         }
         uint32_t maxo = 0;
-        for (uint64_t j = lane; j < nb; j += 32) maxo = max(maxo, staged ? sPO[j].y : po[head + j]);
+        uint64_t needs = 0;
+        for (uint64_t j = lane; j < nb; j += 32) {
+            const uint32_t pj = staged ? sPO[j].x : pp[head + j], oj = staged ? sPO[j].y : po[head + j];
+            maxo = max(maxo, oj);
+            needs += serving_memory(m, static_cast<uint64_t>(pj) + oj, 1);
+        }
         maxo = static_cast<uint32_t>(warp_max_u64(maxo));
+        needs = warp_sum_u64(needs);
         double* dk = P.sat_dk + doff;
         double first[4] = {0.0, 0.0, 0.0, 0.0};  // steps 0..127 (lane = step mod 32)
         for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {  // engine.hpp:358-365 per step
@@ -1075,6 +1205,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
                 rr.dev = d;
                 rr.pre = dur;
                 rr.alast = alast;
+                rr.need = needs;
                 P.sat_rec[lo + head] = static_cast<uint32_t>(ridx);
             }
         }
@@ -1155,22 +1286,44 @@ __global__ void __launch_bounds__(32) k_resolve(const __grid_constant__ ReplayPa
     __shared__ uint2 spo[1][kStage];
     __shared__ double spd[1][kStage];
     __shared__ __align__(16) double sdk[1][128];
-    const uint32_t warp = 0;
+    const uint32_t warp = 0, lane = threadIdx.x & 31;
     const uint32_t d = blockIdx.x;
     if (d >= P.ndev) return;
+    const uint64_t lo = P.dev_off[d];
     uint64_t head = 0;
     double T = -INFINITY;  // server idle before the first arrival (probe B4b)
-    Acc A;
     for (uint32_t k = P.dev_seg[d]; k < P.dev_seg[d + 1]; ++k) {
         const Seg sg = P.segs[k];
-        if ((threadIdx.x & 31) == 0) P.entry[k] = Entry{head, T};
-        if (head >= sg.end) continue;  // an earlier batch already covers this segment
-        bool synced;
-        run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp], spd[warp],
-                                 sdk[warp], nullptr);
-        if (synced) {
-            head = P.spec[k].exit_head;
-            T = P.spec[k].exit_T;
+        if (lane == 0) P.entry[k] = Entry{head, T};
+        Acc A;
+        if (P.struct_out)  // [start, head): members of an earlier segment's batch
+            for (uint64_t j = sg.start + lane; j < min(head, sg.end); j += 32) P.bmeta_bins[lo + j] = 0;
+        if (head < sg.end) {  // (else an earlier batch already covers this segment)
+            bool synced;
+            run_batches<RUN_RESOLVE>(P, d, head, T, sg.end, sg.start, &P.spec[k], synced, A, spo[warp], spd[warp],
+                                     sdk[warp], nullptr);
+            if (synced) {
+                if (P.struct_out) {  // from the sync point on, the speculative run's batches and counts
+                    const SpecOut& so = P.spec[k];
+                    const uint32_t rel = static_cast<uint32_t>(head - sg.start);
+                    const uint32_t nreg = min(so.nregen, static_cast<uint32_t>(kRegen));
+                    const uint32_t hit = __ballot_sync(FULL, lane < nreg && so.regen[lane] == rel);
+                    const uint32_t j = __ffs(hit) - 1;  // synced: the head is regen point j
+                    const bool suf = lane > j && lane <= static_cast<uint32_t>(kRegen);
+                    A.nbatch += warp_sum_u64(suf ? so.ib[lane] : 0u);
+                    A.max_need = max(A.max_need, warp_max_u64(suf ? so.ineed[lane] : 0ull));
+                    A.maxb = max(A.maxb, warp_max_u64(suf ? so.imaxb[lane] : 0u));
+                }
+                head = P.spec[k].exit_head;
+                T = P.spec[k].exit_T;
+            }
+        }
+        if (P.struct_out && lane == 0) {
+            Partial& q = P.part[k];
+            q.nbatch = A.nbatch;
+            q.max_need = A.max_need;
+            q.maxb = A.maxb;
+            q.t_end = T;
         }
     }
 }
@@ -1202,7 +1355,7 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
     if (head < sg.end)
         run_batches<RUN_FULL>(P, sg.dev, head, T, sg.end, sg.start, nullptr, synced, A, spo_w, spd_w, sdk_w, wreg);
     const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
-    const uint32_t fl = static_cast<uint32_t>(warp_max_u64(A.flags));
+    const uint32_t fl = __reduce_or_sync(FULL, A.flags);
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) {
         const uint64_t b0 = __shfl_xor_sync(FULL, A.acc[0], s);
@@ -1224,6 +1377,297 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
         q.flags = fl;
         q.t_end = T;
     }
+}
+
+constexpr uint32_t kLaneMax = 4;     // members a lane replays by itself in k_batch_stats
+constexpr uint32_t kHistWin = 4096;  // first-pass histogram bins per CTA in shared memory (8 binades)
+
+// The decode steps of up to 32 batches at once, one per lane, from their
+// recorded starts: a batch's timeline depends only on its members and its
+// start (engine.hpp:319-387), so batches replay independently.  Per step the
+// lane folds the alive members' durations in batch order, advances the
+// absolute time (now + d, the reference's f64 add) and post-processes the
+// sample: slow count and first slow step, the sample-bin range, histogram
+// runs (a lane adds a run's weight when its key changes), the exact sum
+// (telescoped when every step time lies in [now, 2 now], as the full pass).
+// Batches of more than kLaneMax members go through run_batches one at a time.
+__device__ __forceinline__ void hist_flush(const ReplayParams& P, uint32_t* shist, uint32_t key, uint64_t cnt) {
+    const uint32_t r = key - P.hwin_base;
+    if (r < P.hwin) atomicAdd(shist + r, static_cast<uint32_t>(cnt));
+    else atomicAdd(reinterpret_cast<unsigned long long*>(P.hist + key), static_cast<unsigned long long>(cnt));
+}
+
+template <bool SINGLE, bool ONEF>
+__device__ __forceinline__ void lane_batch(const ReplayParams& P, const colo_model& m, uint64_t lo, uint64_t qb,
+                                           uint32_t n, double start, bool idle, bool first_pass, Acc& A,
+                                           uint64_t* bins_rw, uint32_t* shist) {
+    // SINGLE: n == 1 (the loops over members and over the member ends drop
+    // out); ONEF: one histogram filter (the first pass)
+    constexpr uint32_t J = SINGLE ? 1u : kLaneMax;
+    const double gam = m.decode_coef_const, del = m.decode_coef_context;
+    const uint32_t* __restrict__ pp = P.p + lo;
+    const uint32_t* __restrict__ po = P.o + lo;
+    uint32_t oj[J];
+    double pd[J];
+    double dur = 0.0;
+    uint32_t maxo = 0;
+    uint64_t max_inc = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < J; ++j) {
+        const uint32_t pj = j < n ? pp[qb + j] : 0u;
+        oj[j] = j < n ? po[qb + j] : 0u;
+        pd[j] = static_cast<double>(pj);
+        if (j < n) {
+            dur += m.prefill_coef_linear * pd[j] + m.prefill_coef_quad * pd[j] * pd[j];  // engine.hpp:321-325
+            maxo = max(maxo, oj[j]);
+            max_inc = max(max_inc, static_cast<uint64_t>(pj) + oj[j]);
+        }
+    }
+    double now = start + dur;
+    const double span = static_cast<double>(maxo) *
+                        (static_cast<double>(n) * (gam + del * static_cast<double>(max_inc + maxo))) * 1.001;
+    const bool tele = now >= 0x1p-44 && span <= now && gam >= 0.0 && del >= 0.0;
+    if (tele) acc_fixed_sub(A.acc, A.flags, now, n);
+    const uint32_t nf = ONEF ? 1u : (P.hist ? P.nfilters : 0u);
+    constexpr uint32_t F = ONEF ? 1u : 3u;
+    uint32_t rkey[F];
+    uint32_t rcnt[F];
+#pragma unroll
+    for (uint32_t f = 0; f < F; ++f) {
+        rkey[f] = 0xffffffffu;
+        rcnt[f] = 0;
+    }
+    uint32_t first_slow = 0xffffffffu, bmin = 0xffffffffu, bmax = 0, nslow = 0;
+    uint64_t gen = 0;
+    double kd = 0.0;
+    for (uint32_t k = 0; k < maxo; ++k) {
+        double d = 0.0;
+        uint32_t alive = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < J; ++j)
+            if (SINGLE || (j < n && k < oj[j])) {
+                d += gam + del * (pd[j] + kd);  // cost_model.hpp:28-35, batch 1, in batch order
+                ++alive;
+            }
+        kd += 1.0;
+        const double nn = now + d;
+        const double s = nn - now;  // TPT sample of every alive member (engine.hpp:370-375)
+        now = nn;
+        gen += alive;
+        const bool sl = s > P.tau;
+        nslow += sl ? alive : 0u;
+        first_slow = sl ? min(first_slow, k) : first_slow;
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(s));
+        if (!(s < 0.0)) {
+            const uint32_t bn = static_cast<uint32_t>(bits >> 42);
+            bmin = min(bmin, bn);
+            bmax = max(bmax, bn);
+        }
+        if (nf) {
+            const uint64_t hb = bits >> P.filter_shift;
+            const uint32_t bin = static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1));
+#pragma unroll
+            for (uint32_t f = 0; f < F; ++f) {
+                const bool match = f < nf && hb == P.prefix[f];
+                const uint32_t key = f * COLO_HIST_BINS + bin;
+                const bool chg = match && key != rkey[f];
+                if (chg && rcnt[f]) hist_flush(P, shist, rkey[f], rcnt[f]);
+                rcnt[f] = chg ? alive : rcnt[f] + (match ? alive : 0u);
+                rkey[f] = chg ? key : rkey[f];
+            }
+        }
+        if (!tele) {
+            acc_fixed(A.acc, A.flags, s, alive);
+        } else if (!SINGLE) {
+#pragma unroll
+            for (uint32_t j = 0; j < J; ++j)
+                if (j < n && k + 1 == oj[j]) acc_fixed(A.acc, A.flags, now, 1u);  // + T_{o_j - 1}
+        }
+    }
+    if (SINGLE && tele) acc_fixed(A.acc, A.flags, now, 1u);  // + T_{o - 1}
+    A.gen += gen;
+    A.slow_tok += nslow;
+#pragma unroll
+    for (uint32_t f = 0; f < F; ++f)
+        if (rcnt[f]) hist_flush(P, shist, rkey[f], rcnt[f]);
+#pragma unroll
+    for (uint32_t j = 0; j < J; ++j)
+        if (j < n) {  // a query is slow iff one of its tokens is
+            const bool slowq = oj[j] > first_slow;
+            A.slow_q += slowq;
+            if (P.labels) P.labels[lo + qb + j] = slowq ? 1 : 0;
+        }
+    if (first_pass)
+        bins_rw[lo + qb] = (1ull << 63) | (idle ? 1ull << 62 : 0ull) | (static_cast<uint64_t>(bmax) << 21) | bmin;
+}
+
+// A batch of more than kLaneMax members: the warp replays it alone from its
+// start with run_batches (out of line: rare, and it keeps k_batch_stats'
+// register count to the lane path's)
+__device__ __noinline__ void big_batch(const ReplayParams& P, uint32_t d, uint64_t head, double T, uint64_t seg_start,
+                                       Acc& A, uint2* spo_w, double* spd_w, double* sdk_w, double* wreg) {
+    Acc B;
+    bool synced;
+    run_batches<RUN_FULL>(P, d, head, T, head + 1, seg_start, nullptr, synced, B, spo_w, spd_w, sdk_w, wreg);
+    A.gen += B.gen;
+    A.slow_tok += B.slow_tok;
+    A.slow_q += B.slow_q;
+    add3(A.acc, B.acc[0], B.acc[1], B.acc[2]);
+    A.flags |= B.flags;
+}
+
+// Post-processing of the first stats pass over the batches the speculative
+// and resolve passes recorded
+// (first_pass: every batch; bmeta gets each batch's sample-bin range), or of
+// a narrowing pass over the batches whose recorded range covers a filter bin.
+// One warp per replay segment takes the batches that start in it, queues them
+// in shared memory and replays them 32 at a time (lane_batch).
+__device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint32_t w, uint32_t warp, uint32_t lane,
+                                                    double* wreg, uint32_t* shist) {
+    // two queues per warp: single-member batches (the common case, replayed
+    // by a loop without the member loops) and the rest
+    __shared__ uint64_t qq[kWarps][2][64];
+    __shared__ double qs[kWarps][2][64];
+    __shared__ uint32_t qn[kWarps][2][64];
+    uint2* const spo_w = reinterpret_cast<uint2*>(wreg);
+    double* const spd_w = wreg + kStage;
+    double* const sdk_w = wreg + 2 * kStage;
+    const Seg sg = P.segs[w];
+    const uint32_t d = sg.dev;
+    const uint64_t lo = P.dev_off[d], N = P.dev_off[d + 1] - lo;
+    const colo_model& m = P.prof[P.dev_prof[d]].m;
+    const bool first_pass = P.sparse_bins == nullptr;
+    const bool onef = P.hist != nullptr && P.nfilters == 1;
+    const uint64_t* bins = first_pass ? P.bmeta_bins : P.sparse_bins;
+    const double* starts = first_pass ? P.bmeta_start : P.sparse_start;
+    uint64_t* const bins_rw = first_pass ? P.bmeta_bins : nullptr;
+    const uint32_t sh = 42 - P.filter_shift;  // filter prefix -> its top-21-bit bin
+    uint32_t fb[3];
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+        fb[f] = f < static_cast<int>(P.nfilters) ? static_cast<uint32_t>(P.prefix[f] >> sh) : 0xffffffffu;
+    Acc A;
+    uint32_t nq[2] = {0, 0};
+    auto process = [&](uint32_t qi, uint32_t cnt) {
+        const bool has = lane < cnt;
+        const uint64_t qb = has ? qq[warp][qi][lane] : 0ull;
+        const uint32_t n = has ? qn[warp][qi][lane] & 0x7fffffffu : 0u;
+        const bool idle = has && (qn[warp][qi][lane] >> 31);
+        const double st = has ? qs[warp][qi][lane] : 0.0;
+        if (qi == 0) {
+            if (has) {
+                if (onef) lane_batch<true, true>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                else lane_batch<true, false>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+            }
+        } else {
+            if (has && n <= kLaneMax) {
+                if (onef) lane_batch<false, true>(P, m, lo, qb, n, st, idle, first_pass, A, bins_rw, shist);
+                else lane_batch<false, false>(P, m, lo, qb, n, st, idle, first_pass, A, bins_rw, shist);
+            }
+            uint32_t big = __ballot_sync(FULL, has && n > kLaneMax);
+            while (big) {  // the warp together, one batch at a time (run_batches from its start)
+                const uint32_t l = __ffs(big) - 1;
+                big &= big - 1;
+                const uint64_t head = __shfl_sync(FULL, qb, l);
+                const bool idl = __shfl_sync(FULL, idle, l);
+                const double T = idl ? -INFINITY : __shfl_sync(FULL, st, l);
+                big_batch(P, d, head, T, sg.start, A, spo_w, spd_w, sdk_w, wreg);
+            }
+        }
+        __syncwarp();
+    };
+    for (uint64_t j0 = sg.start; j0 < sg.end; j0 += 32) {
+        const uint64_t q = j0 + lane;
+        const uint64_t bb = q < N ? bins[lo + q] : 0ull;
+        const bool stq = q >= N || (bb >> 63);  // a batch starts here (or the device ends)
+        const uint32_t smask = __ballot_sync(FULL, stq);
+        const bool mine = q < sg.end && q < N && (bb >> 63);
+        const uint32_t above = lane == 31 ? 0u : smask & (~0u << (lane + 1));
+        uint64_t far = 0;  // the first batch start past this chunk (for the batch that runs into it)
+        if (__any_sync(FULL, mine && above == 0)) {
+            for (uint64_t k0 = j0 + 32;; k0 += 32) {
+                const uint64_t qk = k0 + lane;
+                const uint32_t m2 = __ballot_sync(FULL, qk >= N || (bins[lo + qk] >> 63));
+                if (m2) {
+                    far = k0 + __ffs(m2) - 1;
+                    break;
+                }
+            }
+        }
+        const uint64_t end = above ? j0 + __ffs(above) - 1 : far;
+        bool sel = mine;
+        if (!first_pass && sel) {  // narrowing pass: only batches whose sample-bin range covers a filter bin
+            const uint32_t mn = static_cast<uint32_t>(bb & 0x1fffff), mx = static_cast<uint32_t>((bb >> 21) & 0x1fffff);
+            bool hit = false;
+#pragma unroll
+            for (int f = 0; f < 3; ++f) hit |= mn <= fb[f] && fb[f] <= mx;
+            sel = hit;
+        }
+#pragma unroll
+        for (uint32_t qi = 0; qi < 2; ++qi) {
+            const bool in = sel && ((end - q == 1) == (qi == 0));
+            const uint32_t sm = __ballot_sync(FULL, in);
+            if (in) {
+                const uint32_t pos = nq[qi] + __popc(sm & ((1u << lane) - 1));
+                qq[warp][qi][pos] = q;
+                qn[warp][qi][pos] = static_cast<uint32_t>(end - q) | (((bb >> 62) & 1ull) ? 0x80000000u : 0u);
+                qs[warp][qi][pos] = starts[lo + q];
+            }
+            nq[qi] += __popc(sm);
+            __syncwarp();
+            if (nq[qi] >= 32) {
+                process(qi, 32);
+                if (lane < nq[qi] - 32) {  // (reads [32, nq), writes [0, nq - 32): disjoint)
+                    const uint64_t a = qq[warp][qi][32 + lane];
+                    const uint32_t b = qn[warp][qi][32 + lane];
+                    const double c = qs[warp][qi][32 + lane];
+                    qq[warp][qi][lane] = a;
+                    qn[warp][qi][lane] = b;
+                    qs[warp][qi][lane] = c;
+                }
+                nq[qi] -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    if (nq[0]) process(0, nq[0]);
+    if (nq[1]) process(1, nq[1]);
+    if (first_pass) {
+        const uint64_t gen = warp_sum_u64(A.gen), slow_tok = warp_sum_u64(A.slow_tok), slow_q = warp_sum_u64(A.slow_q);
+        const uint32_t fl = __reduce_or_sync(FULL, A.flags);
+#pragma unroll
+        for (int s2 = 16; s2 > 0; s2 >>= 1) {
+            const uint64_t b0 = __shfl_xor_sync(FULL, A.acc[0], s2);
+            const uint64_t b1 = __shfl_xor_sync(FULL, A.acc[1], s2);
+            const uint64_t b2 = __shfl_xor_sync(FULL, A.acc[2], s2);
+            add3(A.acc, b0, b1, b2);
+        }
+        if (lane == 0) {
+            Partial& q = P.part[w];
+            q.gen = gen;
+            q.slow_tok = slow_tok;
+            q.slow_q = slow_q;
+            q.acc[0] = A.acc[0];
+            q.acc[1] = A.acc[1];
+            q.acc[2] = A.acc[2];
+            q.flags = fl;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_batch_stats(const __grid_constant__ ReplayParams P) {
+    extern __shared__ double stile[];  // per warp the run_batches region, then the CTA's histogram window
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t* const shist = reinterpret_cast<uint32_t*>(stile + kTileBytes / 8);
+    for (uint32_t i = threadIdx.x; i < P.hwin; i += blockDim.x) shist[i] = 0;
+    __syncthreads();
+    const uint32_t w = blockIdx.x * kWarps + warp;
+    if (w < P.nsegs) batch_stats_segment(P, w, warp, lane, stile + warp * (32 * 33), shist);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < P.hwin; i += blockDim.x)
+        if (shist[i])
+            atomicAdd(reinterpret_cast<unsigned long long*>(P.hist + P.hwin_base + i),
+                      static_cast<unsigned long long>(shist[i]));
 }
 
 // Narrowing stats passes over the batches of the first pass whose sample-bin
@@ -1829,9 +2273,16 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (opts->stats_mode == 2 && ctx->bmeta_valid && P.hist && !P.vstage && !P.bstage) {  // narrowing pass: only batches that can hit a filter bin
             P.sparse_start = static_cast<const double*>(ctx->d_bmeta);
             P.sparse_bins = reinterpret_cast<const uint64_t*>(static_cast<const double*>(ctx->d_bmeta) + n);
-            COLO_CK(ctx, cudaFuncSetAttribute(k_sparse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
-            COLO_LAUNCHED(ctx);
-            k_sparse_hist<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+            const char* bse = std::getenv("COLO_BATCH_STATS");
+            if (!(bse && bse[0] == '0')) {
+                COLO_CK(ctx, cudaFuncSetAttribute(k_batch_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+                COLO_LAUNCHED(ctx);
+                k_batch_stats<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+            } else {
+                COLO_CK(ctx, cudaFuncSetAttribute(k_sparse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+                COLO_LAUNCHED(ctx);
+                k_sparse_hist<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+            }
         } else {
             COLO_LAUNCHED(ctx);
             k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
@@ -1845,9 +2296,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (flag)
             return set_err(ctx, COLO_EVALIDATION,
                            "trace rejected: unsorted arrivals, zero tokens, or a query that cannot fit the device alone");
+        unsigned long long mctx_seen = 0;  // max p + o over the trace (k_validate)
         {  // decode-latency tables up to the trace's largest context
             unsigned long long mctx = 0;
             COLO_CK(ctx, cudaMemcpy(&mctx, P.maxctx, 8, cudaMemcpyDeviceToHost));
+            mctx_seen = mctx;
             P.dtab_n = 0;
             if (mctx > 0 && mctx < (1ull << 20)) {
                 const uint64_t tn = mctx + 1;
@@ -1880,6 +2333,13 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         cudaEvent_t ev[4];
         if (timing)
             for (auto& e : ev) cudaEventCreate(&e);
+        const char* bse = std::getenv("COLO_BATCH_STATS");
+        // first stats pass: the speculative and resolve passes also lay down the
+        // batch structure, and k_batch_stats replays every batch's decode steps
+        // from its start, many batches at once (no full replay pass)
+        const bool bstats = opts->stats_mode == 1 && P.bmeta_bins && !P.samples && !P.bstage && !P.vstage &&
+                            !(bse && bse[0] == '0');
+        P.struct_out = bstats ? 1u : 0u;
         if (timing) cudaEventRecord(ev[0], ctx->stream);
         COLO_LAUNCHED(ctx);
         k_speculate<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P);
@@ -1889,13 +2349,58 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (timing) cudaEventRecord(ev[1], ctx->stream);
         if (timing) {
             P.dbg = reinterpret_cast<unsigned long long*>(ctx->d_counters);
-            cudaMemsetAsync(ctx->d_counters, 0, 32, ctx->stream);
+            cudaMemsetAsync(ctx->d_counters, 0, 64, ctx->stream);
         }
         COLO_LAUNCHED(ctx);
         k_resolve<<<static_cast<uint32_t>(ndev), 32, 0, ctx->stream>>>(P);
         if (timing) cudaEventRecord(ev[2], ctx->stream);
-        COLO_LAUNCHED(ctx);
-        k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+        if (bstats) {
+            P.dbg = nullptr;
+            cudaEvent_t es = nullptr;
+            if (timing) {
+                cudaEventCreate(&es);
+                cudaEventRecord(es, ctx->stream);
+            }
+            // the first pass's histogram (bins = top 21 bits) gets a per-CTA window
+            // in shared memory from half the smallest decode-step constant up 8
+            // binades (TPT samples are at least about one step); u32 counts stay
+            // exact while a CTA's samples are below 2^32 (4 segments of at most
+            // 8192 queries, plus a straddling batch, times outputs < 2^16)
+            P.hwin = 0;
+            if (P.hist && P.nfilters == 1 && P.filter_shift == 63 && P.prefix[0] == 0 && P.hist_shift == 42 &&
+                mctx_seen > 0 && mctx_seen < (1ull << 16) && seg <= 8192) {
+                double g = models[0].decode_coef_const;
+                for (size_t i = 1; i < nprofiles; ++i) g = std::min(g, models[i].decode_coef_const);
+                const double lo_s = 0.5 * g;
+                uint64_t b = 0;
+                std::memcpy(&b, &lo_s, 8);
+                if (lo_s > 0.0 && std::isfinite(lo_s)) {
+                    P.hwin_base = static_cast<uint32_t>(b >> 42);
+                    P.hwin = kHistWin;
+                }
+            }
+            const size_t bs_smem = kTileBytes + P.hwin * 4u;
+            COLO_CK(ctx, cudaFuncSetAttribute(k_batch_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
+            COLO_LAUNCHED(ctx);
+            k_batch_stats<<<seg_blocks, kWarps * 32, bs_smem, ctx->stream>>>(P);
+            P.hwin = 0;
+            if (timing) {
+                cudaEvent_t ee;
+                cudaEventCreate(&ee);
+                cudaEventRecord(ee, ctx->stream);
+                cudaEventSynchronize(ee);
+                float x = 0, y = 0;
+                cudaEventElapsedTime(&x, ev[2], es);
+                cudaEventElapsedTime(&y, es, ee);
+                std::fprintf(stderr, "colo replay: (setup %.3f ms) batch stats %.3f ms\n", x, y);
+                cudaEventDestroy(es);
+                cudaEventDestroy(ee);
+            }
+        } else {
+            COLO_LAUNCHED(ctx);
+            k_replay_full<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+        }
+        P.dbg = nullptr;
         if (timing) {
             cudaEventRecord(ev[3], ctx->stream);
             cudaEventSynchronize(ev[3]);
@@ -1903,8 +2408,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             cudaEventElapsedTime(&a, ev[0], ev[1]);
             cudaEventElapsedTime(&b, ev[1], ev[2]);
             cudaEventElapsedTime(&c, ev[2], ev[3]);
-            unsigned long long hits[4] = {0, 0, 0, 0};
-            cudaMemcpy(hits, ctx->d_counters, 32, cudaMemcpyDeviceToHost);
+            unsigned long long hits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            cudaMemcpy(hits, ctx->d_counters, 64, cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "colo replay full pass: %llu idle-start queries in %llu windows, %llu other batches "
+                                 "(%llu queries)\n", hits[4], hits[5], hits[6], hits[7]);
             std::fprintf(stderr, "colo replay: %zu segments (len %llu), speculate %.3f ms, resolve %.3f ms (%llu fast "
                                  "[%llu by chain sums, %llu record windows] / %llu formed batches), replay %.3f ms\n",
                          ns, static_cast<unsigned long long>(seg), a, b, hits[0], hits[2], hits[3], hits[1], c);
