@@ -801,18 +801,18 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
         out["mean"] = None
         return out
     ranks = [nearest_rank_index(q, n) for q in quantiles]
-    h = hist.cpu().numpy()
+    sel = _select_dev(hist.view(1, HIST_BINS).expand(nf, HIST_BINS), ranks)
     prefixes = []
     for f in range(nf):
-        b, ranks[f] = _select(h, ranks[f])
+        b, ranks[f] = sel[f]
         prefixes.append(b)
     for fs, hs in ((42, 21), (21, 0)):
         hist, _ = run_pass(hs, fs, tuple(prefixes))
         if reduce is not None:
             reduce(hist)
-        hh = hist.cpu().numpy().reshape(nf, HIST_BINS)
+        sel = _select_dev(hist.view(nf, HIST_BINS), ranks)
         for f in range(nf):
-            b, ranks[f] = _select(hh[f], ranks[f])
+            b, ranks[f] = sel[f]
             prefixes[f] = (prefixes[f] << 21) | b
     for q, p in zip(quantiles, prefixes):
         out[f"p{int(round(q * 100))}"] = float(np.array([p], np.uint64).view(np.float64)[0])
@@ -823,13 +823,22 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
     return out
 
 
-def _select(h: np.ndarray, rank: int) -> Tuple[int, int]:
-    cum = np.cumsum(h.astype(np.int64))
-    b = int(np.searchsorted(cum, rank, side="left"))
-    if b >= len(h):
-        raise ColoError(_lib.COLO_EBREACH, "histogram pass lost samples")
-    before = int(cum[b - 1]) if b else 0
-    return b, rank - before
+def _select_dev(h, ranks) -> List[Tuple[int, int]]:
+    """_select for every row of an int64 histogram tensor [nf, bins] where it
+    lives (on the GPU: a cumulative sum and a search, two words per row back
+    to the host instead of the histogram)."""
+    torch = _torch()
+    cum = torch.cumsum(h, dim=1)
+    rk = torch.tensor(ranks, dtype=torch.int64, device=h.device).view(-1, 1)
+    b = torch.searchsorted(cum, rk, right=False)  # first bin with cum >= rank
+    before = torch.where(b > 0, cum.gather(1, (b - 1).clamp(min=0)), torch.zeros_like(b))
+    res = torch.cat([b, before], dim=1).cpu().tolist()
+    out = []
+    for (bi, bf), r in zip(res, ranks):
+        if bi >= h.shape[1]:
+            raise ColoError(_lib.COLO_EBREACH, "histogram pass lost samples")
+        out.append((int(bi), int(r - bf)))
+    return out
 
 
 def serving_stats_c(ctx: Context, profiles, arrival, prompt, output, dev_offsets, dev_profile, tau=math.inf):

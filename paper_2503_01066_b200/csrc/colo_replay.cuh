@@ -8,10 +8,10 @@ namespace colo {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
-__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-    for (int s = 16; s > 0; s >>= 1) v = max(v, __shfl_xor_sync(kFullMask, v, s));
-    return v;
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {  // two 32-bit warp reductions (REDUX)
+    const uint32_t hi = __reduce_max_sync(kFullMask, static_cast<uint32_t>(v >> 32));
+    const uint32_t lo = __reduce_max_sync(kFullMask, static_cast<uint32_t>(v >> 32) == hi ? static_cast<uint32_t>(v) : 0u);
+    return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
 __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {

@@ -676,13 +676,10 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 sPO[j - head] = make_uint2(pj, oj);
                 sPD[j - head] = static_cast<double>(pj);
             }
-            max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
-            maxo = max(maxo, static_cast<uint32_t>(warp_max_u64(ok ? oj : 0u)));
-            if (MODE == RUN_FULL) {
-                uint32_t mo = ok ? oj : 0xffffffffu;
-#pragma unroll
-                for (int s2 = 16; s2 > 0; s2 >>= 1) mo = min(mo, __shfl_xor_sync(FULL, mo, s2));
-                mino = min(mino, mo);
+            maxo = max(maxo, __reduce_max_sync(FULL, ok ? oj : 0u));
+            if (MODE == RUN_FULL) {  // (the other passes only need the batch's extent and step count)
+                max_inc = max(max_inc, warp_max_u64(ok ? static_cast<uint64_t>(pj) + oj : 0ull));
+                mino = min(mino, __reduce_min_sync(FULL, ok ? oj : 0xffffffffu));
             }
             if (cnt) need_total = __shfl_sync(FULL, incl, cnt - 1);
             end += cnt;
@@ -1501,6 +1498,93 @@ __device__ __forceinline__ void lane_batch(const ReplayParams& P, const colo_mod
         bins_rw[lo + qb] = (1ull << 63) | (idle ? 1ull << 62 : 0ull) | (static_cast<uint64_t>(bmax) << 21) | bmin;
 }
 
+// lane_batch for a single-member batch in the first stats pass (histogram
+// key = the sample's top 21 bits = its bmeta bin) when the step constant is
+// positive (validate_profile_pair), so every step duration is positive:
+// 0.0 + x == x, every sample is >= 0 and matches the first pass's filter.
+// Telescoping sums only; other batches take lane_batch.
+__device__ __forceinline__ bool lane_single_p1(const ReplayParams& P, const colo_model& m, uint64_t lo, uint64_t qb,
+                                               double start, bool idle, Acc& A, uint64_t* bins_rw, uint32_t* shist) {
+    const double gam = m.decode_coef_const, del = m.decode_coef_context;
+    const uint32_t pj = P.p[lo + qb], o = P.o[lo + qb];
+    const double pd = static_cast<double>(pj);
+    double now = start + (0.0 + (m.prefill_coef_linear * pd + m.prefill_coef_quad * pd * pd));  // engine.hpp:321-325
+    const double span = static_cast<double>(o) * (gam + del * static_cast<double>(static_cast<uint64_t>(pj) + o + o)) * 1.001;
+    if (!(now >= 0x1p-44 && span <= now)) return false;  // the sum would not telescope
+    acc_fixed_sub(A.acc, A.flags, now, 1u);
+    uint32_t first_slow = 0xffffffffu, bmin = 0xffffffffu, bmax = 0, nslow = 0, rkey = 0xffffffffu, rcnt = 0;
+    double x = pd;  // pd + k, exact
+#pragma unroll 2
+    for (uint32_t k = 0; k < o; ++k) {
+        const double d = gam + del * x;  // cost_model.hpp:28-35 (batch 1) = 0.0 + d
+        x += 1.0;
+        const double nn = now + d;
+        const double s = nn - now;  // >= 0: TPT sample (engine.hpp:370-375)
+        now = nn;
+        const bool sl = s > P.tau;
+        nslow += sl;
+        first_slow = (sl && first_slow == 0xffffffffu) ? k : first_slow;
+        const uint32_t bn = static_cast<uint32_t>(__double2hiint(s)) >> 10;  // bits >> 42
+        bmin = min(bmin, bn);
+        bmax = max(bmax, bn);
+        if (bn != rkey) {
+            if (rcnt) hist_flush(P, shist, rkey, rcnt);
+            rkey = bn;
+            rcnt = 0;
+        }
+        ++rcnt;
+    }
+    if (rcnt) hist_flush(P, shist, rkey, rcnt);
+    acc_fixed(A.acc, A.flags, now, 1u);  // + T_{o - 1}
+    A.gen += o;
+    A.slow_tok += nslow;
+    const bool slowq = o > first_slow;
+    A.slow_q += slowq;
+    if (P.labels) P.labels[lo + qb] = slowq ? 1 : 0;
+    bins_rw[lo + qb] = (1ull << 63) | (idle ? 1ull << 62 : 0ull) | (static_cast<uint64_t>(bmax) << 21) | bmin;
+    return true;
+}
+
+// lane_batch for a single-member batch in a narrowing pass (only its
+// samples whose high bits match a filter prefix feed the histogram; no other
+// output), under the same positive-step-constant condition as lane_single_p1.
+__device__ __forceinline__ void lane_single_narrow(const ReplayParams& P, const colo_model& m, uint64_t lo,
+                                                   uint64_t qb, double start) {
+    const double gam = m.decode_coef_const, del = m.decode_coef_context;
+    const uint32_t pj = P.p[lo + qb], o = P.o[lo + qb];
+    const double pd = static_cast<double>(pj);
+    double now = start + (0.0 + (m.prefill_coef_linear * pd + m.prefill_coef_quad * pd * pd));  // engine.hpp:321-325
+    const uint32_t nf = P.nfilters;
+    const uint64_t pre0 = P.prefix[0], pre1 = nf > 1 ? P.prefix[1] : ~0ull, pre2 = nf > 2 ? P.prefix[2] : ~0ull;
+    uint32_t rkey = 0xffffffffu, rcnt = 0;
+    double x = pd;
+#pragma unroll 2
+    for (uint32_t k = 0; k < o; ++k) {
+        const double d = gam + del * x;  // = 0.0 + d (d > 0)
+        x += 1.0;
+        const double nn = now + d;
+        const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(nn - now));
+        now = nn;
+        const uint64_t top = bits >> P.filter_shift;
+        if (top == pre0 || top == pre1 || top == pre2) {
+            const uint32_t bin = static_cast<uint32_t>((bits >> P.hist_shift) & (COLO_HIST_BINS - 1));
+#pragma unroll
+            for (uint32_t f = 0; f < 3; ++f) {
+                if (f < nf && top == P.prefix[f]) {
+                    const uint32_t key = f * COLO_HIST_BINS + bin;
+                    if (key != rkey) {
+                        if (rcnt) atomicAdd(reinterpret_cast<unsigned long long*>(P.hist + rkey), static_cast<unsigned long long>(rcnt));
+                        rkey = key;
+                        rcnt = 0;
+                    }
+                    ++rcnt;
+                }
+            }
+        }
+    }
+    if (rcnt) atomicAdd(reinterpret_cast<unsigned long long*>(P.hist + rkey), static_cast<unsigned long long>(rcnt));
+}
+
 // A batch of more than kLaneMax members: the warp replays it alone from its
 // start with run_batches (out of line: rare, and it keeps k_batch_stats'
 // register count to the lane path's)
@@ -1538,6 +1622,11 @@ __device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint3
     const colo_model& m = P.prof[P.dev_prof[d]].m;
     const bool first_pass = P.sparse_bins == nullptr;
     const bool onef = P.hist != nullptr && P.nfilters == 1;
+    // the first pass's shape: one filter on the sign bit, bins = top 21 bits
+    const bool p1 = first_pass && onef && P.filter_shift == 63 && P.prefix[0] == 0 && P.hist_shift == 42 &&
+                    m.decode_coef_const > 0.0 && m.decode_coef_context >= 0.0;
+    // a narrowing pass: only the histogram (no labels, counts or records)
+    const bool pn = !first_pass && P.hist && !P.labels && m.decode_coef_const > 0.0 && m.decode_coef_context >= 0.0;
     const uint64_t* bins = first_pass ? P.bmeta_bins : P.sparse_bins;
     const double* starts = first_pass ? P.bmeta_start : P.sparse_start;
     uint64_t* const bins_rw = first_pass ? P.bmeta_bins : nullptr;
@@ -1556,8 +1645,14 @@ __device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint3
         const double st = has ? qs[warp][qi][lane] : 0.0;
         if (qi == 0) {
             if (has) {
-                if (onef) lane_batch<true, true>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
-                else lane_batch<true, false>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                if (pn) {
+                    lane_single_narrow(P, m, lo, qb, st);
+                } else if (p1 && lane_single_p1(P, m, lo, qb, st, idle, A, bins_rw, shist)) {
+                } else if (onef) {
+                    lane_batch<true, true>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                } else {
+                    lane_batch<true, false>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                }
             }
         } else {
             if (has && n <= kLaneMax) {
@@ -2211,9 +2306,11 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
     P.entry = reinterpret_cast<Entry*>(base + o_entry);
     P.part = reinterpret_cast<Partial*>(base + o_part);
     P.seg_base = reinterpret_cast<uint64_t*>(base + o_base);
-    if (ns)
-        COLO_CK(ctx, cudaMemcpyAsync(base + o_segs, segs.data(), ns * sizeof(Seg), cudaMemcpyHostToDevice, ctx->stream));
-    COLO_CK(ctx, cudaMemcpyAsync(base + o_dseg, dev_seg.data(), (ndev + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (!reuse) {  // (a reuse pass has exactly these segments in place)
+        if (ns)
+            COLO_CK(ctx, cudaMemcpyAsync(base + o_segs, segs.data(), ns * sizeof(Seg), cudaMemcpyHostToDevice, ctx->stream));
+        COLO_CK(ctx, cudaMemcpyAsync(base + o_dseg, dev_seg.data(), (ndev + 1) * 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
     if (want_batches) {
         P.bstage = reinterpret_cast<colo_batch*>(base + o_bstage);
         P.bflag = base + o_bflag;
