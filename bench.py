@@ -746,6 +746,18 @@ C4_SEED = 4040
 C4_CHUNK = 128  # devices per chunk context (1B queries): one rank's 8-GPU share
 
 
+def profile_one_step(torch, step):
+    """COLO_PROFILE_STEP=1: one extra, untimed step between cudaProfilerStart /
+    Stop, so `ncu --profile-from-start off` sees exactly one step's kernels
+    (profiles/step_inst.py turns that capture into the issue-rate roofline)."""
+    if os.environ.get("COLO_PROFILE_STEP"):
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+
+
 def issue_roofline(kind: str, step_s: float, clk: dict, queries: int) -> dict:
     """Issue-rate roofline of a replay step: the warp instructions one step
     executes (smsp__inst_executed.sum summed over the step's kernels, from the
@@ -826,6 +838,7 @@ def c4_measure(args, world, rank, local, dist, devices_cap, steps, warmup, cpu=F
     if dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    profile_one_step(torch, step)
     with ClockSampler(local) as clk:
         l0 = sum(p[0].launches() for p in parts)
         ev0.record()
@@ -942,6 +955,7 @@ def c3_measure(args, world, rank, local, dist, steps, warmup, cpu=False):
     if dist:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    profile_one_step(torch, step)
     with ClockSampler(local) as clk:
         l0 = ctx.launches()
         ev0.record()

@@ -801,7 +801,7 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
         out["mean"] = None
         return out
     ranks = [nearest_rank_index(q, n) for q in quantiles]
-    sel = _select_dev(hist.view(1, HIST_BINS).expand(nf, HIST_BINS), ranks)
+    sel = _select_dev(hist.view(1, HIST_BINS).expand(nf, HIST_BINS).contiguous(), ranks)
     prefixes = []
     for f in range(nf):
         b, ranks[f] = sel[f]
@@ -824,18 +824,25 @@ def stats_protocol(run_pass, reduce=None, quantiles=(0.50, 0.90, 0.99)):
 
 
 def _select_dev(h, ranks) -> List[Tuple[int, int]]:
-    """_select for every row of an int64 histogram tensor [nf, bins] where it
-    lives (on the GPU: a cumulative sum and a search, two words per row back
-    to the host instead of the histogram)."""
+    """For every row of an int64 histogram tensor [nf, bins] (bins a multiple
+    of 1024), the first bin whose cumulative count reaches the row's rank and
+    the rank inside it, computed where the histogram lives: block sums of 1024
+    bins, their prefix, then the prefix inside the one block; two words per
+    row come back to the host instead of the histogram."""
     torch = _torch()
-    cum = torch.cumsum(h, dim=1)
+    nf, nb = h.shape
+    hb = h.reshape(nf, nb // 1024, 1024)
+    csum = torch.cumsum(hb.sum(dim=2), dim=1)  # [nf, nb/1024]
     rk = torch.tensor(ranks, dtype=torch.int64, device=h.device).view(-1, 1)
-    b = torch.searchsorted(cum, rk, right=False)  # first bin with cum >= rank
-    before = torch.where(b > 0, cum.gather(1, (b - 1).clamp(min=0)), torch.zeros_like(b))
-    res = torch.cat([b, before], dim=1).cpu().tolist()
+    blk = torch.searchsorted(csum, rk, right=False).clamp(max=nb // 1024 - 1)  # first block reaching the rank
+    base = torch.where(blk > 0, csum.gather(1, (blk - 1).clamp(min=0)), torch.zeros_like(blk))
+    inner = torch.cumsum(hb[torch.arange(nf, device=h.device), blk.view(-1)], dim=1) + base  # [nf, 1024]
+    b = torch.searchsorted(inner, rk, right=False)
+    before = torch.where(b > 0, inner.gather(1, (b - 1).clamp(min=0)), base)
+    res = torch.cat([blk * 1024 + b, before, inner[:, -1:]], dim=1).cpu().tolist()
     out = []
-    for (bi, bf), r in zip(res, ranks):
-        if bi >= h.shape[1]:
+    for (bi, bf, last), r in zip(res, ranks):
+        if bi >= nb or last < r:
             raise ColoError(_lib.COLO_EBREACH, "histogram pass lost samples")
         out.append((int(bi), int(r - bf)))
     return out
