@@ -1377,7 +1377,11 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
 }
 
 constexpr uint32_t kLaneMax = 4;     // members a lane replays by itself in k_batch_stats
-constexpr uint32_t kHistWin = 4096;  // first-pass histogram bins per CTA in shared memory (8 binades)
+constexpr uint32_t kHistWin = 2048;  // first-pass histogram bins per CTA in shared memory (4 binades)
+// k_batch_stats' per-warp region for run_batches on a queued batch (member
+// stage, step durations, alive counts; never the idle-start tile: a queued
+// batch starts at or after every member's arrival)
+constexpr int kBsWarpBytes = (2 * kStage + 128) * 8 + 128 * 4;
 
 // The decode steps of up to 32 batches at once, one per lane, from their
 // recorded starts: a batch's timeline depends only on its members and its
@@ -1590,6 +1594,10 @@ __device__ __forceinline__ void lane_single_narrow(const ReplayParams& P, const 
 // register count to the lane path's)
 __device__ __noinline__ void big_batch(const ReplayParams& P, uint32_t d, uint64_t head, double T, uint64_t seg_start,
                                        Acc& A, uint2* spo_w, double* spd_w, double* sdk_w, double* wreg) {
+    if (!(P.arr[P.dev_off[d] + head] <= T)) {  // (cannot happen: the region has no idle-start tile)
+        if ((threadIdx.x & 31) == 0) atomicOr(P.err, 2);
+        return;
+    }
     Acc B;
     bool synced;
     run_batches<RUN_FULL>(P, d, head, T, head + 1, seg_start, nullptr, synced, B, spo_w, spd_w, sdk_w, wreg);
@@ -1753,11 +1761,11 @@ __device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint3
 __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_batch_stats(const __grid_constant__ ReplayParams P) {
     extern __shared__ double stile[];  // per warp the run_batches region, then the CTA's histogram window
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t* const shist = reinterpret_cast<uint32_t*>(stile + kTileBytes / 8);
+    uint32_t* const shist = reinterpret_cast<uint32_t*>(stile + kWarps * kBsWarpBytes / 8);
     for (uint32_t i = threadIdx.x; i < P.hwin; i += blockDim.x) shist[i] = 0;
     __syncthreads();
     const uint32_t w = blockIdx.x * kWarps + warp;
-    if (w < P.nsegs) batch_stats_segment(P, w, warp, lane, stile + warp * (32 * 33), shist);
+    if (w < P.nsegs) batch_stats_segment(P, w, warp, lane, stile + warp * (kBsWarpBytes / 8), shist);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < P.hwin; i += blockDim.x)
         if (shist[i])
@@ -2372,9 +2380,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             P.sparse_bins = reinterpret_cast<const uint64_t*>(static_cast<const double*>(ctx->d_bmeta) + n);
             const char* bse = std::getenv("COLO_BATCH_STATS");
             if (!(bse && bse[0] == '0')) {
-                COLO_CK(ctx, cudaFuncSetAttribute(k_batch_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
+                COLO_CK(ctx, cudaFuncSetAttribute(k_batch_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kWarps * kBsWarpBytes));
                 COLO_LAUNCHED(ctx);
-                k_batch_stats<<<seg_blocks, kWarps * 32, kTileBytes, ctx->stream>>>(P);
+                k_batch_stats<<<seg_blocks, kWarps * 32, kWarps * kBsWarpBytes, ctx->stream>>>(P);
             } else {
                 COLO_CK(ctx, cudaFuncSetAttribute(k_sparse_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileBytes));
                 COLO_LAUNCHED(ctx);
@@ -2459,7 +2468,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
                 cudaEventRecord(es, ctx->stream);
             }
             // the first pass's histogram (bins = top 21 bits) gets a per-CTA window
-            // in shared memory from half the smallest decode-step constant up 8
+            // in shared memory from half the smallest decode-step constant up 4
             // binades (TPT samples are at least about one step); u32 counts stay
             // exact while a CTA's samples are below 2^32 (4 segments of at most
             // 8192 queries, plus a straddling batch, times outputs < 2^16)
@@ -2476,7 +2485,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
                     P.hwin = kHistWin;
                 }
             }
-            const size_t bs_smem = kTileBytes + P.hwin * 4u;
+            const size_t bs_smem = kWarps * kBsWarpBytes + P.hwin * 4u;
             COLO_CK(ctx, cudaFuncSetAttribute(k_batch_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs_smem));
             COLO_LAUNCHED(ctx);
             k_batch_stats<<<seg_blocks, kWarps * 32, bs_smem, ctx->stream>>>(P);
@@ -2533,7 +2542,10 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         k_vseg_emit<<<seg_blocks, kWarps * 32, 0, ctx->stream>>>(P, vs);
     }
     COLO_CK(ctx, cudaGetLastError());
+    int late = 0;
+    COLO_CK(ctx, cudaMemcpyAsync(&late, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (late) return set_err(ctx, COLO_EBREACH, "replay: internal consistency check failed");
     std::memcpy(ctx->rs_sig, sig, sizeof sig);
     ctx->rs_valid = true;
     if (!reuse) ctx->bmeta_valid = P.bmeta_bins != nullptr;  // records of exactly this replay
