@@ -45,6 +45,7 @@ namespace {
 constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
+constexpr double kSpecGiveUp = 900.0;  // s of queueing after which a speculative run without idle starts stops
 constexpr int kSatHdr = 4;   // per all-queued record: its chain sums in 4 candidate binades (k_sat_durations)
 #ifndef COLO_REPLAY_BLOCKS
 #define COLO_REPLAY_BLOCKS 5
@@ -651,6 +652,16 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 }
                 if (progressed) continue;
             }
+            if (MODE == RUN_SPEC && ridx <= 1 && T - ah > kSpecGiveUp) {
+                // A deep backlog and no idle start since the segment's first query:
+                // the speculative run stops and drops its regeneration points, so
+                // the resolve pass replays this segment itself (at saturation
+                // through the all-queued records) instead of waiting for the
+                // queue to drain here
+                ridx = 0;
+                head = stop;
+                break;
+            }
             if (MODE == RUN_RESOLVE && P.dbg && lane == 0) atomicAdd(P.dbg + 1, 1ull);
             tail_ptr = find_tail(arr, N, tail_ptr < head ? head : tail_ptr, T);
             tail = tail_ptr;
@@ -1132,6 +1143,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
             needs += serving_memory(m, static_cast<uint64_t>(pj) + oj, 1);
         }
         maxo = static_cast<uint32_t>(warp_max_u64(maxo));
+        uint32_t mino = 0xffffffffu;
+        for (uint64_t j = lane; j < nb; j += 32) mino = min(mino, staged ? sPO[j].y : po[head + j]);
+        mino = __reduce_min_sync(FULL, mino);
         needs = warp_sum_u64(needs);
         double* dk = P.sat_dk + doff;
         double first[4] = {0.0, 0.0, 0.0, 0.0};  // steps 0..127 (lane = step mod 32)
@@ -1141,7 +1155,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
             double kd[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
-            if (staged && tab_ok) {
+            if (staged && tab_ok && k0 + 128 <= mino) {  // every member alive at every step of the window
+                const double* __restrict__ dt = P.dtab[pi] + kb;
+#pragma unroll 4
+                for (uint64_t j = 0; j < nb; ++j) {
+                    const uint32_t pj = sPO[j].x;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[r] += dt[pj + 32 * r];
+                }
+            } else if (staged && tab_ok) {
                 const double* __restrict__ dt = P.dtab[pi] + kb;
 #pragma unroll 4
                 for (uint64_t j = 0; j < nb; ++j) {
