@@ -162,6 +162,96 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
     if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
+// Sweep-size grids whose byte cells exceed shared memory (C5 step 50: 161 x
+// 160 x 10 = 257,600 cells): the cells are packed five 6-bit codes per word
+// (codes are 0, 1 or 2 + n <= L + 2 < 64) into 206 KB of shared memory, built
+// by each CTA from the byte cells, so every lookup stays on the SM instead of
+// gathering through L1/L2.  The stream bit of each cached bucket (cell
+// (ci, 0, 0)) gets a byte table of its own: those cells sit I*B apart, which
+// would put a warp's packed-word reads in a few banks.  One 1024-thread CTA per
+// SM streams the tuples with four loads in flight per thread; the
+// composition is compose32_fast's.
+constexpr int kPackThreads = 1024;
+#ifndef COLO_PACK_FROM
+#define COLO_PACK_FROM (96 * 1024)
+#endif
+constexpr size_t kPackFrom = COLO_PACK_FROM;  // byte-cell tables above this size take the packed kernel
+
+__device__ __forceinline__ uint32_t packed_cell(const uint32_t* pk, uint32_t idx) {
+    const uint32_t w = __umulhi(idx, 0xCCCCCCCDu) >> 2;  // idx / 5
+    return (pk[w] >> (6u * (idx - 5u * w))) & 63u;
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kPackThreads, 1) k_decide_packed(const __grid_constant__ DecideParams P) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const MapView& mv = P.mv;
+    const uint32_t ncells = mv.off_bytes, nw = (ncells + 4) / 5;
+    uint32_t* pk = reinterpret_cast<uint32_t*>(sm);
+    uint8_t* hed = sm + ((nw * 4 + 15u) & ~15u);
+    uint8_t* sbit = hed + ((mv.hed_bytes + 15u) & ~15u);  // [C] cell (ci, 0, 0) == AllToHost
+    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
+        uint32_t word = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < 5; ++r) {
+            const uint32_t i = 5 * w + r;
+            if (i < ncells) word |= static_cast<uint32_t>(__ldg(mv.off + i)) << (6 * r);
+        }
+        pk[w] = word;
+    }
+    for (uint32_t i = threadIdx.x; i < mv.hed_bytes; i += blockDim.x) hed[i] = mv.hed[i];
+    for (uint32_t ci = threadIdx.x; ci < mv.C; ci += blockDim.x) sbit[ci] = __ldg(mv.off + ci * mv.I * mv.B) == 1;
+    __syncthreads();
+    const FastMap f{mv.max_c, mv.max_i, mv.max_b, mv.hmax, mv.L, mv.I, mv.B, mv.fc.c_lo, mv.fc.c_hi, mv.fi.c_lo,
+                    mv.fi.c_hi, mv.fb.c_lo, mv.fb.c_hi, mv.fc.d, mv.fi.d, mv.fb.d};
+    uint32_t cnt[COLO_NCOUNTERS] = {};
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    constexpr int U = 4;
+    const uint64_t wbase = tid & ~uint64_t(31);  // warp-uniform trip count
+    for (uint64_t base = tid, wb = wbase; wb < P.n; base += stride * U, wb += stride * U) {
+        uint4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * stride;
+            t[u] = i < P.n ? __ldcs(P.in + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * stride;
+            // compose32_fast with the cell read from the packed words
+            const uint32_t c = t[u].x, inc = t[u].y, b = t[u].w & 0xffffu, pend = (t[u].w >> 16) & 0xffu,
+                           dev = t[u].w >> 24;
+            const bool oor = (c > f.max_c) | (inc - 1u >= f.max_i) | (b - 1u >= f.max_b);  // maps.hpp:105-107
+            const uint32_t ci = fdiv(min(c, f.max_c) + f.dc - 1u, f.cc_lo, f.cc_hi);
+            const uint32_t ii = fdiv(min(inc - 1u, f.max_i - 1u) + f.di, f.ci_lo, f.ci_hi) - 1u;
+            const uint32_t bi = fdiv(min(b - 1u, f.max_b - 1u) + f.db, f.cb_lo, f.cb_hi) - 1u;
+            uint32_t code = packed_cell(pk, (ci * f.I + ii) * f.B + bi);
+            code = oor ? 1u : code;  // engine.hpp:517-521
+            const bool a2h = code == 1;
+            const uint32_t layers = code >= 2 ? code - 2 : 0u;
+            const uint32_t free_now = a2h ? dev : min(layers, dev);
+            const uint32_t total = min(pend + (a2h ? f.L : layers), f.L);
+            const bool hoor = (c - 1u >= f.hmax);
+            const bool forced = oor | hoor;
+            const uint32_t hbit = hed[forced ? 0u : (ci - 1u) * (f.L + 1) + total];
+            const uint32_t recompute = forced ? 1u : hbit;
+            uint32_t v = (a2h ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS) | (layers << 2) | (free_now << 10) |
+                         (recompute << 18) | (oor ? COLO_V_OFFLOAD_OOR : 0u) | ((!oor & hoor) ? COLO_V_HEDGE_OOR : 0u) |
+                         ((COLO_VD_FREE_LOADBACK + recompute) << 21);
+            v = code == 0 ? 0u : v;
+            // admit_to_store's stream bit: lookup(charged, 1, 1) (engine.hpp:437-444)
+            const uint32_t ch = t[u].z;
+            const bool soor = ch > f.max_c;
+            const uint32_t sb = sbit[fdiv(min(ch, f.max_c) + f.dc - 1u, f.cc_lo, f.cc_hi)];
+            v |= soor ? (COLO_V_STREAM | COLO_V_STREAM_OOR) : (sb ? COLO_V_STREAM : 0u);
+            if (i < P.n) __stcs(P.out + i, v);
+            if (COUNT) count_warp(v, i < P.n, cnt);
+        }
+    }
+    if (COUNT) flush_warp_counters(cnt, P.counters);
+}
+
 // Tuple stream through a TMA pipeline: each CTA streams 16-KB tiles of tuples
 // into shared memory kStages tiles ahead with cp.async.bulk (one elected
 // thread, mbarrier completion), so the compute never waits on DRAM and needs
@@ -703,6 +793,20 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
     P.counters = d_counters;
     const size_t smem = ((P.mv.off_bytes + 15u) & ~15u) + P.mv.hed_bytes;
     const bool use_smem = smem <= 96 * 1024;
+    const bool fastgrid = P.mv.hsame && P.mv.fc.d > 1 && P.mv.fi.d > 1 && P.mv.fb.d > 1;
+    const size_t packed = ((((P.mv.off_bytes + 4u) / 5u) * 4u + 15u) & ~size_t(15)) + ((P.mv.hed_bytes + 15u) & ~15u) +
+                          P.mv.C;
+    if (smem > kPackFrom && fastgrid && P.mv.L + 2 < 64 && packed <= 220 * 1024) {  // packed cells in shared memory
+        const void* fn = d_counters ? (const void*)k_decide_packed<true> : (const void*)k_decide_packed<false>;
+        COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)packed));
+        int blocks = blocks_for(ctx, fn, kPackThreads, packed);
+        const uint64_t need_blocks = (n + kPackThreads - 1) / kPackThreads;
+        if (static_cast<uint64_t>(blocks) > need_blocks) blocks = static_cast<int>(need_blocks);
+        void* args[] = {&P};
+        COLO_LAUNCHED(ctx);
+        COLO_CK(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kPackThreads), args, packed, stream));
+        return COLO_OK;
+    }
     if (use_smem && !(reinterpret_cast<uintptr_t>(d_in) & 15u)) {  // TMA pipeline
         // 4 stages while the cells are small; 2 for sweep-size grids, so two
         // CTAs still fit next to 64 KB of cells
