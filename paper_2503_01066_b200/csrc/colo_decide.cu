@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
 // composition is compose32_fast's.
 constexpr int kPackThreads = 1024;
 #ifndef COLO_PACK_FROM
-#define COLO_PACK_FROM (96 * 1024)
+#define COLO_PACK_FROM (32 * 1024)
 #endif
 constexpr size_t kPackFrom = COLO_PACK_FROM;  // byte-cell tables above this size take the packed kernel
 
