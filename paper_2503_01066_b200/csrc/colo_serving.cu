@@ -1156,12 +1156,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
 #pragma unroll
             for (int r = 0; r < 4; ++r) kd[r] = static_cast<double>(kb + 32 * r);
             if (staged && tab_ok && k0 + 128 <= mino) {  // every member alive at every step of the window
+                // two steps from the table, two computed (the same f64 value: dtab[x] =
+                // gamma + delta * (double)x and (double)p + (double)k == (double)(p + k)),
+                // so L1 and the f64 pipe share the fold
                 const double* __restrict__ dt = P.dtab[pi] + kb;
 #pragma unroll 4
                 for (uint64_t j = 0; j < nb; ++j) {
                     const uint32_t pj = sPO[j].x;
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc[r] += dt[pj + 32 * r];
+                    const double pdj = sPD[j];
+                    acc[0] += dt[pj];
+                    acc[1] += dt[pj + 32];
+                    acc[2] += gam + del * (pdj + kd[2]);
+                    acc[3] += gam + del * (pdj + kd[3]);
                 }
             } else if (staged && tab_ok) {
                 const double* __restrict__ dt = P.dtab[pi] + kb;
