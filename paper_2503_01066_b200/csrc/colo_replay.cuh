@@ -85,15 +85,15 @@ __device__ __forceinline__ double pow2i(int k) {  // k in [-1022, 1023]
     return __longlong_as_double(static_cast<long long>(static_cast<uint64_t>(k + 1023) << 52));
 }
 // RN_u(x) / u for u = 1/sc (a power of two): false on a tie, a negative / NaN
-// x, or a result >= 2^53 (x*sc is exact: callers keep sc in [2^-60, 2^260]
-// and x either 0 or >= 2^-700)
+// x, or a result >= 2^51 (x*sc is exact: callers keep sc in [2^-60, 2^260]
+// and x either 0 or >= 2^-700).  Adding 2^52 rounds x*sc to an integer (the
+// f64 spacing there is 1) whose value is the low mantissa bits.
 __device__ __forceinline__ bool rn_units(double x, double sc, uint64_t& r) {
     const double xs = x * sc;
-    if (!(xs < 9007199254740992.0) || !(x >= 0.0) || (x != 0.0 && x < 0x1p-700)) return false;
-    const uint64_t fl = __double2ull_rd(xs);
-    const double fr = xs - static_cast<double>(fl);  // exact below 2^53
-    r = fl + (fr > 0.5 ? 1u : 0u);
-    return fr != 0.5;
+    if (!(xs < 2251799813685248.0) || !(x >= 0.0) || (x != 0.0 && x < 0x1p-700)) return false;
+    const double t = xs + 4503599627370496.0;
+    r = static_cast<uint64_t>(__double_as_longlong(t)) & ((1ull << 52) - 1);
+    return fabs(xs - (t - 4503599627370496.0)) != 0.5;
 }
 __device__ __forceinline__ bool chain_rk(double t0, const double (&d)[4], uint32_t K, uint64_t (&rk)[4], double& u,
                                          uint64_t& room) {
