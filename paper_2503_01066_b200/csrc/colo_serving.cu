@@ -1420,6 +1420,9 @@ constexpr int kBsWarpBytes = (2 * kStage + 128) * 8 + 128 * 4;
 // runs (a lane adds a run's weight when its key changes), the exact sum
 // (telescoped when every step time lies in [now, 2 now], as the full pass).
 // Batches of more than kLaneMax members go through run_batches one at a time.
+// A histogram run of cnt samples into bin key: the CTA's shared-memory window
+// (u32: the host enables it only when a CTA's samples stay below 2^31) or the
+// global histogram.
 __device__ __forceinline__ void hist_flush(const ReplayParams& P, uint32_t* shist, uint32_t key, uint64_t cnt) {
     const uint32_t r = key - P.hwin_base;
     if (r < P.hwin) atomicAdd(shist + r, static_cast<uint32_t>(cnt));
@@ -2497,12 +2500,21 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
             }
             // the first pass's histogram (bins = top 21 bits) gets a per-CTA window
             // in shared memory from half the smallest decode-step constant up 4
-            // binades (TPT samples are at least about one step); u32 counts stay
-            // exact while a CTA's samples are below 2^32 (4 segments of at most
-            // 8192 queries, plus a straddling batch, times outputs < 2^16)
+            // binades (TPT samples are at least about one step).  Its u32 counts
+            // cannot wrap: a CTA replays the batches that start in its kWarps
+            // segments, whose members are those queries plus at most one batch
+            // past the last segment (at most budget / kv_bytes_per_token
+            // members: every query needs more than one token's KV), each with
+            // fewer than max(p + o) samples.
+            uint64_t bmax = 0;
+            for (size_t i = 0; i < nprofiles; ++i)
+                bmax = std::max<uint64_t>(bmax, (gpus[i].capacity_bytes - gpus[i].runtime_reserve_bytes -
+                                                 models[i].weights_bytes) / models[i].kv_bytes_per_token);
+            const double per_cta = (static_cast<double>(kWarps) * static_cast<double>(seg) + static_cast<double>(bmax)) *
+                                   static_cast<double>(mctx_seen);
             P.hwin = 0;
             if (P.hist && P.nfilters == 1 && P.filter_shift == 63 && P.prefix[0] == 0 && P.hist_shift == 42 &&
-                mctx_seen > 0 && mctx_seen < (1ull << 16) && seg <= 8192) {
+                mctx_seen > 0 && per_cta < 2147483648.0) {
                 double g = models[0].decode_coef_const;
                 for (size_t i = 1; i < nprofiles; ++i) g = std::min(g, models[i].decode_coef_const);
                 const double lo_s = 0.5 * g;
