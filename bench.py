@@ -780,7 +780,7 @@ def issue_roofline(kind: str, step_s: float, clk: dict, queries: int) -> dict:
     inst = float(d["inst_per_query"]) * queries if d.get("inst_per_query") else float(d["inst_per_step"])
     ach = inst / step_s
     return dict(out, achieved=ach, frac=ach / peak, inst_per_step=inst, inst_per_query=d.get("inst_per_query"),
-                kernels=d.get("kernels"), source=os.path.relpath(files[-1], ROOT))
+                source=os.path.relpath(files[-1], ROOT))
 
 
 def c4_measure(args, world, rank, local, dist, devices_cap, steps, warmup, cpu=False):
