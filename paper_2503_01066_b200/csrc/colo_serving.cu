@@ -271,7 +271,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
             const uint32_t bad = __ballot_sync(FULL, !fits);
             const uint32_t nv = bad ? static_cast<uint32_t>(__ffs(bad) - 1) : 32u;  // lanes [0, nv): batches
             uint32_t hb = 0;
-            if (MODE == RUN_RESOLVE) {  // stop at the first idle start the speculative run also had
+            if constexpr (MODE == RUN_RESOLVE) {  // stop at the first idle start the speculative run also had
                 const uint32_t rel = static_cast<uint32_t>(q - seg_start);
                 bool hit = false;
                 for (uint32_t i = 0; i < nreg; ++i) hit |= sp->regen[i] == rel;
@@ -457,7 +457,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 if (lane == 0 && ridx < kRegen) sp->regen[ridx] = static_cast<uint32_t>(head - seg_start);
                 ++ridx;
             }
-            if (MODE == RUN_RESOLVE) {
+            if constexpr (MODE == RUN_RESOLVE) {
                 const uint32_t rel = static_cast<uint32_t>(head - seg_start);
                 while (ridx < nreg && sp->regen[ridx] < rel) ++ridx;
                 if (ridx < nreg && sp->regen[ridx] == rel) {
