@@ -1430,7 +1430,7 @@ __device__ __forceinline__ void hist_flush(const ReplayParams& P, uint32_t* shis
 }
 
 template <bool SINGLE, bool ONEF>
-__device__ __forceinline__ void lane_batch(const ReplayParams& P, const colo_model& m, uint64_t lo, uint64_t qb,
+__device__ __noinline__ void lane_batch(const ReplayParams& P, const colo_model& m, uint64_t lo, uint64_t qb,
                                            uint32_t n, double start, bool idle, bool first_pass, Acc& A,
                                            uint64_t* bins_rw, uint32_t* shist) {
     // SINGLE: n == 1 (the loops over members and over the member ends drop
@@ -1687,10 +1687,10 @@ __device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint3
                 if (pn) {
                     lane_single_narrow(P, m, lo, qb, st);
                 } else if (p1 && lane_single_p1(P, m, lo, qb, st, idle, A, bins_rw, shist)) {
-                } else if (onef) {
-                    lane_batch<true, true>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                } else if (onef) {  // (the general loop with n = 1: a smaller kernel than a third variant)
+                    lane_batch<false, true>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
                 } else {
-                    lane_batch<true, false>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
+                    lane_batch<false, false>(P, m, lo, qb, 1u, st, idle, first_pass, A, bins_rw, shist);
                 }
             }
         } else {
