@@ -594,6 +594,20 @@ __device__ __forceinline__ void fused_slow(const FusedParams& P, const uint32_t*
 template <bool COUNT>
 __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__ FusedParams P) {
     extern __shared__ __align__(16) uint32_t smw[];
+    // COUNT: the counters of one verdict as eight byte fields (counter k in byte
+    // k), indexed by its bits 19-24 (offload / hedge nullopt, outcome, stream,
+    // stream nullopt); each lane adds these to a packed word and unpacks it
+    // before a byte can overflow, instead of eight warp votes per verdict
+    __shared__ uint64_t inc_tab[COUNT ? 64 : 1];
+    if (COUNT)
+        for (uint32_t key = threadIdx.x; key < 64; key += blockDim.x) {
+            const uint32_t vd = (key >> 2) & 3u;
+            inc_tab[key] = (vd < 3 ? 1ull << (8 * vd) : 0ull) | (static_cast<uint64_t>(key & 1u) << (8 * COLO_CNT_OFFLOAD_OOR)) |
+                           (static_cast<uint64_t>((key >> 1) & 1u) << (8 * COLO_CNT_HEDGE_OOR)) |
+                           (static_cast<uint64_t>((key >> 4) & 1u) << (8 * COLO_CNT_STREAM)) |
+                           (static_cast<uint64_t>((key >> 5) & 1u) << (8 * COLO_CNT_STREAM_OOR)) |
+                           (1ull << (8 * COLO_CNT_TOTAL));
+        }
     for (uint32_t s = 0; s < P.nsets; ++s) {
         const MapView& mv = P.sets[s];
         const uint32_t nt = (mv.C + 1) * (mv.I + 1);
@@ -602,6 +616,15 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
     }
     __syncthreads();
     uint32_t cnt[COLO_NCOUNTERS] = {};
+    uint64_t pk = 0;                      // COUNT: packed byte counters of this lane's fast-path verdicts
+    uint32_t pkn = 0;                     // verdicts in pk (< 256)
+    uint32_t lc[COLO_NCOUNTERS] = {};     // this lane's unpacked counts
+    auto unpack = [&]() {
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) lc[k] += static_cast<uint32_t>((pk >> (8 * k)) & 0xffu);
+        pk = 0;
+        pkn = 0;
+    };
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t gwarp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -660,9 +683,12 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
                 uint4* dst = reinterpret_cast<uint4*>(P.out + cs + lane * 8);
                 __stcs(dst, make_uint4(v[0], v[1], v[2], v[3]));
                 __stcs(dst + 1, make_uint4(v[4], v[5], v[6], v[7]));
-                if (COUNT)
+                if (COUNT) {
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) count_warp(v[k], true, cnt);
+                    for (int k = 0; k < 8; ++k) pk += inc_tab[(v[k] >> 19) & 63u];
+                    pkn += 8;
+                    if (pkn > 240) unpack();  // (warp-uniform: every lane takes 8 per chunk)
+                }
                 prev_b = __shfl_sync(FULL, cb[7], 31);
             } else {
                 fused_slow<true, COUNT>(P, smw, cs, ce, lane, cnt);
@@ -680,6 +706,11 @@ __global__ void __launch_bounds__(kThreads) k_fused_fast(const __grid_constant__
             co0 = no0;
             co1 = no1;
         }
+    }
+    if (COUNT) {
+        unpack();
+#pragma unroll
+        for (int k = 0; k < COLO_NCOUNTERS; ++k) cnt[k] += __reduce_add_sync(FULL, lc[k]);
     }
     if (COUNT) flush_warp_counters(cnt, P.counters);
 }

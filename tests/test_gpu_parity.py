@@ -272,6 +272,10 @@ def test_fused_host_pipeline_and_tuple_crosscheck(ctx, orc):
     v2 = cs.features_decide(ctx, sets, pr, ou, offs, dset)
     assert torch.equal(v1, v2)
     assert int(c1[7]) == D * per and int(c1[0] + c1[1] + c1[2]) == D * per
+    f = cs.verdict_fields(u32(v1))  # every counter equals a recount of the verdict words
+    exp = [(f["verdict"] == 0).sum(), (f["verdict"] == 1).sum(), (f["verdict"] == 2).sum(), f["offload_oor"].sum(),
+           f["hedge_oor"].sum(), f["stream"].sum(), f["stream_oor"].sum(), D * per]
+    assert list(c1.cpu().numpy()) == [int(x) for x in exp]
     hp, ho = pr.cpu().numpy().view(np.uint32), ou.cpu().numpy().view(np.uint32)
     hv, hc = cs.features_decide_host(ctx, sets, hp, ho, offs.cpu().numpy(), dset.cpu().numpy(), counters=True)
     assert (hv == u32(v1)).all() and (hc.astype(np.int64) == c1.cpu().numpy()).all()
