@@ -2285,9 +2285,9 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
         if (prof[d] >= nprofiles) return set_err(ctx, COLO_EINVAL, "device profile index out of range");
     }
     uint64_t seg = opts->segment_len;
-    if (seg == 0) {  // enough segments to fill the GPU several times over, 256..8192 queries each
+    if (seg == 0) {  // enough segments to fill the GPU several times over, 256..16384 queries each
         const uint64_t target = static_cast<uint64_t>(ctx->sm_count) * 64;
-        seg = std::min<uint64_t>(8192, std::max<uint64_t>(256, n / std::max<uint64_t>(target, 1)));
+        seg = std::min<uint64_t>(16384, std::max<uint64_t>(256, n / std::max<uint64_t>(target, 1)));
     }
     std::vector<Seg> segs;
     std::vector<uint32_t> dev_seg(ndev + 1);
