@@ -705,8 +705,9 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         const double* __restrict__ rdk = recd ? P.sat_dk + rrec->doff : nullptr;
         // The replay walks each array sequentially: keep the next ~1K queries of
         // prompt/output and the arrivals around the queue tail warm in L2 so the
-        // dependent loads of later batches hit L2 instead of DRAM.
-        {
+        // dependent loads of later batches hit L2 instead of DRAM (issued when the
+        // head crosses a 256-query line, not for every batch).
+        if ((end ^ head) >> 8) {
             const uint64_t q = end + 512 + lane * 32;
             if (q < N) {
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + q));
