@@ -1550,7 +1550,7 @@ __device__ __forceinline__ bool lane_single_p1(const ReplayParams& P, const colo
     acc_fixed_sub(A.acc, A.flags, now, 1u);
     uint32_t first_slow = 0xffffffffu, bmin = 0xffffffffu, bmax = 0, nslow = 0, rkey = 0xffffffffu, rcnt = 0;
     double x = pd;  // pd + k, exact
-#pragma unroll 2
+#pragma unroll 4
     for (uint32_t k = 0; k < o; ++k) {
         const double d = gam + del * x;  // cost_model.hpp:28-35 (batch 1) = 0.0 + d
         x += 1.0;
