@@ -1130,24 +1130,28 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
         const bool tab_ok = warp_max_u64(mi) < P.dtab_n;
         __syncwarp();
         auto member_pd = [&](uint64_t j) -> double { return staged ? sPD[j] : static_cast<double>(pp[head + j]); };
-        double dur = 0.0;  // engine.hpp:321-325 (cost_model.hpp:18-25, batch 1, unrecorded)
-#pragma unroll 4
-        for (uint64_t j = 0; j < nb; ++j) {
-            const double t = member_pd(j);
-            dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
-        }
-        uint32_t maxo = 0;
+        uint32_t maxo = 0, mino = 0xffffffffu;
         uint64_t needs = 0;
         for (uint64_t j = lane; j < nb; j += 32) {
             const uint32_t pj = staged ? sPO[j].x : pp[head + j], oj = staged ? sPO[j].y : po[head + j];
             maxo = max(maxo, oj);
+            mino = min(mino, oj);
             needs += serving_memory(m, static_cast<uint64_t>(pj) + oj, 1);
         }
-        maxo = static_cast<uint32_t>(warp_max_u64(maxo));
-        uint32_t mino = 0xffffffffu;
-        for (uint64_t j = lane; j < nb; j += 32) mino = min(mino, staged ? sPO[j].y : po[head + j]);
+        maxo = __reduce_max_sync(FULL, maxo);
         mino = __reduce_min_sync(FULL, mino);
         needs = warp_sum_u64(needs);
+        // engine.hpp:321-325 (cost_model.hpp:18-25, batch 1, unrecorded): folded with
+        // the decode steps below when one all-alive window covers the batch
+        const bool fused_pre = staged && tab_ok && maxo <= 128 && mino >= 128;
+        double dur = 0.0;
+        if (!fused_pre) {
+#pragma unroll 4
+            for (uint64_t j = 0; j < nb; ++j) {
+                const double t = member_pd(j);
+                dur += m.prefill_coef_linear * t + m.prefill_coef_quad * t * t;
+            }
+        }
         double* dk = P.sat_dk + doff;
         double first[4] = {0.0, 0.0, 0.0, 0.0};  // steps 0..127 (lane = step mod 32)
         for (uint32_t k0 = 0; k0 < maxo; k0 += 128) {  // engine.hpp:358-365 per step
@@ -1161,14 +1165,27 @@ __global__ void __launch_bounds__(kWarps * 32) k_sat_durations(const __grid_cons
                 // gamma + delta * (double)x and (double)p + (double)k == (double)(p + k)),
                 // so L1 and the f64 pipe share the fold
                 const double* __restrict__ dt = P.dtab[pi] + kb;
+                if (fused_pre) {
 #pragma unroll 4
-                for (uint64_t j = 0; j < nb; ++j) {
-                    const uint32_t pj = sPO[j].x;
-                    const double pdj = sPD[j];
-                    acc[0] += dt[pj];
-                    acc[1] += dt[pj + 32];
-                    acc[2] += gam + del * (pdj + kd[2]);
-                    acc[3] += gam + del * (pdj + kd[3]);
+                    for (uint64_t j = 0; j < nb; ++j) {
+                        const uint32_t pj = sPO[j].x;
+                        const double pdj = sPD[j];
+                        dur += m.prefill_coef_linear * pdj + m.prefill_coef_quad * pdj * pdj;
+                        acc[0] += dt[pj];
+                        acc[1] += dt[pj + 32];
+                        acc[2] += gam + del * (pdj + kd[2]);
+                        acc[3] += gam + del * (pdj + kd[3]);
+                    }
+                } else {
+#pragma unroll 4
+                    for (uint64_t j = 0; j < nb; ++j) {
+                        const uint32_t pj = sPO[j].x;
+                        const double pdj = sPD[j];
+                        acc[0] += dt[pj];
+                        acc[1] += dt[pj + 32];
+                        acc[2] += gam + del * (pdj + kd[2]);
+                        acc[3] += gam + del * (pdj + kd[3]);
+                    }
                 }
             } else if (staged && tab_ok) {
                 const double* __restrict__ dt = P.dtab[pi] + kb;
