@@ -239,6 +239,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
     while (head < stop && head < N) {
         // ---- batch window: engine.hpp:146-147,178-188,270-276 -------------------
         uint64_t tail;
+        const SatRec* rrec_head = nullptr;  // FULL: the all-queued record that is this batch
         bool idle_b = false;
         uint32_t bmin = 0xffffffffu, bmax = 0;  // bins (bits >> 42) of this batch's samples
         const double ah = arr[head];
@@ -663,12 +664,38 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 break;
             }
             if (MODE == RUN_RESOLVE && P.dbg && lane == 0) atomicAdd(P.dbg + 1, 1ull);
-            tail_ptr = find_tail(arr, N, tail_ptr < head ? head : tail_ptr, T);
-            tail = tail_ptr;
+            if (MODE == RUN_FULL && P.sat_on && P.sat_end[lo + head] != 0) {
+                // an all-queued record at head whose last member has arrived is
+                // the batch formation would build (see the resolve fast path):
+                // no queue-tail search and no need scan
+                const SatRec* __restrict__ q = P.sat_recs + P.sat_rec[lo + head];
+                if (q->dev == d && q->start == head && q->alast <= T) rrec_head = q;
+            }
+            if (rrec_head == nullptr) {
+                tail_ptr = find_tail(arr, N, tail_ptr < head ? head : tail_ptr, T);
+                tail = tail_ptr;
+            }
         }
         // ---- batch formation: FIFO, at least one, sum(need) <= budget (engine.hpp:292-306)
         uint64_t end = head, need_total = 0, max_inc = 0;
         uint32_t maxo = 0, mino = 0xffffffffu;
+        if (MODE == RUN_FULL && rrec_head != nullptr) {
+            end = rrec_head->end;
+            need_total = rrec_head->need;
+            for (uint64_t j0 = head; j0 < end; j0 += 32) {  // stage the members
+                const uint64_t j = j0 + lane;
+                const bool valid = j < end;
+                const uint32_t pj = valid ? pp[j] : 0u, oj = valid ? po[j] : 0u;
+                if (valid && j - head < kStage) {
+                    sPO[j - head] = make_uint2(pj, oj);
+                    sPD[j - head] = static_cast<double>(pj);
+                }
+                maxo = max(maxo, __reduce_max_sync(FULL, oj));
+                max_inc = max(max_inc, warp_max_u64(static_cast<uint64_t>(pj) + oj));
+                mino = min(mino, __reduce_min_sync(FULL, valid ? oj : 0xffffffffu));
+            }
+            tail = end;
+        }
         while (end < tail) {
             const uint64_t j = end + lane;
             const bool valid = j < tail;
@@ -700,8 +727,9 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
         const uint64_t nb = end - head;
         // FULL pass: a batch the all-queued records describe exactly takes its
         // prefill and step durations from them (the same folds, done once)
-        const bool recd = (MODE == RUN_FULL || (MODE == RUN_RESOLVE && P.struct_out)) && P.sat_on && P.sat_end[lo + head] == end;
-        const SatRec* __restrict__ rrec = recd ? P.sat_recs + P.sat_rec[lo + head] : nullptr;
+        const bool recd = rrec_head != nullptr ||
+                          ((MODE == RUN_FULL || (MODE == RUN_RESOLVE && P.struct_out)) && P.sat_on && P.sat_end[lo + head] == end);
+        const SatRec* __restrict__ rrec = rrec_head != nullptr ? rrec_head : recd ? P.sat_recs + P.sat_rec[lo + head] : nullptr;
         const double* __restrict__ rdk = recd ? P.sat_dk + rrec->doff : nullptr;
         // The replay walks each array sequentially: keep the next ~1K queries of
         // prompt/output and the arrivals around the queue tail warm in L2 so the
