@@ -1594,9 +1594,12 @@ __device__ __forceinline__ bool lane_single_p1(const ReplayParams& P, const colo
     if (!(now >= 0x1p-44 && span <= now)) return false;  // the sum would not telescope
     acc_fixed_sub(A.acc, A.flags, now, 1u);
     uint32_t first_slow = 0xffffffffu, bmin = 0xffffffffu, bmax = 0, nslow = 0, rkey = 0xffffffffu, rcnt = 0;
+    // A finished run waits in (pkey, pcnt) and is flushed at the end of its
+    // 4-step group: the lanes' runs end at different steps, so flushing at
+    // the step would issue the (divergent) flush at almost every step
+    uint32_t pkey = 0, pcnt = 0;
     double x = pd;  // pd + k, exact
-#pragma unroll 4
-    for (uint32_t k = 0; k < o; ++k) {
+    auto step = [&](uint32_t k) {
         const double d = gam + del * x;  // cost_model.hpp:28-35 (batch 1) = 0.0 + d
         x += 1.0;
         const double nn = now + d;
@@ -1608,13 +1611,25 @@ __device__ __forceinline__ bool lane_single_p1(const ReplayParams& P, const colo
         const uint32_t bn = static_cast<uint32_t>(__double2hiint(s)) >> 10;  // bits >> 42
         bmin = min(bmin, bn);
         bmax = max(bmax, bn);
-        if (bn != rkey) {
-            if (rcnt) hist_flush(P, shist, rkey, rcnt);
-            rkey = bn;
-            rcnt = 0;
+        const bool chg = bn != rkey;
+        const bool ends = chg && rcnt != 0;
+        if (ends && pcnt) hist_flush(P, shist, pkey, pcnt);  // a second run ends in the group (rare)
+        pkey = ends ? rkey : pkey;
+        pcnt = ends ? rcnt : pcnt;
+        rkey = chg ? bn : rkey;
+        rcnt = chg ? 1u : rcnt + 1;
+    };
+    uint32_t k = 0;
+    for (; k + 4 <= o; k += 4) {
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) step(k + i);
+        if (pcnt) {
+            hist_flush(P, shist, pkey, pcnt);
+            pcnt = 0;
         }
-        ++rcnt;
     }
+    for (; k < o; ++k) step(k);
+    if (pcnt) hist_flush(P, shist, pkey, pcnt);
     if (rcnt) hist_flush(P, shist, rkey, rcnt);
     acc_fixed(A.acc, A.flags, now, 1u);  // + T_{o - 1}
     A.gen += o;
