@@ -13,6 +13,7 @@
 // Reference paths are relative to /root/reference/proj/.
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "colo_internal.h"
 #include "colo_tma.cuh"
@@ -341,6 +342,10 @@ struct ExactParams {
     uint32_t L;
     uint32_t wf_mode;  // 1: workspace_factor == 1.0 (need = 2 kv below 2^53), 0: generic llround
     const uint16_t* tab;  // kExactTab entries: bits 0-7 hedge threshold, bit 8 stream bit (k_exact_tab)
+    // exact_verdict_fast's launch conditions (fast = 0: every lane takes exact_verdict)
+    uint32_t fast;   // wf_mode 1, 1 <= abpt < 2^40, ak < 2^50
+    uint32_t cmax;   // floor(budget / ak): cached * ak > budget <=> cached > cmax (no wrap below kSmemTab)
+    float over_f;    // (float)(L + 2)
 };
 
 // Per-value tables for the exact path, indexed by a 16-bit token count c.
@@ -450,15 +455,71 @@ __device__ __forceinline__ uint32_t exact_verdict(const ExactParams& P, bool cpa
     return (code == 0 ? 0u : v) | (stream ? COLO_V_STREAM : 0u);
 }
 
-// Exact per-query verdicts: one 1024-thread CTA per SM, four tuples in flight
-// per thread in registers, the per-value tables in shared memory so their
-// gathers stay out of L1 (measured against a 2-stage TMA tuple pipeline at 256
-// threads: 1.57e11 vs 1.37e11 decisions/s).
+__device__ __noinline__ uint32_t exact_verdict_slow(const ExactParams& P, bool cpa, const uint4 t, const uint8_t* thr,
+                                                   const uint32_t* sbits) {
+    return exact_verdict(P, cpa, t, thr, sbits);
+}
+
+// exact_verdict for the common lane, without branches and with as few
+// ALU-pipe operations as the exact result allows (the kernel is bound by the
+// ALU pipe: compares, selects, bit fields).  The lane's values lie below
+// kSmemTab (both tables in shared memory), kv below 2^53, the hedge entry is
+// threshold-shaped, and the launch satisfies ExactParams::fast; then, when
+// neither AllToHost nor NoAction applies, 0 < deficit <= need < 2^54 and
+// per_layer < 2^54, so (deficit + per_layer - 1) never wraps and the
+// reference's ceil(deficit / per_layer) is found from the fp32 estimate q
+// (within 2^-12 of the quotient while it is <= L + 2) by one signed
+// remainder r = deficit - q * per_layer:
+//   n = q + (r > 0) + (r > per_layer) - (r == -per_layer).
+// An estimate above L + 2 means n > L.  Any other lane sets slow and takes
+// exact_verdict afterwards.
+__device__ __forceinline__ uint32_t exact_verdict_fast(const ExactParams& P, const uint4 t, const uint8_t* thr,
+                                                       const uint32_t* sbits, bool& slow) {
+    const uint32_t cached = t.x, incoming = t.y, charged = t.z;
+    const uint32_t batch = t.w & 0xffffu, pending = (t.w >> 16) & 0xffu, dev = t.w >> 24;
+    const uint32_t L = P.L;
+    const bool fallback = (incoming == 0) | (batch == 0);
+    const bool hoor = cached == 0;  // also per_layer == 0 (abpt >= 1, no wrap)
+    const uint64_t ak = static_cast<uint64_t>(cached) * P.ak;  // acts + kv (maps.hpp:54-61)
+    const uint64_t kv = static_cast<uint64_t>(batch * static_cast<uint64_t>(incoming)) * P.kvbpt;  // cost_model.hpp:54-56
+    const uint64_t need = kv + kv;  // serving_memory, workspace_factor 1 (cost_model.hpp:59-66)
+    const uint64_t headroom = P.budget - ak;
+    const bool a2h_c = cached > P.cmax;
+    const bool noact = need <= headroom;
+    const uint64_t deficit = need - headroom;
+    const uint64_t per_layer = static_cast<uint64_t>(cached) * P.abpt;
+    float rcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(__ull2float_rn(per_layer)));
+    const float fq = __fmul_rz(__ull2float_rn(deficit), rcp);
+    const bool over = fq > P.over_f;
+    const uint32_t q = static_cast<uint32_t>(fq);
+    const int64_t r = static_cast<int64_t>(deficit - q * per_layer);
+    const int64_t pl = static_cast<int64_t>(per_layer);
+    const uint32_t n = q + (r > 0) + (r > pl) - (r == -pl);
+    const uint32_t ccode = (over | (n > L)) ? 1u : 2u + n;
+    const uint32_t code = (fallback | a2h_c) ? 1u : (noact ? 0u : (hoor ? 1u : ccode));
+    const bool a2h = code == 1;
+    const uint32_t layers = code >= 2 ? code - 2 : 0u;
+    const uint32_t free_now = a2h ? dev : min(layers, dev);
+    const uint32_t total = min(pending + (a2h ? L : layers), L);
+    const uint32_t th = thr[min(cached, kSmemTab - 1)];
+    const uint32_t recompute = (fallback | hoor) ? 1u : static_cast<uint32_t>(total >= th);
+    const uint32_t v = (a2h ? COLO_ACT_ALLTOHOST : COLO_ACT_FREELAYERS) | (layers << 2) | (free_now << 10) |
+                       (recompute << 18) | (fallback ? COLO_V_OFFLOAD_OOR : 0u) |
+                       ((!fallback && hoor) ? COLO_V_HEDGE_OOR : 0u) | ((COLO_VD_FREE_LOADBACK + recompute) << 21);
+    const bool stream = (sbits[min(charged, kSmemTab - 1) >> 5] >> (charged & 31)) & 1u;
+    // (bitwise: no short-circuit branches)
+    slow = (max(cached, charged) >= kSmemTab) | ((th == 0xffu) & !fallback & !hoor) | (!fallback & ((kv >> 53) != 0));
+    return (code == 0 ? 0u : v) | (stream ? COLO_V_STREAM : 0u);
+}
+
+constexpr int kExactU = 4, kExactStages = 3;
 template <bool COUNT>
 __global__ void __launch_bounds__(kPackThreads, 1) k_decide_exact(const __grid_constant__ ExactParams P) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint32_t* sbits = reinterpret_cast<uint32_t*>(sm);
     uint8_t* thr = reinterpret_cast<uint8_t*>(sbits + kSmemTab / 32);
+    uint4* ring = reinterpret_cast<uint4*>(thr + kSmemTab);  // [kExactStages][U][blockDim.x]
     for (uint32_t w = threadIdx.x; w < kSmemTab / 32; w += blockDim.x) {
         uint32_t bits = 0;
         for (uint32_t b = 0; b < 32; ++b) bits |= static_cast<uint32_t>(__ldg(P.tab + 32 * w + b) >> 8) << b;
@@ -467,26 +528,65 @@ __global__ void __launch_bounds__(kPackThreads, 1) k_decide_exact(const __grid_c
     for (uint32_t c = threadIdx.x; c < kSmemTab; c += blockDim.x) thr[c] = static_cast<uint8_t>(__ldg(P.tab + c));
     __syncthreads();
     const bool cpa = P.cpa != 0;
+    const bool fast = P.fast != 0;
     uint32_t cnt[COLO_NCOUNTERS] = {};
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    constexpr int U = 4;
+    constexpr int U = kExactU;
+    // Each thread streams its own tuples through a kExactStages-deep cp.async
+    // ring in shared memory (slot [stage][u][thread]: conflict-free 16 B
+    // reads), so U * kExactStages loads per thread are in flight while it
+    // computes -- register loads would be sunk to their uses by the scheduler.
+    auto issue = [&](int st, uint64_t base) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * stride;
+            uint4* dst = ring + (static_cast<uint32_t>(st) * U + u) * blockDim.x + threadIdx.x;
+            if (i < P.n)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                             "l"(P.in + i)
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     const uint64_t wbase = tid & ~uint64_t(31);  // warp-uniform trip count
+#pragma unroll
+    for (int st = 0; st < kExactStages - 1; ++st) issue(st, tid + st * stride * U);
+    int st = 0;
     for (uint64_t base = tid, wb = wbase; wb < P.n; base += stride * U, wb += stride * U) {
-        uint4 t[U];
+        issue((st + kExactStages - 1) % kExactStages, base + (kExactStages - 1) * stride * U);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kExactStages - 1) : "memory");
+        // every tuple of the warp's U in range (warp-uniform): no per-tuple guards
+        const bool full = wb + (U - 1) * stride + 32 <= P.n;
+        auto body = [&](auto guard) {
+            constexpr bool G = decltype(guard)::value;
+            uint32_t v[U], slowm = 0;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t i = base + u * stride;
-            t[u] = i < P.n ? __ldcs(P.in + i) : make_uint4(0, 1, 0, 1);
-        }
+            for (int u = 0; u < U; ++u) {
+                const uint4* src = ring + (static_cast<uint32_t>(st) * U + u) * blockDim.x + threadIdx.x;
+                const uint4 t = (!G || base + u * stride < P.n) ? *src : make_uint4(0, 1, 0, 1);
+                bool sl;
+                v[u] = exact_verdict_fast(P, t, thr, sbits, sl);
+                slowm |= (sl | !fast) ? 1u << u : 0u;
+            }
+            if (slowm) {  // (the tuples are re-read: keeping them live costs spills)
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t i = base + u * stride;
-            const uint32_t v = exact_verdict(P, cpa, t[u], thr, sbits);
-            if (i < P.n) __stcs(P.out + i, v);
-            if (COUNT) count_warp(v, i < P.n, cnt);
-        }
+                for (int u = 0; u < U; ++u)
+                    if ((slowm >> u) & 1u) v[u] = exact_verdict_slow(P, cpa, P.in[base + u * stride], thr, sbits);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = base + u * stride;
+                const bool ok = !G || i < P.n;
+                if (ok) __stcs(P.out + i, v[u]);
+                if (COUNT) count_warp(v[u], ok, cnt);
+            }
+        };
+        if (full) body(std::false_type{});
+        else body(std::true_type{});
+        st = st + 1 == kExactStages ? 0 : st + 1;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
@@ -888,6 +988,9 @@ colo_status colo_decide_exact(colo_ctx* ctx, const colo_model* m, const colo_gpu
     P.kvbpt = m->kv_bytes_per_token;
     P.ak = m->num_layers * m->act_bytes_per_token_per_layer + (P.cpa ? m->kv_bytes_per_token : 0ull);
     P.wf_mode = m->workspace_factor == 1.0 ? 1u : 0u;
+    P.fast = P.wf_mode == 1 && P.abpt >= 1 && P.abpt < (1ull << 40) && P.ak < (1ull << 50);
+    P.cmax = P.ak == 0 ? 0xffffffffu : static_cast<uint32_t>(std::min<uint64_t>(P.budget / P.ak, 0xffffffffull));
+    P.over_f = static_cast<float>(P.L + 2);
     // per-value tables: rebuilt only when (model, gpu, mode, assumed) changes
     unsigned char key[sizeof(ctx->htab_key)] = {};
     std::memcpy(key, m, sizeof(colo_model));
@@ -904,7 +1007,7 @@ colo_status colo_decide_exact(colo_ctx* ctx, const colo_model* m, const colo_gpu
     }
     P.tab = ctx->d_htab;
     const void* fn = d_counters ? (const void*)k_decide_exact<true> : (const void*)k_decide_exact<false>;
-    const size_t dyn = kSmemTab / 8 + kSmemTab;
+    const size_t dyn = kSmemTab / 8 + kSmemTab + sizeof(uint4) * kExactStages * kExactU * kPackThreads;
     COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int blocks = blocks_for(ctx, fn, kPackThreads, dyn);
     const uint64_t need_blocks = (n + kPackThreads - 1) / kPackThreads;

@@ -15,8 +15,10 @@ from collections import defaultdict
 
 
 def line_totals(rep: str, kernel: str | None = None):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:  # the import honours the kernel filter: only that kernel's launches
+        cmd += ["--kernel-name", f"regex:{kernel}"]
+    raw = subprocess.run(cmd, capture_output=True, text=True).stdout
     inst = defaultdict(int)
     samp = defaultdict(int)
     text = {}

@@ -160,13 +160,18 @@ def test_decide_exact_quotient_edges(ctx, orc):
     per-cached hedge thresholds) against the oracle where the ceil-divide of
     maps.hpp:227 lands exactly on integers (tiny per-layer bytes), around n = L,
     across the whole u32 range (u64 wrap in the byte products) and for
-    cached values past the threshold table."""
+    cached values past the threshold table; models with workspace factor 1
+    take the branch-free fast path (signed-remainder ceil, cmax AllToHost
+    test), the others the general one."""
     rng = np.random.default_rng(31)
     small = [(cs.ModelProfile(num_layers=L, kv_bytes_per_token=kv, act_bytes_per_token_per_layer=a,
                               workspace_factor=wf, weights_bytes=w),
               cs.GpuProfile(capacity_bytes=cap, h2d_bandwidth=h2d, d2h_bandwidth=h2d, runtime_reserve_bytes=0))
              for L, kv, a, wf, w, cap, h2d in ((32, 3, 1, 0.0, 1, 400_000, 1000), (40, 5, 2, 0.5, 1000, 2_000_000, 77),
-                                               (7, 1, 3, 0.25, 1, 60_000, 3), (253, 2, 1, 1.0, 1, 1_000_000, 10_000))]
+                                               (7, 1, 3, 0.25, 1, 60_000, 3), (253, 2, 1, 1.0, 1, 1_000_000, 10_000),
+                                               # workspace factor 1: the branch-free fast path on tiny per-layer bytes
+                                               (32, 3, 1, 1.0, 1, 400_000, 1000), (40, 5, 2, 1.0, 1000, 2_000_000, 77),
+                                               (7, 1, 3, 1.0, 1, 60_000, 3), (200, 1, 7, 1.0, 5, 3_000_000, 50))]
     big = [(m, G) for m, _ in MODELS.values()]
     for m, g in small + big:
         om, og = m.to_c(), g.to_c()
