@@ -121,6 +121,8 @@ struct DecideParams {
     uint32_t* out;
     uint64_t n;
     uint64_t* counters;
+    const uint8_t* img;  // k_decide_packed: the map set's shared-memory image (colo_mapset::d_img), or null
+    uint32_t img_bytes;
 };
 
 template <bool SMEM, bool COUNT>
@@ -176,11 +178,50 @@ constexpr int kPackThreads = 1024;
 #ifndef COLO_PACK_FROM
 #define COLO_PACK_FROM (32 * 1024)
 #endif
-constexpr size_t kPackFrom = COLO_PACK_FROM;  // byte-cell tables above this size take the packed kernel
+constexpr size_t kPackFrom = COLO_PACK_FROM;
+#ifndef COLO_PACK_U
+#define COLO_PACK_U 6
+#endif  // byte-cell tables above this size take the packed kernel
 
 __device__ __forceinline__ uint32_t packed_cell(const uint32_t* pk, uint32_t idx) {
     const uint32_t w = __umulhi(idx, 0xCCCCCCCDu) >> 2;  // idx / 5
     return (pk[w] >> (6u * (idx - 5u * w))) & 63u;
+}
+
+// the packed image: cells five 6-bit codes per word, the hedge bits, the
+// per-cached-bucket stream bytes (cell (ci, 0, 0) == AllToHost), each part
+// 16-byte aligned
+__device__ __forceinline__ void pack_image(const MapView& mv, uint32_t* pk, uint8_t* hed, uint8_t* sbit, uint32_t t0,
+                                           uint32_t nt) {
+    const uint32_t ncells = mv.off_bytes, nw = (ncells + 4) / 5;
+    for (uint32_t w = t0; w < nw; w += nt) {
+        uint32_t word = 0;
+#pragma unroll
+        for (uint32_t r = 0; r < 5; ++r) {
+            const uint32_t i = 5 * w + r;
+            if (i < ncells) word |= static_cast<uint32_t>(__ldg(mv.off + i)) << (6 * r);
+        }
+        pk[w] = word;
+    }
+    for (uint32_t i = t0; i < mv.hed_bytes; i += nt) hed[i] = mv.hed[i];
+    for (uint32_t ci = t0; ci < mv.C; ci += nt) sbit[ci] = __ldg(mv.off + ci * mv.I * mv.B) == 1;
+}
+
+__global__ void k_pack_image(const __grid_constant__ MapView mv, uint8_t* __restrict__ img) {
+    const uint32_t nw = (mv.off_bytes + 4) / 5;
+    uint32_t* pk = reinterpret_cast<uint32_t*>(img);
+    uint8_t* hed = img + ((nw * 4 + 15u) & ~15u);
+    uint8_t* sbit = hed + ((mv.hed_bytes + 15u) & ~15u);
+    pack_image(mv, pk, hed, sbit, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+// bytes of the packed image when the grid takes k_decide_packed, else 0
+size_t packed_image_bytes(const MapView& mv) {
+    const size_t smem = ((mv.off_bytes + 15u) & ~15u) + mv.hed_bytes;
+    const bool fastgrid = mv.hsame && mv.fc.d > 1 && mv.fi.d > 1 && mv.fb.d > 1;
+    const size_t packed = ((((mv.off_bytes + 4u) / 5u) * 4u + 15u) & ~size_t(15)) + ((mv.hed_bytes + 15u) & ~15u) +
+                          ((mv.C + 15u) & ~15u);
+    return (smem > kPackFrom && fastgrid && mv.L + 2 < 64 && packed <= 220 * 1024) ? packed : 0;
 }
 
 template <bool COUNT>
@@ -191,31 +232,36 @@ __global__ void __launch_bounds__(kPackThreads, 1) k_decide_packed(const __grid_
     uint32_t* pk = reinterpret_cast<uint32_t*>(sm);
     uint8_t* hed = sm + ((nw * 4 + 15u) & ~15u);
     uint8_t* sbit = hed + ((mv.hed_bytes + 15u) & ~15u);  // [C] cell (ci, 0, 0) == AllToHost
-    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) {
-        uint32_t word = 0;
-#pragma unroll
-        for (uint32_t r = 0; r < 5; ++r) {
-            const uint32_t i = 5 * w + r;
-            if (i < ncells) word |= static_cast<uint32_t>(__ldg(mv.off + i)) << (6 * r);
+    if (P.img) {  // the map set's prebuilt image: one bulk copy (L2-resident after the first CTA)
+        __shared__ uint64_t bar;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(&bar, P.img_bytes);
+            bulk_g2s(sm, P.img, P.img_bytes, &bar);
         }
-        pk[w] = word;
+        __syncthreads();
+        mbar_wait(&bar, 0);
+    } else {
+        pack_image(mv, pk, hed, sbit, threadIdx.x, blockDim.x);
+        __syncthreads();
     }
-    for (uint32_t i = threadIdx.x; i < mv.hed_bytes; i += blockDim.x) hed[i] = mv.hed[i];
-    for (uint32_t ci = threadIdx.x; ci < mv.C; ci += blockDim.x) sbit[ci] = __ldg(mv.off + ci * mv.I * mv.B) == 1;
-    __syncthreads();
     const FastMap f{mv.max_c, mv.max_i, mv.max_b, mv.hmax, mv.L, mv.I, mv.B, mv.fc.c_lo, mv.fc.c_hi, mv.fi.c_lo,
                     mv.fi.c_hi, mv.fb.c_lo, mv.fb.c_hi, mv.fc.d, mv.fi.d, mv.fb.d};
     uint32_t cnt[COLO_NCOUNTERS] = {};
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    constexpr int U = 4;
+    constexpr int U = COUNT ? 4 : COLO_PACK_U;  // (the counters need the registers)
     const uint64_t wbase = tid & ~uint64_t(31);  // warp-uniform trip count
     for (uint64_t base = tid, wb = wbase; wb < P.n; base += stride * U, wb += stride * U) {
+      // every tuple of the warp's U in range (warp-uniform): no per-tuple guards
+      auto body = [&](auto guard) {
+        constexpr bool G = decltype(guard)::value;
         uint4 t[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = base + u * stride;
-            t[u] = i < P.n ? __ldcs(P.in + i) : make_uint4(0, 0, 0, 0);
+            t[u] = (!G || i < P.n) ? __ldcs(P.in + i) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -246,9 +292,13 @@ __global__ void __launch_bounds__(kPackThreads, 1) k_decide_packed(const __grid_
             const bool soor = ch > f.max_c;
             const uint32_t sb = sbit[fdiv(min(ch, f.max_c) + f.dc - 1u, f.cc_lo, f.cc_hi)];
             v |= soor ? (COLO_V_STREAM | COLO_V_STREAM_OOR) : (sb ? COLO_V_STREAM : 0u);
-            if (i < P.n) __stcs(P.out + i, v);
-            if (COUNT) count_warp(v, i < P.n, cnt);
+            const bool ok = !G || i < P.n;
+            if (ok) __stcs(P.out + i, v);
+            if (COUNT) count_warp(v, ok, cnt);
         }
+      };
+      if (wb + (U - 1) * stride + 32 <= P.n) body(std::false_type{});
+      else body(std::true_type{});
     }
     if (COUNT) flush_warp_counters(cnt, P.counters);
 }
@@ -902,9 +952,12 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
     const size_t smem = ((P.mv.off_bytes + 15u) & ~15u) + P.mv.hed_bytes;
     const bool use_smem = smem <= 96 * 1024;
     const bool fastgrid = P.mv.hsame && P.mv.fc.d > 1 && P.mv.fi.d > 1 && P.mv.fb.d > 1;
-    const size_t packed = ((((P.mv.off_bytes + 4u) / 5u) * 4u + 15u) & ~size_t(15)) + ((P.mv.hed_bytes + 15u) & ~15u) +
-                          P.mv.C;
-    if (smem > kPackFrom && fastgrid && P.mv.L + 2 < 64 && packed <= 220 * 1024) {  // packed cells in shared memory
+    const size_t packed = packed_image_bytes(P.mv);
+    if (packed) {  // packed cells in shared memory
+        if (ms->d_img && ms->img_bytes == packed) {
+            P.img = ms->d_img;
+            P.img_bytes = static_cast<uint32_t>(packed);
+        }
         const void* fn = d_counters ? (const void*)k_decide_packed<true> : (const void*)k_decide_packed<false>;
         COLO_CK(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)packed));
         int blocks = blocks_for(ctx, fn, kPackThreads, packed);
@@ -952,6 +1005,25 @@ colo_status launch_decide(colo_ctx* ctx, cudaStream_t stream, const colo_mapset*
 }
 
 }  // namespace
+
+namespace colo {
+
+colo_status build_pack_image(colo_ctx* ctx, colo_mapset* ms) {
+    const MapView mv = make_view(ms);
+    const size_t bytes = packed_image_bytes(mv);
+    if (bytes == 0) return COLO_OK;
+    if (!ms->d_img) {
+        COLO_CK(ctx, cudaMalloc(&ms->d_img, bytes));
+        ms->img_bytes = static_cast<uint32_t>(bytes);
+    }
+    COLO_CK(ctx, cudaMemsetAsync(ms->d_img, 0, bytes, ctx->stream));
+    COLO_LAUNCHED(ctx);
+    k_pack_image<<<148, 256, 0, ctx->stream>>>(mv, ms->d_img);
+    COLO_CK(ctx, cudaGetLastError());
+    return COLO_OK;
+}
+
+}  // namespace colo
 
 extern "C" {
 

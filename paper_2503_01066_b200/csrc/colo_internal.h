@@ -66,6 +66,8 @@ struct colo_mapset {
     uint8_t* d_hed = nullptr;   // Hc*F hedge bits
     uint32_t* d_tab = nullptr;  // (C+1)*(I+1) trace-fused verdict table (hedge_step == cached_step only)
     uint32_t* d_str = nullptr;  // C+1 stream bits per cached bucket
+    uint8_t* d_img = nullptr;   // k_decide_packed's shared-memory image (packed cells, hedge bits, stream bytes)
+    uint32_t img_bytes = 0;     // 0: the grid does not take the packed kernel
     bool fast = false;
 };
 
@@ -80,6 +82,9 @@ colo_status check_model_limits(const colo_model* m);
 double fixed_mean(const uint64_t sum[3], uint64_t n);
 void fixed_add(uint64_t acc[3], const uint64_t v[3]);
 // in-place ncclAllReduce on the context's stream (NCCL resolved at run time)
+// k_decide_packed's shared-memory image of a map set (sweep-size grids only;
+// a no-op otherwise), rebuilt whenever the cells change
+colo_status build_pack_image(colo_ctx* ctx, colo_mapset* ms);
 colo_status nccl_allreduce_raw(colo_ctx* ctx, void* comm, void* d_buf, size_t count, int dtype, int op);
 
 }  // namespace colo

@@ -193,6 +193,11 @@ colo_status colo_mapset_build(colo_ctx* ctx, const colo_model* m, const colo_gpu
         COLO_LAUNCHED(ctx);
         k_build_tab<<<static_cast<uint32_t>((ntab + 255) / 256), 256, 0, ctx->stream>>>(mv, ms->d_tab, ms->d_str);
     }
+    if (colo::build_pack_image(ctx, ms) != COLO_OK) {
+        std::string why = ctx->err;
+        colo_mapset_destroy(ms);
+        return set_err(ctx, COLO_ECUDA, why);
+    }
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) {
@@ -232,6 +237,8 @@ colo_status colo_mapset_from_cells(colo_ctx* ctx, const colo_model* m, const col
         COLO_LAUNCHED(ctx);
         k_build_tab<<<static_cast<uint32_t>((ntab + 255) / 256), 256, 0, ctx->stream>>>(mv, ms->d_tab, ms->d_str);
     }
+    colo_status ist = colo::build_pack_image(ctx, ms);  // from the loaded cells
+    if (ist != COLO_OK) return ist;
     COLO_CK(ctx, cudaGetLastError());
     COLO_CK(ctx, cudaStreamSynchronize(ctx->stream));
     return COLO_OK;
@@ -265,6 +272,7 @@ void colo_mapset_destroy(colo_mapset* ms) {
     cudaFree(ms->d_hed);
     cudaFree(ms->d_tab);
     cudaFree(ms->d_str);
+    cudaFree(ms->d_img);
     delete ms;
 }
 

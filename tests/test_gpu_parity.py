@@ -102,6 +102,20 @@ def test_map_errors(ctx):
     assert (ld.cells()[0] == off).all() and (ld.cells()[1] == hed).all()
 
 
+def test_packed_map_from_cells(ctx):
+    """A sweep-size grid (step 50: the packed shared-memory kernel, whose
+    image the map set builds once) loaded from its cells decides exactly like
+    the built map: the image is rebuilt from the loaded cells."""
+    steps, bounds = cs.GridSteps(50, 50, 5), cs.GridBounds()
+    ms = cs.MapSet.build(ctx, cs.ModelProfile(), G, steps, bounds, cs.TrainingMode.CPT)
+    off, hed = ms.cells()
+    ld = cs.MapSet.from_cells(ctx, cs.ModelProfile(), G, steps, bounds, cs.TrainingMode.CPT, 50, 8000, 128,
+                              cs.profile_hash(cs.ModelProfile(), G), off, hed)
+    rng = np.random.default_rng(17)
+    dt = to_dev_tuples(random_tuples(rng, 2_000_003, 32))
+    assert (u32(cs.decide(ctx, ld, dt)) == u32(cs.decide(ctx, ms, dt))).all()
+
+
 # ----------------------------------------------------------------- decide
 @pytest.mark.parametrize("mn", list(MODELS))
 def test_decide_golden(ctx, mn):
