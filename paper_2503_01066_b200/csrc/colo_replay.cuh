@@ -88,13 +88,16 @@ __device__ __forceinline__ double pow2i(int k) {  // k in [-1022, 1023]
 // x, or a result >= 2^51 (x*sc is exact: callers keep sc in [2^-60, 2^260]
 // and x either 0 or >= 2^-700).  Adding 2^52 rounds x*sc to an integer (the
 // f64 spacing there is 1) whose value is the low mantissa bits.
+template <bool POS = false>  // POS: the caller guarantees x >= 2^-700 (durations of validated profiles)
 __device__ __forceinline__ bool rn_units(double x, double sc, uint64_t& r) {
     const double xs = x * sc;
-    if (!(xs < 2251799813685248.0) || !(x >= 0.0) || (x != 0.0 && x < 0x1p-700)) return false;
+    if (POS ? !(xs < 2251799813685248.0) : (!(xs < 2251799813685248.0) || !(x >= 0.0) || (x != 0.0 && x < 0x1p-700)))
+        return false;
     const double t = xs + 4503599627370496.0;
     r = static_cast<uint64_t>(__double_as_longlong(t)) & ((1ull << 52) - 1);
     return fabs(xs - (t - 4503599627370496.0)) != 0.5;
 }
+template <bool POS = false>
 __device__ __forceinline__ bool chain_rk(double t0, const double (&d)[4], uint32_t K, uint64_t (&rk)[4], double& u,
                                          uint64_t& room) {
     const uint32_t lane = threadIdx.x & 31;
@@ -108,7 +111,7 @@ __device__ __forceinline__ bool chain_rk(double t0, const double (&d)[4], uint32
     for (int r = 0; r < 4; ++r) {
         const uint32_t i = 32 * r + lane;
         rk[r] = 0;
-        if (i < K) ok &= rn_units(d[r], sc, rk[r]);
+        if (i < K) ok &= rn_units<POS>(d[r], sc, rk[r]);
     }
     return __all_sync(kFullMask, ok);
 }
@@ -121,12 +124,15 @@ __device__ __forceinline__ uint64_t warp_sum_small(uint64_t v) {
     return static_cast<uint64_t>(c0) + (static_cast<uint64_t>(c1) << 19) + (static_cast<uint64_t>(c2) << 38);
 }
 
-// now_{K-1} (the batch's end) or false
+// now_{K-1} (the batch's end) or false.  POS: every duration of the first
+// K is >= 2^-700 (a decode step of a validated profile whose step constant
+// is at least that), so rn_units skips its sign and range tests.
+template <bool POS = false>
 __device__ __forceinline__ bool chain_fast_end(double t0, const double (&d)[4], uint32_t K, double& t_end) {
     uint64_t rk[4];
     double u;
     uint64_t room;
-    if (!chain_rk(t0, d, K, rk, u, room)) return false;
+    if (!chain_rk<POS>(t0, d, K, rk, u, room)) return false;
     const uint64_t s = warp_sum_small(rk[0] + rk[1] + rk[2] + rk[3]);  // lane sums < 2^55
     if (s >= room) return false;
     t_end = t0 + static_cast<double>(s) * u;  // exact: a multiple of u below 2^(e+1)

@@ -206,6 +206,8 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
     const uint32_t* __restrict__ pp = P.p + lo;
     const uint32_t* __restrict__ po = P.o + lo;
     const bool want_hist = MODE == RUN_FULL && P.hist != nullptr;
+    // every decode step duration >= the step constant (positive coefficients, validate_profile_pair)
+    const bool dpos = m.decode_coef_const >= 0x1p-700 && m.decode_coef_context >= 0.0;
     uint64_t tail_ptr = head;
     uint32_t ridx = 0;
     const uint32_t nreg = MODE == RUN_RESOLVE ? min(sp->nregen, static_cast<uint32_t>(kRegen)) : 0u;
@@ -337,7 +339,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         dk[r] = i < K ? 0.0 + (gam + del * (tqL + static_cast<double>(k0 + i))) : 0.0;
                     }
                     double te;
-                    if (chain_fast_end(t, dk, K, te)) {
+                    if (dpos ? chain_fast_end<true>(t, dk, K, te) : chain_fast_end(t, dk, K, te)) {
                         t = te;
                     } else {
                         for (uint32_t i = 0; i < K; ++i) t = t + (0.0 + (gam + del * (tqL + static_cast<double>(k0 + i))));
@@ -695,6 +697,19 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 mino = min(mino, __reduce_min_sync(FULL, valid ? oj : 0xffffffffu));
             }
             tail = end;
+        } else if (tail == head + 1) {  // one query in the queue: the batch is that query
+            const uint32_t pj = pp[head], oj = po[head];
+            need_total = serving_memory(m, static_cast<uint64_t>(pj) + oj, 1);
+            if (lane == 0) {
+                sPO[0] = make_uint2(pj, oj);
+                sPD[0] = static_cast<double>(pj);
+            }
+            maxo = oj;
+            if (MODE == RUN_FULL) {
+                max_inc = static_cast<uint64_t>(pj) + oj;
+                mino = oj;
+            }
+            end = tail;
         }
         while (end < tail) {
             const uint64_t j = end + lane;
@@ -844,7 +859,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                 // only the batch's end is needed: the chain as one warp scan while
                 // it stays in its binade, else one lane's sequential fold
                 double te;
-                if (chain_fast_end(now, dk, cnt, te)) {
+                if (dpos ? chain_fast_end<true>(now, dk, cnt, te) : chain_fast_end(now, dk, cnt, te)) {
                     now = te;
                 } else {
                     __syncwarp();
