@@ -1466,7 +1466,7 @@ __global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_replay_full(cons
 }
 
 constexpr uint32_t kLaneMax = 4;     // members a lane replays by itself in k_batch_stats
-constexpr uint32_t kHistWin = 2048;  // first-pass histogram bins per CTA in shared memory (4 binades)
+constexpr uint32_t kHistWin = 1024;  // first-pass histogram bins per CTA in shared memory (from just below the step constant)
 // k_batch_stats' per-warp region for run_batches on a queued batch (member
 // stage, step durations, alive counts; never the idle-start tile: a queued
 // batch starts at or after every member's arrival)
@@ -1865,7 +1865,7 @@ __device__ __forceinline__ void batch_stats_segment(const ReplayParams& P, uint3
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, kReplayBlocks) k_batch_stats(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32, 6) k_batch_stats(const __grid_constant__ ReplayParams P) {
     extern __shared__ double stile[];  // per warp the run_batches region, then the CTA's histogram window
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint32_t* const shist = reinterpret_cast<uint32_t*>(stile + kWarps * kBsWarpBytes / 8);
@@ -2593,7 +2593,7 @@ colo_status colo_replay_serving(colo_ctx* ctx, const colo_model* models, const c
                 mctx_seen > 0 && per_cta < 2147483648.0) {
                 double g = models[0].decode_coef_const;
                 for (size_t i = 1; i < nprofiles; ++i) g = std::min(g, models[i].decode_coef_const);
-                const double lo_s = 0.5 * g;
+                const double lo_s = g * (1.0 - 0x1p-20);  // every single-query sample is >= g within rounding
                 uint64_t b = 0;
                 std::memcpy(&b, &lo_s, 8);
                 if (lo_s > 0.0 && std::isfinite(lo_s)) {
