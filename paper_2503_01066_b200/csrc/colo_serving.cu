@@ -50,7 +50,10 @@ constexpr int kSatHdr = 4;   // per all-queued record: its chain sums in 4 candi
 #ifndef COLO_REPLAY_BLOCKS
 #define COLO_REPLAY_BLOCKS 5
 #endif
-constexpr int kReplayBlocks = COLO_REPLAY_BLOCKS;  // resident CTAs per SM the replay pass is compiled for
+constexpr int kReplayBlocks = COLO_REPLAY_BLOCKS;
+#ifndef COLO_SPEC_BLOCKS
+#define COLO_SPEC_BLOCKS 6  // resident CTAs per SM k_speculate is compiled for
+#endif  // resident CTAs per SM the replay pass is compiled for
 constexpr int kTileBytes = kWarps * 32 * 33 * 8;   // k_replay_full's dynamic shared memory
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -1346,7 +1349,7 @@ __global__ void k_seg_scan(const __grid_constant__ ReplayParams P) {
     }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_speculate(const __grid_constant__ ReplayParams P) {
+__global__ void __launch_bounds__(kWarps * 32, COLO_SPEC_BLOCKS) k_speculate(const __grid_constant__ ReplayParams P) {
     __shared__ uint2 spo[kWarps][kStage];
     __shared__ double spd[kWarps][kStage];
     __shared__ __align__(16) double sdk[kWarps][128];
