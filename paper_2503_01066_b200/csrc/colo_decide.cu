@@ -516,11 +516,11 @@ __device__ __noinline__ uint32_t exact_verdict_slow(const ExactParams& P, bool c
 // kSmemTab (both tables in shared memory), kv below 2^53, the hedge entry is
 // threshold-shaped, and the launch satisfies ExactParams::fast; then, when
 // neither AllToHost nor NoAction applies, 0 < deficit <= need < 2^54 and
-// per_layer < 2^54, so (deficit + per_layer - 1) never wraps and the
-// reference's ceil(deficit / per_layer) is found from the fp32 estimate q
-// (within 2^-12 of the quotient while it is <= L + 2) by one signed
-// remainder r = deficit - q * per_layer:
-//   n = q + (r > 0) + (r > per_layer) - (r == -per_layer).
+// per_layer < 2^54, so sum = deficit + per_layer - 1 never wraps and the
+// reference's sum / per_layer is found from the fp32 estimate q of the
+// quotient (within 2^-12 of it while it is <= L + 2, so q is the floor or
+// one off) by one signed remainder r = sum - q * per_layer:
+//   n = q + (r >= per_layer) - (r < 0).
 // An estimate above L + 2 means n > L.  Any other lane sets slow and takes
 // exact_verdict afterwards.
 __device__ __forceinline__ uint32_t exact_verdict_fast(const ExactParams& P, const uint4 t, const uint8_t* thr,
@@ -538,14 +538,15 @@ __device__ __forceinline__ uint32_t exact_verdict_fast(const ExactParams& P, con
     const bool noact = need <= headroom;
     const uint64_t deficit = need - headroom;
     const uint64_t per_layer = static_cast<uint64_t>(cached) * P.abpt;
+    // n = floor(sum / per_layer), sum = deficit + per_layer - 1 (maps.hpp:227; no wrap here)
+    const uint64_t sum = deficit + (per_layer - 1);
     float rcp;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(__ull2float_rn(per_layer)));
-    const float fq = __fmul_rz(__ull2float_rn(deficit), rcp);
+    const float fq = __fmul_rz(__ull2float_rn(sum), rcp);
     const bool over = fq > P.over_f;
     const uint32_t q = static_cast<uint32_t>(fq);
-    const int64_t r = static_cast<int64_t>(deficit - q * per_layer);
-    const int64_t pl = static_cast<int64_t>(per_layer);
-    const uint32_t n = q + (r > 0) + (r > pl) - (r == -pl);
+    const int64_t r = static_cast<int64_t>(sum - q * per_layer);
+    const uint32_t n = q + (r >= static_cast<int64_t>(per_layer)) - (r < 0);
     const uint32_t ccode = (over | (n > L)) ? 1u : 2u + n;
     const uint32_t code = (fallback | a2h_c) ? 1u : (noact ? 0u : (hoor ? 1u : ccode));
     const bool a2h = code == 1;
