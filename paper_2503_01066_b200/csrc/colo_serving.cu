@@ -46,7 +46,10 @@ constexpr int kWarps = 4;    // warps per CTA
 constexpr int kStage = 256;  // batch members staged in shared memory per warp
 constexpr int kRegen = 30;   // idle batch starts recorded per speculative segment
 constexpr double kSpecGiveUp = 900.0;  // s of queueing after which a speculative run without idle starts stops
-constexpr int kSatHdr = 4;   // per all-queued record: its chain sums in 4 candidate binades (k_sat_durations)
+#ifndef COLO_SAT_HDR
+#define COLO_SAT_HDR 4
+#endif
+constexpr int kSatHdr = COLO_SAT_HDR;  // per all-queued record: its chain sums in kSatHdr candidate binades (k_sat_durations)
 #ifndef COLO_REPLAY_BLOCKS
 #define COLO_REPLAY_BLOCKS 5
 #endif
@@ -83,6 +86,14 @@ struct alignas(16) SatRec {
     double alast;         // the batch's last arrival (the fast path needs alast <= T)
     uint64_t need;        // sum of the members' serving memory (engine.hpp:297-306)
 };
+
+// the record's chain sum for binade offset c (0 <= c < kSatHdr)
+__device__ __forceinline__ uint64_t rec_R(const SatRec& x, int c) {
+    uint64_t r = x.R[0];
+#pragma unroll
+    for (int i = 1; i < kSatHdr; ++i) r = c == i ? x.R[i] : r;
+    return r;
+}
 
 struct SpecOut {
     uint64_t exit_head;
@@ -512,7 +523,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                     const double al = x.dev == d ? x.alast : 0.0;
                     if (P.dbg && lane == 0) atomicAdd(P.dbg + 3, 1ull);
                     {  // the windows after that: into L2
-                        const char* q = reinterpret_cast<const char*>(P.sat_recs + r + 64) + lane * 160;
+                        const char* q = reinterpret_cast<const char*>(P.sat_recs + r + 64) + lane * 2 * sizeof(SatRec);
                         if (r + 128 < P.sat_nrec) asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
                     }
                     // The window in one step: while T stays in its binade e every
@@ -533,7 +544,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                                  static_cast<uint64_t>(x.start) == (lane == 0 ? head : static_cast<uint64_t>(pend)) &&
                                  x.start < stop && x.start < N;
                         const int c = eT - binade_of(al);
-                        const uint64_t Rc = c == 0 ? x.R[0] : c == 1 ? x.R[1] : c == 2 ? x.R[2] : x.R[3];
+                        const uint64_t Rc = rec_R(x, c);
                         v = v && c >= 0 && c < kSatHdr && Rc != ~0ull;
                         uint64_t rp = 0;
                         v = v && rn_units(x.pre, sc, rp);
@@ -590,7 +601,7 @@ __device__ void run_batches(const ReplayParams& P, uint32_t d, uint64_t& head, d
                         double now = (T + 0.0) + pre;
                         const bool rng = K <= 128 && now >= 0x1p-190 && now <= 0x1p190 && alast >= 0x1p-190;
                         const int c = rng ? binade_of(now) - binade_of(alast) : -1;
-                        const uint64_t Rc = c == 0 ? x.R[0] : c == 1 ? x.R[1] : c == 2 ? x.R[2] : x.R[3];
+                        const uint64_t Rc = rec_R(x, c);
                         const uint64_t R = __shfl_sync(FULL, Rc, l);
                         const uint64_t nbits = static_cast<uint64_t>(__double_as_longlong(now));
                         const uint64_t mnow = (nbits & ((1ull << 52) - 1)) | (1ull << 52);
