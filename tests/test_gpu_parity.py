@@ -169,6 +169,23 @@ def test_decide_exact_random_vs_oracle(ctx, orc):
             assert (u32(cs.decide_exact(ctx, m, G, cs.TrainingMode(cpa), dt)) == orc.decide_exact(om, OG, cpa, t)).all()
 
 
+def test_decide_exact_fast_range_vs_oracle(ctx, orc):
+    """Values below the shared-memory tables (the branch-free fast path of
+    k_decide_exact) and the C5 bench's own question stream, 2M tuples each,
+    against the oracle in both modes."""
+    rng = np.random.default_rng(29)
+    for mn, (m, om) in MODELS.items():
+        L = int(om.num_layers)
+        for t in (random_tuples(rng, 2_000_003, L, hi=16_384),
+                  cs.synth_tuples(ctx, 2_000_000, L, 77).cpu().numpy().view(TUPLE_DTYPE).reshape(-1)):
+            dt = to_dev_tuples(t)
+            for cpa in (0, 1):
+                got = u32(cs.decide_exact(ctx, m, G, cs.TrainingMode(cpa), dt))
+                want = orc.decide_exact(om, OG, cpa, t)
+                bad = np.nonzero(got != want)[0]
+                assert bad.size == 0, (mn, cpa, t[bad[:3]], got[bad[:3]], want[bad[:3]])
+
+
 def test_decide_exact_quotient_edges(ctx, orc):
     """The divide-free exact path (fp32 quotient estimate + u64 correction,
     per-cached hedge thresholds) against the oracle where the ceil-divide of
