@@ -165,18 +165,21 @@ __global__ void __launch_bounds__(kThreads) k_decide(const __grid_constant__ Dec
     if (COUNT) flush_warp_counters(cnt, P.counters);
 }
 
-// Sweep-size grids whose byte cells exceed shared memory (C5 step 50: 161 x
-// 160 x 10 = 257,600 cells): the cells are packed five 6-bit codes per word
-// (codes are 0, 1 or 2 + n <= L + 2 < 64) into 206 KB of shared memory, built
-// by each CTA from the byte cells, so every lookup stays on the SM instead of
-// gathering through L1/L2.  The stream bit of each cached bucket (cell
-// (ci, 0, 0)) gets a byte table of its own: those cells sit I*B apart, which
-// would put a warp's packed-word reads in a few banks.  One 1024-thread CTA per
-// SM streams the tuples with four loads in flight per thread; the
-// composition is compose32_fast's.
+// Tuple-stream decisions on grids with the fast composition (every C5 grid,
+// up to the sweep-size ones whose byte cells exceed shared memory -- step 50:
+// 161 x 160 x 10 = 257,600 cells): the cells are packed five 6-bit codes per
+// word (codes are 0, 1 or 2 + n <= L + 2 < 64) into at most 206 KB of shared
+// memory, copied by one bulk copy from the map set's prebuilt image, so every
+// lookup stays on the SM instead of gathering through L1/L2.  The stream bit
+// of each cached bucket (cell (ci, 0, 0)) gets a byte table of its own: those
+// cells sit I*B apart, which would put a warp's packed-word reads in a few
+// banks.  One 1024-thread CTA per SM streams the tuples with six loads in
+// flight per thread; the composition is compose32_fast's.  It beats the TMA
+// pipeline below at every C5 step (step 250: 2.74e11 vs 2.52e11/s), so the
+// TMA kernel is left to grids without the fast composition.
 constexpr int kPackThreads = 1024;
 #ifndef COLO_PACK_FROM
-#define COLO_PACK_FROM (32 * 1024)
+#define COLO_PACK_FROM 0  // byte-cell tables above this size take the packed kernel
 #endif
 constexpr size_t kPackFrom = COLO_PACK_FROM;
 #ifndef COLO_PACK_U
